@@ -1,0 +1,84 @@
+"""ctypes binding of ``libspecrollout_b200.so`` (declared in
+``include/specrollout_b200.h``).
+
+The library is the only compute path: if it is missing, or no CUDA device is
+visible, :func:`lib` raises :class:`DeviceError` -- there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from .errors import ConfigError, DeviceError
+
+LIB_PATH = Path(__file__).resolve().parent / "libspecrollout_b200.so"
+
+_i32, _i64, _u32, _dbl, _vp = (ctypes.c_int, ctypes.c_int64, ctypes.c_uint32,
+                               ctypes.c_double, ctypes.c_void_p)
+
+# name -> argument types (all return int status unless listed in _RESTYPES)
+SIGNATURES: dict[str, list] = {
+    "sr_version": [],
+    "sr_last_error": [],
+    "sr_device_sm_count": [],
+    "sr_keyed_tokens": [_i32, _vp, _vp, _i32, _i64, _i32, _vp, _vp],
+    "sr_keyed_uniforms": [_i32, _vp, _vp, _i32, _i32, _vp, _vp],
+    "sr_verify_windows": [_i32, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _i32,
+                          _vp, _vp, _vp, _vp],
+    "sr_ngram_propose": [_i32, _vp, _i64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
+}
+_RESTYPES = {"sr_last_error": ctypes.c_char_p}
+
+_lib = None
+
+
+def load(path: os.PathLike | None = None) -> ctypes.CDLL:
+    """Load the shared library and bind every declared symbol (no GPU needed)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path is not None else LIB_PATH
+    if not p.exists():
+        raise DeviceError(
+            f"CUDA extension not built: {p} is missing "
+            "(run `python -m paper_2511_16193_b200.build`)")
+    handle = ctypes.CDLL(str(p))
+    for name, argtypes in SIGNATURES.items():
+        fn = getattr(handle, name)
+        fn.argtypes = argtypes
+        fn.restype = _RESTYPES.get(name, ctypes.c_int)
+    if path is None:
+        _lib = handle
+    return handle
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded library, after checking that a CUDA device is usable."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device visible: the B200 rollout path needs a GPU")
+    return load()
+
+
+def check(status: int, what: str) -> None:
+    if status == 0:
+        return
+    msg = load().sr_last_error().decode(errors="replace")
+    if status == 2:
+        raise ConfigError(f"{what}: {msg}")
+    raise DeviceError(f"{what}: {msg} (status {status})")
+
+
+def stream_handle(stream=None) -> int:
+    """cudaStream_t of ``stream`` (default: torch's current stream)."""
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def ptr(t) -> int:
+    return t.data_ptr()
