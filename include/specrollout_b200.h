@@ -100,6 +100,21 @@ int sr_ngram_propose(int batch, const int32_t* tokens, int64_t stride, const int
                      int min_n, int max_n, int k, int32_t* out_draft, int32_t* out_ndraft,
                      int64_t* scratch, sr_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * K1 building block: C = A[M,K] . W[N,K]^T with a fused epilogue (the
+ * projections of the target model's verification forward; no reference
+ * counterpart -- the reference has no model).
+ *   dtype 1: bf16 A/W on tcgen05 tensor cores (TMA + TMEM), bn = 128|256|0
+ *   dtype 0: fp32 A/W on CUDA cores (parity path), bn ignored
+ * epilogue 0: C = acc + bias (bf16; f32 when dtype 0)
+ *          1: C(f32) += acc                      (residual stream)
+ *          2: C[M, N/2] = silu(gate) * up, W rows interleaved per 32:
+ *             16 gate rows then the 16 matching up rows
+ *          3: C(f32) = acc + bias                (logits)
+ * ------------------------------------------------------------------------- */
+int sr_gemm(int dtype, int M, int N, int K, const void* A, int lda, const void* W, int ldw,
+            void* C, int ldc, int epilogue, const float* bias, int bn, sr_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

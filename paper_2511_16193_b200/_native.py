@@ -28,6 +28,7 @@ SIGNATURES: dict[str, list] = {
     "sr_verify_windows": [_i32, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _i32,
                           _vp, _vp, _vp, _vp],
     "sr_ngram_propose": [_i32, _vp, _i64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
+    "sr_gemm": [_i32, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _i32, _vp, _i32, _vp],
 }
 _RESTYPES = {"sr_last_error": ctypes.c_char_p}
 

@@ -1,0 +1,438 @@
+// K1: verify-forward GEMMs on the 5th-gen tensor cores.
+//
+// The target model's verification forward over B prompts x N drafters x
+// (k+1) positions is a dense contraction of the M verify
+// rows with every weight matrix.  This kernel is a persistent,
+// warp-specialized tcgen05 GEMM:
+//
+//   warp 0      TMA producer: 128x64 activation tile + BNx64 weight tile per
+//               stage into 128B-swizzled smem, mbarrier expect_tx.
+//   warp 1      TMEM owner + MMA issuer: one thread issues
+//               tcgen05.mma.cta_group::1.kind::f16 (M=128, N=BN, K=16) x4 per
+//               stage into a double-buffered fp32 TMEM accumulator and
+//               commits smem slots / finished accumulators to mbarriers.
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> registers -> fused
+//               bias / residual-add / SwiGLU / cast -> global.
+//
+// Tiles are walked M-fastest so the CTAs resident at once share weight
+// tiles through L2 (weights are the dominant HBM stream at small M).  The
+// accumulation order over K is fixed by the tile config, which depends only
+// on (N, K): a row's result is independent of M and of its position in the
+// batch, which makes speculative verify and plain decode bit-identical.
+#include "common.cuh"
+#include "gemm.cuh"
+#include "sm100.cuh"
+
+#include <cudaTypedefs.h>
+
+namespace sr {
+
+namespace {
+
+constexpr int kBM = 128, kBK = 64;
+constexpr int kThreads = 192;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr uint32_t kABytes = kBM * kBK * 2;
+  static constexpr uint32_t kBBytes = BN * kBK * 2;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kTmemCols = 2 * BN;  // two accumulator buffers
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * kStageBytes + 256;
+};
+
+__device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+
+// Epilogue for 32 consecutive accumulator columns [col, col+32) of one row.
+template <int EPI>
+__device__ __forceinline__ void epilogue32(const uint32_t (&v)[32], int row, int col, int M,
+                                           int N, void* C, int ldc, const float* bias) {
+  if (row >= M) return;
+  float f[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+  const bool full = col + 32 <= N;
+  if constexpr (EPI == kEpiStoreBf16 || EPI == kEpiStoreF32) {
+    if (bias != nullptr) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) f[i] += (col + i < N) ? bias[col + i] : 0.0f;
+    }
+  }
+  if constexpr (EPI == kEpiStoreBf16) {
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)row * ldc + col;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack_bf16(f[8 * q + 0], f[8 * q + 1]);
+        w.y = pack_bf16(f[8 * q + 2], f[8 * q + 3]);
+        w.z = pack_bf16(f[8 * q + 4], f[8 * q + 5]);
+        w.w = pack_bf16(f[8 * q + 6], f[8 * q + 7]);
+        reinterpret_cast<uint4*>(out)[q] = w;
+      }
+    } else {
+      for (int i = 0; i < 32 && col + i < N; ++i) out[i] = __float2bfloat16_rn(f[i]);
+    }
+  } else if constexpr (EPI == kEpiStoreF32) {
+    float* out = reinterpret_cast<float*>(C) + (int64_t)row * ldc + col;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        reinterpret_cast<float4*>(out)[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+    } else {
+      for (int i = 0; i < 32 && col + i < N; ++i) out[i] = f[i];
+    }
+  } else if constexpr (EPI == kEpiResidualF32) {
+    float* out = reinterpret_cast<float*>(C) + (int64_t)row * ldc + col;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 r = reinterpret_cast<float4*>(out)[q];
+        r.x += f[4 * q]; r.y += f[4 * q + 1]; r.z += f[4 * q + 2]; r.w += f[4 * q + 3];
+        reinterpret_cast<float4*>(out)[q] = r;
+      }
+    } else {
+      for (int i = 0; i < 32 && col + i < N; ++i) out[i] += f[i];
+    }
+  } else if constexpr (EPI == kEpiSwiGLU) {
+    // columns [col, col+16) are gate, [col+16, col+32) the matching up rows
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)row * ldc + col / 2;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        uint4 w;
+        w.x = pack_bf16(silu(f[8 * q + 0]) * f[16 + 8 * q + 0], silu(f[8 * q + 1]) * f[16 + 8 * q + 1]);
+        w.y = pack_bf16(silu(f[8 * q + 2]) * f[16 + 8 * q + 2], silu(f[8 * q + 3]) * f[16 + 8 * q + 3]);
+        w.z = pack_bf16(silu(f[8 * q + 4]) * f[16 + 8 * q + 4], silu(f[8 * q + 5]) * f[16 + 8 * q + 5]);
+        w.w = pack_bf16(silu(f[8 * q + 6]) * f[16 + 8 * q + 6], silu(f[8 * q + 7]) * f[16 + 8 * q + 7]);
+        reinterpret_cast<uint4*>(out)[q] = w;
+      }
+    }
+  }
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    int M, int N, int K, void* C, int ldc, const float* __restrict__ bias) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_m = (M + kBM - 1) / kBM, num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch_desc(&tmA);
+    sm100::tma_prefetch_desc(&tmB);
+    for (int s = 0; s < S; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      sm100::mbar_init(&tfull[a], 1);
+      sm100::mbar_init(&tempty[a], 128);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_blk = tile % num_m, n_blk = tile / num_m;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          sm100::mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+          sm100::tma_load_2d(sA + stage * Cfg::kABytes, &tmA, &full[stage], kb * kBK, m_blk * kBM,
+                             sm100::kEvictLast);
+          sm100::tma_load_2d(sB + stage * Cfg::kBBytes, &tmB, &full[stage], kb * kBK, n_blk * BN,
+                             sm100::kEvictNormal);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = sm100::umma_idesc_bf16(kBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          sm100::mbar_wait(&full[stage], phase);
+          sm100::tc_fence_after();
+          const uint32_t a0 = sm100::smem_u32(sA + stage * Cfg::kABytes);
+          const uint32_t b0 = sm100::smem_u32(sB + stage * Cfg::kBBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            sm100::umma_bf16(d, sm100::umma_desc_sw128(a0 + k * 32), sm100::umma_desc_sw128(b0 + k * 32),
+                             idesc, (kb | k) != 0);
+          }
+          sm100::umma_commit(&empty[stage]);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+        sm100::umma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int m_blk = tile % num_m, n_blk = tile / num_m;
+      sm100::mbar_wait(&tfull[acc], acc_phase);
+      sm100::tc_fence_after();
+      const int row = m_blk * kBM + quad * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        sm100::tmem_ld_32x32b_x32(taddr + c * 32, v);
+        sm100::tmem_ld_wait();
+        const int col = n_blk * BN + c * 32;
+        if (col < N) epilogue32<EPI>(v, row, col, M, N, C, ldc, bias);
+      }
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+int g_num_sms = 0;
+
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <int BN, int EPI>
+int launch_typed(const GemmPlan& p, cudaStream_t stream) {
+  using Cfg = GemmCfg<BN>;
+  auto kern = gemm_tcgen05_kernel<BN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SR_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
+    attr_set = true;
+  }
+  const int tiles = ((p.M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, kThreads, Cfg::kSmem, stream>>>(p.a, p.b, p.M, p.N, p.K, p.c, p.ldc, p.bias);
+  return check_launch("gemm_tcgen05_kernel");
+}
+
+template <int BN>
+int launch_bn(const GemmPlan& p, cudaStream_t stream) {
+  switch (p.epi) {
+    case kEpiStoreBf16: return launch_typed<BN, kEpiStoreBf16>(p, stream);
+    case kEpiResidualF32: return launch_typed<BN, kEpiResidualF32>(p, stream);
+    case kEpiSwiGLU: return launch_typed<BN, kEpiSwiGLU>(p, stream);
+    case kEpiStoreF32: return launch_typed<BN, kEpiStoreF32>(p, stream);
+  }
+  return config_error("unknown epilogue");
+}
+
+}  // namespace
+
+int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                   uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+  auto enc = tmap_encoder();
+  if (enc == nullptr) {
+    set_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
+    return SR_ERR_RUNTIME;
+  }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu stride=%llu", (int)r,
+              (unsigned long long)inner, (unsigned long long)outer, (unsigned long long)row_bytes);
+    return SR_ERR_CONFIG;
+  }
+  return SR_OK;
+}
+
+int gemm_bf16_plan(GemmPlan* p, int M, int N, int K, const __nv_bfloat16* A, int lda,
+                   const __nv_bfloat16* W, int ldw, void* C, int ldc, int epi,
+                   const float* bias, int bn) {
+  SR_REQUIRE(M >= 0 && N > 0 && K > 0, "bad GEMM shape");
+  SR_REQUIRE(lda % 8 == 0 && ldw % 8 == 0 && lda >= K && ldw >= K, "lda/ldw must be >= K and multiples of 8");
+  SR_REQUIRE(ldc % 8 == 0, "ldc must be a multiple of 8");
+  SR_REQUIRE(((uintptr_t)A & 15) == 0 && ((uintptr_t)W & 15) == 0 && ((uintptr_t)C & 15) == 0,
+             "A, W, C must be 16-byte aligned");
+  if (bn == 0) bn = (N % 256 == 0 && N >= 1024) ? 256 : 128;
+  SR_REQUIRE(bn == 128 || bn == 256, "bn must be 128 or 256");
+  SR_REQUIRE(epi != kEpiSwiGLU || N % 32 == 0, "SwiGLU needs N % 32 == 0");
+  p->M = M; p->N = N; p->K = K; p->bn = bn; p->epi = epi; p->c = C; p->ldc = ldc; p->bias = bias;
+  const int mrows = M > 0 ? M : 1;
+  int rc = make_tmap_bf16(&p->a, A, (uint64_t)K, (uint64_t)mrows, (uint64_t)lda * 2, kBK, kBM);
+  if (rc) return rc;
+  return make_tmap_bf16(&p->b, W, (uint64_t)K, (uint64_t)N, (uint64_t)ldw * 2, kBK, bn);
+}
+
+int gemm_bf16_launch(const GemmPlan& p, cudaStream_t stream) {
+  if (p.M == 0) return SR_OK;
+  return p.bn == 256 ? launch_bn<256>(p, stream) : launch_bn<128>(p, stream);
+}
+
+// ---------------------------------------------------------------------------
+// fp32 parity GEMM (CUDA cores).  64x64 tile, 256 threads, 4x4 per thread,
+// k ascending in steps of 16: deterministic and batch invariant.
+
+namespace {
+
+constexpr int kFT = 64, kFK = 16;
+
+template <int EPI>
+__global__ void __launch_bounds__(256)
+gemm_f32_kernel(int M, int N, int K, const float* __restrict__ A, int lda,
+                const float* __restrict__ W, int ldw, float* __restrict__ C, int ldc,
+                const float* __restrict__ bias) {
+  __shared__ float sa[kFK][kFT + 4];
+  __shared__ float sw[kFK][kFT + 4];
+  const int m0 = blockIdx.y * kFT, n0 = blockIdx.x * kFT;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += kFK) {
+    for (int i = threadIdx.x; i < kFT * kFK; i += 256) {
+      const int r = i / kFK, kk = i % kFK;
+      sa[kk][r] = (m0 + r < M && k0 + kk < K) ? A[(int64_t)(m0 + r) * lda + k0 + kk] : 0.0f;
+      sw[kk][r] = (n0 + r < N && k0 + kk < K) ? W[(int64_t)(n0 + r) * ldw + k0 + kk] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kFK; ++kk) {
+      float a[4], w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { a[i] = sa[kk][ty * 4 + i]; w[i] = sw[kk][tx * 4 + i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], w[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  // stage the 64x64 tile so the SwiGLU epilogue can pair gate column c with
+  // up column c+16 (held by another thread)
+  __shared__ float tile[kFT][kFT + 1];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) tile[ty * 4 + i][tx * 4 + j] = acc[i][j];
+  __syncthreads();
+  for (int e = threadIdx.x; e < kFT * kFT; e += 256) {
+    const int r = e / kFT, cidx = e % kFT;
+    const int row = m0 + r, col = n0 + cidx;
+    if (row >= M || col >= N) continue;
+    const float v = tile[r][cidx];
+    if constexpr (EPI == kEpiSwiGLU) {
+      if ((col & 31) >= 16) continue;
+      const float up = tile[r][cidx + 16];
+      C[(int64_t)row * ldc + (col >> 5) * 16 + (col & 15)] = v / (1.0f + expf(-v)) * up;
+    } else if constexpr (EPI == kEpiResidualF32) {
+      C[(int64_t)row * ldc + col] += v;
+    } else {
+      C[(int64_t)row * ldc + col] = v + (bias != nullptr ? bias[col] : 0.0f);
+    }
+  }
+}
+
+}  // namespace
+
+int gemm_f32(int M, int N, int K, const float* A, int lda, const float* W, int ldw, void* C,
+             int ldc, int epi, const float* bias, cudaStream_t stream) {
+  SR_REQUIRE(M >= 0 && N > 0 && K > 0, "bad GEMM shape");
+  if (M == 0) return SR_OK;
+  dim3 grid((N + kFT - 1) / kFT, (M + kFT - 1) / kFT);
+  float* c = reinterpret_cast<float*>(C);
+  switch (epi) {
+    case kEpiStoreBf16:
+    case kEpiStoreF32:
+      gemm_f32_kernel<kEpiStoreF32><<<grid, 256, 0, stream>>>(M, N, K, A, lda, W, ldw, c, ldc, bias);
+      break;
+    case kEpiResidualF32:
+      gemm_f32_kernel<kEpiResidualF32><<<grid, 256, 0, stream>>>(M, N, K, A, lda, W, ldw, c, ldc, bias);
+      break;
+    case kEpiSwiGLU:
+      gemm_f32_kernel<kEpiSwiGLU><<<grid, 256, 0, stream>>>(M, N, K, A, lda, W, ldw, c, ldc, bias);
+      break;
+    default:
+      return config_error("unknown epilogue");
+  }
+  return check_launch("gemm_f32_kernel");
+}
+
+}  // namespace sr
+
+extern "C" int sr_gemm(int dtype, int M, int N, int K, const void* A, int lda, const void* W,
+                       int ldw, void* C, int ldc, int epilogue, const float* bias, int bn,
+                       sr_stream_t stream) {
+  if (dtype == 1) {
+    sr::GemmPlan plan;
+    int rc = sr::gemm_bf16_plan(&plan, M, N, K, reinterpret_cast<const __nv_bfloat16*>(A), lda,
+                                reinterpret_cast<const __nv_bfloat16*>(W), ldw, C, ldc, epilogue,
+                                bias, bn);
+    if (rc) return rc;
+    return sr::gemm_bf16_launch(plan, (cudaStream_t)stream);
+  }
+  SR_REQUIRE(dtype == 0, "dtype must be 0 (f32) or 1 (bf16)");
+  return sr::gemm_f32(M, N, K, reinterpret_cast<const float*>(A), lda,
+                      reinterpret_cast<const float*>(W), ldw, C, ldc, epilogue, bias,
+                      (cudaStream_t)stream);
+}

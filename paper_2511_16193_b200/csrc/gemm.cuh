@@ -1,0 +1,39 @@
+// K1 verify GEMMs: D[M,N] = A[M,K] . W[N,K]^T with fused epilogues.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+
+namespace sr {
+
+enum GemmEpilogue : int {
+  kEpiStoreBf16 = 0,    // C bf16 = acc (+ bias)
+  kEpiResidualF32 = 1,  // C f32 += acc            (residual stream)
+  kEpiSwiGLU = 2,       // C bf16 [M, N/2] = silu(gate) * up; W rows interleaved
+                        //   in blocks of 32: 16 gate rows then 16 up rows
+  kEpiStoreF32 = 3,     // C f32 = acc (+ bias)     (logits)
+};
+
+// Host: encode a 2D bf16 tensor map (inner dim contiguous) with 128B swizzle.
+int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                   uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer);
+
+struct GemmPlan {
+  CUtensorMap a, b;
+  int M, N, K, bn, epi;
+  void* c;
+  int ldc;
+  const float* bias;
+};
+
+// Build a plan (tensor maps) once; launch many times (graph-capturable).
+int gemm_bf16_plan(GemmPlan* plan, int M, int N, int K, const __nv_bfloat16* A, int lda,
+                   const __nv_bfloat16* W, int ldw, void* C, int ldc, int epi,
+                   const float* bias, int bn);
+int gemm_bf16_launch(const GemmPlan& plan, cudaStream_t stream);
+
+// fp32 parity path (CUDA cores, fixed k order): same epilogues, f32 activations.
+int gemm_f32(int M, int N, int K, const float* A, int lda, const float* W, int ldw, void* C,
+             int ldc, int epi, const float* bias, cudaStream_t stream);
+
+}  // namespace sr

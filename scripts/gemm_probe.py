@@ -1,0 +1,70 @@
+"""Time the tcgen05 GEMM on the verify-forward shapes against cuBLAS (torch).
+
+    python scripts/gemm_probe.py [--m 1280]
+"""
+
+from __future__ import annotations
+
+import argparse
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+from paper_2511_16193_b200 import _native  # noqa: E402
+
+SHAPES_15B = {  # name: (N, K, epilogue)
+    "qkv": (2048, 1536, 0), "o": (1536, 1536, 1), "gate_up": (17920, 1536, 2),
+    "down": (1536, 8960, 1), "lm_head": (151936, 1536, 3),
+}
+
+
+def time_it(fn, iters=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--m", type=int, default=1280)
+    args = ap.parse_args()
+    lib = _native.lib()
+    M = args.m
+    st = _native.stream_handle()
+    for name, (N, K, epi) in SHAPES_15B.items():
+        A = torch.randn(M, K, device="cuda").bfloat16()
+        W = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
+        if epi == 1:
+            C = torch.zeros(M, N, device="cuda")
+        elif epi == 2:
+            C = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+        elif epi == 3:
+            C = torch.empty(M, N, device="cuda")
+        else:
+            C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        for bn in (128, 256):
+            if N % bn and bn == 256:
+                continue
+
+            def run():
+                _native.check(lib.sr_gemm(1, M, N, K, A.data_ptr(), K, W.data_ptr(), K,
+                                          C.data_ptr(), C.stride(0), epi, None, bn, st), "gemm")
+            ms = time_it(run)
+            tf = 2 * M * N * K / ms / 1e9
+            print(f"{name:8s} M={M} N={N} K={K} bn={bn}: {ms*1e3:8.1f} us  {tf:7.1f} TFLOP/s")
+        ms = time_it(lambda: torch.matmul(A, W.t()))
+        print(f"{name:8s} cuBLAS: {ms*1e3:8.1f} us  {2*M*N*K/ms/1e9:7.1f} TFLOP/s")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,105 @@
+"""GPU numerics: the tcgen05 bf16 GEMM and the fp32 CUDA-core GEMM vs a torch
+fp32 reference of the same op, plus batch invariance (row results do not
+depend on M)."""
+
+from __future__ import annotations
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+EPI_STORE, EPI_RESID, EPI_SWIGLU, EPI_F32 = 0, 1, 2, 3
+
+
+def sr_gemm(A, W, C, epi, bias=None, bn=0):
+    from paper_2511_16193_b200 import _native
+
+    lib = _native.lib()
+    dtype = 1 if A.dtype == torch.bfloat16 else 0
+    M, K = A.shape
+    N = W.shape[0]
+    _native.check(lib.sr_gemm(dtype, M, N, K, A.data_ptr(), A.stride(0), W.data_ptr(),
+                              W.stride(0), C.data_ptr(), C.stride(0), epi,
+                              bias.data_ptr() if bias is not None else None, bn,
+                              _native.stream_handle()), "sr_gemm")
+    torch.cuda.synchronize()
+
+
+def ref(A, W, bias=None):
+    out = A.float() @ W.float().t()
+    return out + bias if bias is not None else out
+
+
+def swiglu_ref(acc):
+    M, N = acc.shape
+    blocks = acc.view(M, N // 32, 2, 16)
+    g, u = blocks[:, :, 0, :], blocks[:, :, 1, :]
+    return (torch.nn.functional.silu(g) * u).reshape(M, N // 2)
+
+
+SHAPES = [(1, 128, 64), (5, 256, 128), (127, 384, 192), (128, 256, 1536),
+          (300, 1536, 1536), (1280, 2048, 1536), (77, 1000, 96), (640, 512, 8960)]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("bn", [128, 256])
+def test_bf16_store_and_f32(M, N, K, bn):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g)
+    exp = ref(A, W, bias)
+    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    sr_gemm(A, W, C, EPI_STORE, bias, bn)
+    torch.testing.assert_close(C.float(), exp, rtol=1e-2, atol=1e-2)
+    C32 = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    sr_gemm(A, W, C32, EPI_F32, bias, bn)
+    torch.testing.assert_close(C32, exp, rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.parametrize("M,N,K", [(5, 256, 128), (300, 1536, 1536), (1280, 1536, 8960)])
+def test_bf16_residual_and_swiglu(M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    R = torch.randn(M, N, device="cuda", generator=g)
+    C = R.clone()
+    sr_gemm(A, W, C, EPI_RESID)
+    torch.testing.assert_close(C, R + ref(A, W), rtol=1e-4, atol=1e-3)
+    S = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+    sr_gemm(A, W, S, EPI_SWIGLU)
+    torch.testing.assert_close(S.float(), swiglu_ref(ref(A, W)), rtol=1e-2, atol=1e-2)
+
+
+def test_bf16_batch_invariance():
+    # rows computed inside M=1280 are bit-identical to the same rows at M=5
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.randn(1280, 1536, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(2048, 1536, device="cuda", generator=g) * 0.05).bfloat16()
+    big = torch.empty(1280, 2048, device="cuda", dtype=torch.float32)
+    sr_gemm(A, W, big, EPI_F32)
+    for start in (0, 3, 640, 1275):
+        small = torch.empty(5, 2048, device="cuda", dtype=torch.float32)
+        sr_gemm(A[start:start + 5].contiguous(), W, small, EPI_F32)
+        assert torch.equal(small, big[start:start + 5])
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 64, 32), (37, 200, 128), (128, 384, 96)])
+def test_f32_gemm(M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    A = torch.randn(M, K, device="cuda", generator=g)
+    W = torch.randn(N, K, device="cuda", generator=g) * 0.1
+    bias = torch.randn(N, device="cuda", generator=g)
+    exp = A.double() @ W.double().t()
+    C = torch.empty(M, N, device="cuda")
+    sr_gemm(A, W, C, EPI_STORE, bias)
+    torch.testing.assert_close(C.double(), exp + bias.double(), rtol=1e-5, atol=1e-5)
+    R = torch.randn(M, N, device="cuda", generator=g)
+    C = R.clone()
+    sr_gemm(A, W, C, EPI_RESID)
+    torch.testing.assert_close(C.double(), R.double() + exp, rtol=1e-5, atol=1e-5)
+    if N % 32 == 0:
+        S = torch.empty(M, N // 2, device="cuda")
+        sr_gemm(A, W, S, EPI_SWIGLU)
+        torch.testing.assert_close(S.double(), swiglu_ref(exp), rtol=1e-5, atol=1e-5)
