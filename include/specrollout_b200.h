@@ -111,9 +111,116 @@ int sr_ngram_propose(int batch, const int32_t* tokens, int64_t stride, const int
  *          2: C[M, N/2] = silu(gate) * up, W rows interleaved per 32:
  *             16 gate rows then the 16 matching up rows
  *          3: C(f32) = acc + bias                (logits)
+ *          4: (bf16 only) fused vocabulary argmax: per (row, N tile of bn
+ *             columns) C(f32)[M, tiles] = max, aux[M, tiles] = its lowest
+ *             column index; logits never reach HBM
  * ------------------------------------------------------------------------- */
 int sr_gemm(int dtype, int M, int N, int K, const void* A, int lda, const void* W, int ldw,
-            void* C, int ldc, int epilogue, const float* bias, int bn, sr_stream_t stream);
+            void* C, int ldc, int epilogue, const float* bias, int bn, int32_t* aux,
+            sr_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * K1+K2+K6  Verification forward of the target model (Qwen2-style decoder:
+ * RMSNorm, RoPE, GQA with QKV bias, SwiGLU, tied or untied lm_head).  The
+ * reference only *prices* verification (`_Executor._verify_cost`,
+ * sim.py:781-792; `true_token` stands in for the model's output,
+ * sim.py:313-320); this computes the target tokens for real.
+ *
+ * Weights layout (device, `dtype` unless noted f32):
+ *   embed, lm_head [vocab, hidden] (lm_head may alias embed); final_norm f32
+ *   layer_weights: HOST array of layers*7 device pointers, per layer:
+ *     ln1 f32 [hidden]; w_qkv [(q+2kv)*hd, hidden]; b_qkv f32 [(q+2kv)*hd];
+ *     w_o [hidden, q*hd]; ln2 f32 [hidden];
+ *     w_gu [2*inter, hidden], rows interleaved per 32 (16 gate, 16 up);
+ *     w_down [hidden, inter]
+ * KV cache: [layers, num_pages, 2 (K,V), kv_heads, 64, head_dim], paged
+ *   through block_table [max_requests, max_pages_per_req] (int32 page ids).
+ * window_kv: [layers, max_branches, 2, kv_heads, window_max, head_dim] holds
+ *   the in-flight KV of Best-of-N drafter branches >= 1 (branch 0 writes its
+ *   window straight into the paged cache).
+ * ------------------------------------------------------------------------- */
+typedef struct sr_seq_info {
+  int32_t q_start;  /* first token row of the sequence in the batch */
+  int32_t q_len;    /* window positions (k+1 verify, 1 decode, P prefill; 0 = idle) */
+  int32_t request;  /* block_table / token-buffer row */
+  int32_t ctx_len;  /* keys already committed in the paged cache */
+  int32_t branch;   /* -1: KV in place; >= 0: window_kv branch slot */
+  int32_t pad0, pad1, pad2;
+} sr_seq_info;
+
+typedef struct sr_model_desc {
+  int32_t hidden, intermediate, layers, q_heads, kv_heads, head_dim, vocab;
+  int32_t dtype;            /* 0 fp32 (CUDA-core parity path), 1 bf16 (tcgen05) */
+  float rms_eps;
+  int32_t max_pos;          /* rows of rope_cos / rope_sin [max_pos, head_dim/2] f32 */
+  int32_t num_pages, page_size, max_requests, max_pages_per_req;
+  int32_t max_branches, window_max;
+  int32_t max_tokens;       /* token rows per forward */
+  int32_t max_seqs;         /* sequences per forward */
+  int32_t max_key;          /* largest key position any forward touches */
+  int32_t logits_capacity;  /* fp32 logit rows the workspace holds (0 = argmax only) */
+  const void* embed;
+  const void* lm_head;
+  const float* final_norm;
+  const void* const* layer_weights;
+  const float* rope_cos;
+  const float* rope_sin;
+  void* kv_cache;
+  const int32_t* block_table;
+  void* window_kv;
+  void* workspace;
+  uint64_t workspace_bytes;
+} sr_model_desc;
+
+typedef struct sr_forward_args {
+  int32_t num_tokens, num_seqs;
+  int32_t max_q_len;        /* host upper bound of q_len over the sequences */
+  int32_t max_key;          /* host upper bound of ctx_len + q_len - 1 */
+  int32_t output;           /* 0: argmax ids (int32 [rows]) ; 1: fp32 logits [rows, vocab] */
+  int32_t num_logit_rows;   /* rows of logit_rows (ignored when it is NULL) */
+  const int32_t* token_ids; /* [num_tokens] */
+  const int32_t* positions; /* [num_tokens] */
+  const sr_seq_info* seqs;  /* [num_seqs] device */
+  const int32_t* logit_rows;/* optional token rows to project (e.g. last prompt token) */
+  void* out;
+  float* out_val;           /* optional max logit per row (argmax output) */
+} sr_forward_args;
+
+uint64_t sr_model_workspace_bytes(const sr_model_desc* desc);
+int sr_model_create(const sr_model_desc* desc, void** handle);
+int sr_model_destroy(void* handle);
+int sr_model_forward(void* handle, const sr_forward_args* args, sr_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * K3  Acceptance + Best-of-N + write-back (model mode).  Replaces
+ * `_verify_prefix` / `_apply_outcome` / `commit` (sim.py:977-1042, 340-353)
+ * with real tokens, and the Best-of-N first-finisher (sim.py:340-361) with an
+ * in-forward longest-accepted-prefix select over N drafters per request.
+ *
+ * seqs [B*N] (drafter n of request b is sequence b*N+n); token_ids [M] are
+ * the verify inputs (slot j+1 holds draft d_{j+1}); target [M] the target
+ * model's token per row.  Commits into tokens [B, tok_stride] at seq_len,
+ * advances seq_len / gen_len (capped by max_new), and writes outcome
+ * [B*N, 4] = (proposed, accepted, committed, wasted) and bon [B] (winner,
+ * -1 = request inactive).
+ * ------------------------------------------------------------------------- */
+int sr_accept_commit(int num_requests, int num_drafters, const void* seqs, const int32_t* token_ids,
+                     const int32_t* target, int32_t* tokens, int64_t tok_stride, int32_t* seq_len,
+                     int32_t* gen_len, const int32_t* max_new, int bonus_token, int32_t* outcome,
+                     int32_t* bon, sr_stream_t stream);
+
+/* Copy the winning branch's window KV into the paged cache (all layers). */
+int sr_kv_commit(void* model, int num_requests, int num_drafters, const void* seqs,
+                 const int32_t* outcome, const int32_t* bon, sr_stream_t stream);
+
+/* Next verify batch from device state: for drafter n of request b, rows
+ * [(b*N+n)*(k+1), +nd+1) = last committed token then the drafts.  drafts
+ * [N, B, k] / ndraft [N, B] are drafter-major (each drafter kernel writes its
+ * own [B, k] block); both NULL = plain decode. */
+int sr_build_verify_batch(int num_requests, int num_drafters, int k, const int32_t* tokens,
+                          int64_t tok_stride, const int32_t* seq_len, const int32_t* gen_len,
+                          const int32_t* max_new, const int32_t* drafts, const int32_t* ndraft,
+                          int32_t* token_ids, int32_t* positions, void* seqs, sr_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,145 @@
+"""CPU ORACLE (test infrastructure only) for the verification forward.
+
+PyTorch-CPU restatement of the Qwen2-style decoder the GPU path runs
+(paper_2511_16193_b200/csrc/model.cu).  The reference has no model at all --
+its "target token" is a keyed random integer (sim.py:313-320) -- so logits
+parity is UNPINNED by the reference; this oracle is cross-checked against
+transformers' Qwen2ForCausalLM in tests/test_oracle_model.py instead.
+
+Arithmetic (both modes): residual stream fp32; RMSNorm y = x*rsqrt(mean(x^2)+eps)*w;
+RoPE on the NeoX halves with the shared float64->float32 cos/sin tables;
+softmax in fp32.  In "bf16" mode values are rounded to bf16 exactly where the
+GPU stores bf16: normed activations, qkv after bias, rotated q/k, softmax
+probabilities entering P.V, attention output, SwiGLU output.  GEMMs
+accumulate in fp32 (double in "fp32" mode for a tighter reference).
+
+Acceptance semantics for spec decoding follow sim.py:983-1042 (exact match,
+optional bonus token) and vLLM's n-gram proposer (oracle/ngram_oracle.py).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import ngram_oracle
+
+
+class Qwen2Oracle:
+    def __init__(self, shape, weights: dict, dtype: str = "fp32"):
+        from paper_2511_16193_b200.model import rope_tables
+
+        self.s = shape
+        self.bf16 = dtype == "bf16"
+        cast = (lambda t: t.bfloat16().float()) if self.bf16 else (lambda t: t.double())
+        self.acc = torch.float32 if self.bf16 else torch.float64
+        w = weights
+        self.embed = cast(w["embed"])
+        self.lm_head = cast(w["lm_head"])
+        self.final_norm = w["final_norm"].to(self.acc)
+        self.layers = []
+        for L in w["layers"]:
+            self.layers.append({
+                "ln1": L["ln1"].to(self.acc), "ln2": L["ln2"].to(self.acc),
+                "wqkv": cast(torch.cat([L["wq"], L["wk"], L["wv"]], 0)),
+                "bqkv": torch.cat([L["bq"], L["bk"], L["bv"]], 0).to(self.acc),
+                "wo": cast(L["wo"]), "wg": cast(L["wg"]), "wu": cast(L["wu"]), "wd": cast(L["wd"]),
+            })
+        cos, sin = rope_tables(shape, 1 << 14)
+        self.cos = torch.from_numpy(cos).to(self.acc)
+        self.sin = torch.from_numpy(sin).to(self.acc)
+
+    def _r(self, t):
+        return t.bfloat16().to(self.acc) if self.bf16 else t
+
+    def _norm(self, x, w):
+        var = (x * x).mean(-1, keepdim=True)
+        return self._r(x * torch.rsqrt(var + self.s.rms_eps) * w)
+
+    def _rope(self, x, pos):
+        half = self.s.head_dim // 2
+        c, s = self.cos[pos][:, None, :], self.sin[pos][:, None, :]
+        x1, x2 = x[..., :half], x[..., half:]
+        return self._r(torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], -1))
+
+    @torch.no_grad()
+    def logits(self, tokens) -> torch.Tensor:
+        """Causal forward over one full sequence; logits [L, V] (fp32/fp64)."""
+        s = self.s
+        T = len(tokens)
+        pos = torch.arange(T)
+        x = self.embed[torch.as_tensor(tokens, dtype=torch.long)].to(self.acc)
+        nq, nkv, hd = s.q_heads, s.kv_heads, s.head_dim
+        G = nq // nkv
+        mask = torch.triu(torch.ones(T, T, dtype=torch.bool), 1)
+        for L in self.layers:
+            h = self._norm(x, L["ln1"])
+            qkv = self._r(h @ L["wqkv"].t() + L["bqkv"])
+            q = qkv[:, : nq * hd].view(T, nq, hd)
+            k = qkv[:, nq * hd: (nq + nkv) * hd].view(T, nkv, hd)
+            v = qkv[:, (nq + nkv) * hd:].view(T, nkv, hd)
+            q, k = self._rope(q, pos), self._rope(k, pos)
+            k = k.repeat_interleave(G, dim=1)
+            v = v.repeat_interleave(G, dim=1)
+            sc = torch.einsum("qhd,khd->hqk", q, k) / float(np.sqrt(hd))
+            sc = sc.masked_fill(mask, float("-inf"))
+            m = sc.amax(-1, keepdim=True)
+            p = torch.exp(sc - m)
+            l = p.sum(-1, keepdim=True)
+            o = torch.einsum("hqk,khd->qhd", self._r(p), v) / l.permute(1, 0, 2)
+            x = x + self._r(o.reshape(T, nq * hd)) @ L["wo"].t()
+            h = self._norm(x, L["ln2"])
+            g, u = h @ L["wg"].t(), h @ L["wu"].t()
+            act = self._r(g / (1.0 + torch.exp(-g)) * u)
+            x = x + act @ L["wd"].t()
+        h = self._norm(x, self.final_norm)
+        return h @ self.lm_head.t()
+
+    def greedy(self, prompt, max_new: int) -> list[int]:
+        """Plain greedy decode (lowest index on ties)."""
+        seq = list(prompt)
+        out = []
+        for _ in range(max_new):
+            tok = int(torch.argmax(self.logits(seq)[-1]))
+            out.append(tok)
+            seq.append(tok)
+        return out
+
+    def spec_decode(self, prompt, max_new: int, k: int, min_n: int = 1, max_n: int = 3,
+                    bonus: bool = False, max_model_len: int | None = None):
+        """n-gram speculative greedy decode with exact-match verification.
+
+        Returns (output tokens, outcome rows [(proposed, accepted, committed, wasted)]).
+        """
+        seq = list(prompt)
+        out, rows = [], []
+        # first token comes from the prompt forward (prefill)
+        first = int(torch.argmax(self.logits(seq)[-1]))
+        out.append(first)
+        seq.append(first)
+        while len(out) < max_new:
+            remaining = max_new - len(out)
+            d = ngram_oracle.propose(seq, min_n, max_n, k, max_model_len)[: min(k, remaining)]
+            lg = self.logits(seq + d)
+            y = [int(torch.argmax(lg[len(seq) - 1 + j])) for j in range(len(d) + 1)]
+            a = 0
+            while a < len(d) and d[a] == y[a]:
+                a += 1
+            n = len(d)
+            if n == 0:
+                c = 1
+            elif a == n:
+                c = n + (1 if bonus else 0)
+            else:
+                c = a + 1
+            c = min(c, remaining)
+            rows.append((n, a, c, 0 if a == n else max(n - a - 1, 0)))
+            out += y[:c]
+            seq += y[:c]
+        return out, rows
+
+
+def margin(logits_row: torch.Tensor) -> float:
+    """Gap between the top-1 and top-2 logit (tie safety of greedy parity)."""
+    top = torch.topk(logits_row.double(), 2).values
+    return float(top[0] - top[1])

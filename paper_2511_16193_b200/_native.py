@@ -28,9 +28,46 @@ SIGNATURES: dict[str, list] = {
     "sr_verify_windows": [_i32, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _i32,
                           _vp, _vp, _vp, _vp],
     "sr_ngram_propose": [_i32, _vp, _i64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
-    "sr_gemm": [_i32, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _i32, _vp, _i32, _vp],
+    "sr_gemm": [_i32, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _i32, _vp, _i32,
+                _vp, _vp],
+    "sr_model_workspace_bytes": [_vp],
+    "sr_model_create": [_vp, _vp],
+    "sr_model_destroy": [_vp],
+    "sr_model_forward": [_vp, _vp, _vp],
+    "sr_accept_commit": [_i32, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp],
+    "sr_kv_commit": [_vp, _i32, _i32, _vp, _vp, _vp, _vp],
+    "sr_build_verify_batch": [_i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                              _vp, _vp],
 }
-_RESTYPES = {"sr_last_error": ctypes.c_char_p}
+_RESTYPES = {"sr_last_error": ctypes.c_char_p, "sr_model_workspace_bytes": ctypes.c_uint64}
+
+
+class SeqInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("q_start", "q_len", "request", "ctx_len", "branch", "pad0", "pad1", "pad2")]
+
+
+class ModelDesc(ctypes.Structure):
+    """Mirror of ``sr_model_desc`` (include/specrollout_b200.h)."""
+
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("hidden", "intermediate", "layers", "q_heads", "kv_heads", "head_dim", "vocab",
+                 "dtype")] + [("rms_eps", ctypes.c_float)] + [
+        (n, ctypes.c_int32) for n in
+        ("max_pos", "num_pages", "page_size", "max_requests", "max_pages_per_req",
+         "max_branches", "window_max", "max_tokens", "max_seqs", "max_key", "logits_capacity")] + [
+        (n, ctypes.c_void_p) for n in
+        ("embed", "lm_head", "final_norm", "layer_weights", "rope_cos", "rope_sin", "kv_cache",
+         "block_table", "window_kv", "workspace")] + [("workspace_bytes", ctypes.c_uint64)]
+
+
+class ForwardArgs(ctypes.Structure):
+    """Mirror of ``sr_forward_args``."""
+
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("num_tokens", "num_seqs", "max_q_len", "max_key", "output", "num_logit_rows")] + [
+        (n, ctypes.c_void_p) for n in
+        ("token_ids", "positions", "seqs", "logit_rows", "out", "out_val")]
 
 _lib = None
 

@@ -1,0 +1,189 @@
+// K3: acceptance + Best-of-N select + token/KV write-back (model mode), and
+// the device-side builder of the next verify batch.
+//
+// Reference semantics (exact match, sim.py:983-1042): with n drafted tokens
+// d_1..d_n verified by target predictions y_0..y_n, the accepted prefix a is
+// the number of leading j with d_{j+1} == y_j; a full accept commits n tokens
+// (+ y_n when the bonus token is on, sim.py:996-999), a partial accept commits
+// the a accepted tokens plus the corrected token y_a (sim.py:1001-1009); n = 0
+// is a plain decode step that commits y_0 (sim.py:966-975).  With N drafters
+// per prompt (Best-of-N, bon.py:79-139 / sim.py:340-361 first finisher) the
+// drafter with the longest accepted prefix wins, ties to the lowest index
+// (incumbent first).  Everything stays on device: the host
+// reads back only the [B*N, 4] outcome rows.
+#include "common.cuh"
+#include "layers.cuh"
+
+#include <cuda_bf16.h>
+
+namespace sr {
+
+namespace {
+
+__global__ void accept_commit_kernel(int B, int N, const SeqInfo* __restrict__ seqs,
+                                     const int32_t* __restrict__ token_ids,
+                                     const int32_t* __restrict__ target, int32_t* __restrict__ tokens,
+                                     int64_t tok_stride, int32_t* __restrict__ seq_len,
+                                     int32_t* __restrict__ gen_len, const int32_t* __restrict__ max_new,
+                                     int bonus, int32_t* __restrict__ outcome,
+                                     int32_t* __restrict__ bon) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= B) return;
+  const int remaining = max_new[b] - gen_len[b];
+  // per-drafter accepted prefix (lane n handles drafter n)
+  int a = -1, n = 0, qs = 0;
+  if (lane < N) {
+    const SeqInfo sq = seqs[b * N + lane];
+    if (sq.q_len > 0 && remaining > 0) {
+      n = sq.q_len - 1;
+      qs = sq.q_start;
+      a = 0;
+      while (a < n && token_ids[qs + a + 1] == target[qs + a]) ++a;
+    }
+  }
+  // longest accepted prefix, lowest drafter index on ties
+  int best_a = a, best_n = lane < N ? lane : 0x7fffffff;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const int oa = __shfl_xor_sync(0xffffffffu, best_a, o);
+    const int on = __shfl_xor_sync(0xffffffffu, best_n, o);
+    if (oa > best_a || (oa == best_a && on < best_n)) { best_a = oa; best_n = on; }
+  }
+  const int win_n = best_n;
+  const int win_q = __shfl_sync(0xffffffffu, qs, win_n & 31);
+  const int win_len = __shfl_sync(0xffffffffu, n, win_n & 31);
+  int committed = 0;
+  if (best_a >= 0) {
+    if (win_len == 0) committed = 1;
+    else if (best_a == win_len) committed = win_len + (bonus ? 1 : 0);
+    else committed = best_a + 1;
+    committed = min(committed, remaining);
+  }
+  const int base = seq_len[b];
+  for (int i = lane; i < committed; i += 32) tokens[(int64_t)b * tok_stride + base + i] = target[win_q + i];
+  if (lane < N) {
+    int32_t* o = outcome + (int64_t)(b * N + lane) * 4;
+    const bool active = a >= 0;
+    const bool win = active && lane == win_n;
+    o[0] = active ? n : 0;
+    o[1] = active ? a : 0;
+    o[2] = win ? committed : 0;
+    o[3] = !active ? 0 : (win ? (a == n ? 0 : max(n - a - 1, 0)) : n);
+  }
+  if (lane == 0) {
+    bon[b] = best_a >= 0 ? win_n : -1;
+    seq_len[b] = base + committed;
+    gen_len[b] += committed;
+  }
+}
+
+// Copy the winning drafter-branch window KV (slots [0, committed)) into the
+// paged cache at positions [ctx_len, ctx_len + committed), every layer.
+template <typename T>
+__global__ void kv_commit_kernel(int N, const SeqInfo* __restrict__ seqs, const int32_t* __restrict__ outcome,
+                                 const int32_t* __restrict__ bon, KvLayout kv) {
+  const int b = blockIdx.x, layer = blockIdx.y;
+  const int w = bon[b];
+  if (w < 0) return;
+  const SeqInfo sq = seqs[b * N + w];
+  if (sq.branch < 0) return;  // the winner wrote its KV in place
+  const int committed = outcome[(int64_t)(b * N + w) * 4 + 2];
+  const int hd = kv.head_dim, nkv = kv.kv_heads;
+  const T* wbase = reinterpret_cast<const T*>(kv.window) + layer * kv.window_layer_elems() +
+                   (int64_t)sq.branch * 2 * nkv * kv.window_max * hd;
+  T* cbase = reinterpret_cast<T*>(kv.cache) + layer * kv.cache_layer_elems();
+  const int32_t* btab = kv.block_table + (int64_t)sq.request * kv.max_pages;
+  const int per_slot = 2 * nkv * hd;
+  for (int e = threadIdx.x; e < committed * per_slot; e += blockDim.x) {
+    const int j = e / per_slot, r = e % per_slot;
+    const int kvsel = r / (nkv * hd), h = (r / hd) % nkv, d = r % hd;
+    const int pos = sq.ctx_len + j;
+    const int page = btab[pos / kv.page];
+    cbase[(((int64_t)page * 2 + kvsel) * nkv + h) * kv.page * hd + (int64_t)(pos % kv.page) * hd + d] =
+        wbase[((int64_t)kvsel * nkv + h) * kv.window_max * hd + (int64_t)j * hd + d];
+  }
+}
+
+// Next verify batch from device state: drafter n of request b gets rows
+// [s*(k+1), s*(k+1) + nd + 1): the last committed token then its drafts.
+__global__ void build_verify_kernel(int B, int N, int k, const int32_t* __restrict__ tokens, int64_t tok_stride,
+                                    const int32_t* __restrict__ seq_len, const int32_t* __restrict__ gen_len,
+                                    const int32_t* __restrict__ max_new, const int32_t* __restrict__ drafts,
+                                    const int32_t* __restrict__ ndraft, int32_t* __restrict__ token_ids,
+                                    int32_t* __restrict__ positions, SeqInfo* __restrict__ seqs) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= B * N) return;
+  const int b = s / N, n = s % N;
+  const int remaining = max_new[b] - gen_len[b];
+  const int L = seq_len[b];
+  int nd = 0;
+  if (remaining > 0) {
+    nd = drafts != nullptr ? ndraft[n * B + b] : 0;
+    nd = max(0, min(nd, min(k, remaining)));
+  }
+  SeqInfo sq;
+  sq.q_start = s * (k + 1);
+  sq.q_len = remaining > 0 ? nd + 1 : 0;
+  sq.request = b;
+  sq.ctx_len = L - 1;
+  sq.branch = n == 0 ? -1 : b * (N - 1) + (n - 1);
+  sq.pad0 = sq.pad1 = sq.pad2 = 0;
+  seqs[s] = sq;
+  for (int j = 0; j <= k; ++j) {
+    const int row = s * (k + 1) + j;
+    int tok;
+    if (j == 0) tok = tokens[(int64_t)b * tok_stride + L - 1];
+    else if (j <= nd) tok = drafts[((int64_t)n * B + b) * k + j - 1];
+    else tok = 0;
+    token_ids[row] = tok;
+    positions[row] = L - 1 + j;
+  }
+}
+
+}  // namespace
+
+int kv_commit(int B, int N, const SeqInfo* seqs, const int32_t* outcome, const int32_t* bon,
+              const KvLayout& kv, int dtype, cudaStream_t s) {
+  if (B == 0 || N <= 1) return SR_OK;
+  dim3 grid(B, kv.layers);
+  if (dtype == 1)
+    kv_commit_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(N, seqs, outcome, bon, kv);
+  else
+    kv_commit_kernel<float><<<grid, 256, 0, s>>>(N, seqs, outcome, bon, kv);
+  return check_launch("kv_commit_kernel");
+}
+
+}  // namespace sr
+
+extern "C" int sr_accept_commit(int num_requests, int num_drafters, const void* seqs,
+                                const int32_t* token_ids, const int32_t* target, int32_t* tokens,
+                                int64_t tok_stride, int32_t* seq_len, int32_t* gen_len,
+                                const int32_t* max_new, int bonus_token, int32_t* outcome,
+                                int32_t* bon, sr_stream_t stream) {
+  SR_REQUIRE(num_requests >= 0, "negative request count");
+  if (num_requests == 0) return SR_OK;
+  SR_REQUIRE(num_drafters >= 1 && num_drafters <= 32, "num_drafters out of [1, 32]");
+  SR_REQUIRE(seqs && token_ids && target && tokens && seq_len && gen_len && max_new && outcome && bon,
+             "null pointer");
+  sr::accept_commit_kernel<<<sr::ceil_div(num_requests, 8), 256, 0, (cudaStream_t)stream>>>(
+      num_requests, num_drafters, reinterpret_cast<const sr::SeqInfo*>(seqs), token_ids, target, tokens,
+      tok_stride, seq_len, gen_len, max_new, bonus_token, outcome, bon);
+  return sr::check_launch("accept_commit_kernel");
+}
+
+extern "C" int sr_build_verify_batch(int num_requests, int num_drafters, int k, const int32_t* tokens,
+                                     int64_t tok_stride, const int32_t* seq_len, const int32_t* gen_len,
+                                     const int32_t* max_new, const int32_t* drafts, const int32_t* ndraft,
+                                     int32_t* token_ids, int32_t* positions, void* seqs,
+                                     sr_stream_t stream) {
+  SR_REQUIRE(num_requests >= 0 && num_drafters >= 1 && k >= 0, "bad batch shape");
+  if (num_requests == 0) return SR_OK;
+  SR_REQUIRE(tokens && seq_len && gen_len && max_new && token_ids && positions && seqs, "null pointer");
+  SR_REQUIRE(drafts == nullptr || ndraft != nullptr, "drafts without ndraft");
+  const int S = num_requests * num_drafters;
+  sr::build_verify_kernel<<<sr::ceil_div(S, 128), 128, 0, (cudaStream_t)stream>>>(
+      num_requests, num_drafters, k, tokens, tok_stride, seq_len, gen_len, max_new, drafts, ndraft,
+      token_ids, positions, reinterpret_cast<sr::SeqInfo*>(seqs));
+  return sr::check_launch("build_verify_kernel");
+}

@@ -56,6 +56,7 @@ template <int EPI>
 __device__ __forceinline__ void epilogue32(const uint32_t (&v)[32], int row, int col, int M,
                                            int N, void* C, int ldc, const float* bias) {
   if (row >= M) return;
+  if constexpr (EPI == kEpiArgmax) return;  // handled in the tile loop
   float f[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
@@ -122,7 +123,8 @@ __device__ __forceinline__ void epilogue32(const uint32_t (&v)[32], int row, int
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    int M, int N, int K, void* C, int ldc, const float* __restrict__ bias) {
+                    int M, int N, int K, void* C, int ldc, const float* __restrict__ bias,
+                    int32_t* __restrict__ aux) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -214,13 +216,31 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       sm100::tc_fence_after();
       const int row = m_blk * kBM + quad * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      float best = -INFINITY;
+      int best_idx = 0x7fffffff;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t v[32];
         sm100::tmem_ld_32x32b_x32(taddr + c * 32, v);
         sm100::tmem_ld_wait();
         const int col = n_blk * BN + c * 32;
-        if (col < N) epilogue32<EPI>(v, row, col, M, N, C, ldc, bias);
+        if constexpr (EPI == kEpiArgmax) {
+          // strict '>' in column order keeps the lowest index on ties
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float f = __uint_as_float(v[i]);
+            if (col + i < N && f > best) { best = f; best_idx = col + i; }
+          }
+        } else {
+          if (col < N) epilogue32<EPI>(v, row, col, M, N, C, ldc, bias);
+        }
+      }
+      if constexpr (EPI == kEpiArgmax) {
+        if (row < M) {
+          const int tiles_n = (N + BN - 1) / BN;
+          reinterpret_cast<float*>(C)[(int64_t)row * tiles_n + n_blk] = best;
+          aux[(int64_t)row * tiles_n + n_blk] = best_idx;
+        }
       }
       sm100::tc_fence_before();
       sm100::mbar_arrive(&tempty[acc]);
@@ -259,7 +279,7 @@ int num_sms() {
 }
 
 template <int BN, int EPI>
-int launch_typed(const GemmPlan& p, cudaStream_t stream) {
+int launch_typed(const GemmPlan& p, int M, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
   auto kern = gemm_tcgen05_kernel<BN, EPI>;
   static bool attr_set = false;
@@ -267,19 +287,20 @@ int launch_typed(const GemmPlan& p, cudaStream_t stream) {
     SR_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
     attr_set = true;
   }
-  const int tiles = ((p.M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN);
+  const int tiles = ((M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, kThreads, Cfg::kSmem, stream>>>(p.a, p.b, p.M, p.N, p.K, p.c, p.ldc, p.bias);
+  kern<<<grid, kThreads, Cfg::kSmem, stream>>>(p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux);
   return check_launch("gemm_tcgen05_kernel");
 }
 
 template <int BN>
-int launch_bn(const GemmPlan& p, cudaStream_t stream) {
+int launch_bn(const GemmPlan& p, int M, cudaStream_t stream) {
   switch (p.epi) {
-    case kEpiStoreBf16: return launch_typed<BN, kEpiStoreBf16>(p, stream);
-    case kEpiResidualF32: return launch_typed<BN, kEpiResidualF32>(p, stream);
-    case kEpiSwiGLU: return launch_typed<BN, kEpiSwiGLU>(p, stream);
-    case kEpiStoreF32: return launch_typed<BN, kEpiStoreF32>(p, stream);
+    case kEpiStoreBf16: return launch_typed<BN, kEpiStoreBf16>(p, M, stream);
+    case kEpiResidualF32: return launch_typed<BN, kEpiResidualF32>(p, M, stream);
+    case kEpiSwiGLU: return launch_typed<BN, kEpiSwiGLU>(p, M, stream);
+    case kEpiStoreF32: return launch_typed<BN, kEpiStoreF32>(p, M, stream);
+    case kEpiArgmax: return launch_typed<BN, kEpiArgmax>(p, M, stream);
   }
   return config_error("unknown epilogue");
 }
@@ -310,26 +331,31 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t 
 
 int gemm_bf16_plan(GemmPlan* p, int M, int N, int K, const __nv_bfloat16* A, int lda,
                    const __nv_bfloat16* W, int ldw, void* C, int ldc, int epi,
-                   const float* bias, int bn) {
+                   const float* bias, int bn, int32_t* aux) {
   SR_REQUIRE(M >= 0 && N > 0 && K > 0, "bad GEMM shape");
+  SR_REQUIRE(epi != kEpiArgmax || aux != nullptr, "argmax epilogue needs an index buffer");
   SR_REQUIRE(lda % 8 == 0 && ldw % 8 == 0 && lda >= K && ldw >= K, "lda/ldw must be >= K and multiples of 8");
-  SR_REQUIRE(ldc % 8 == 0, "ldc must be a multiple of 8");
+  SR_REQUIRE(epi == kEpiArgmax || ldc % 8 == 0, "ldc must be a multiple of 8");
   SR_REQUIRE(((uintptr_t)A & 15) == 0 && ((uintptr_t)W & 15) == 0 && ((uintptr_t)C & 15) == 0,
              "A, W, C must be 16-byte aligned");
-  if (bn == 0) bn = (N % 256 == 0 && N >= 1024) ? 256 : 128;
+  if (bn == 0) bn = N >= 4096 ? 256 : 128;
   SR_REQUIRE(bn == 128 || bn == 256, "bn must be 128 or 256");
   SR_REQUIRE(epi != kEpiSwiGLU || N % 32 == 0, "SwiGLU needs N % 32 == 0");
   p->M = M; p->N = N; p->K = K; p->bn = bn; p->epi = epi; p->c = C; p->ldc = ldc; p->bias = bias;
+  p->aux = aux;
   const int mrows = M > 0 ? M : 1;
   int rc = make_tmap_bf16(&p->a, A, (uint64_t)K, (uint64_t)mrows, (uint64_t)lda * 2, kBK, kBM);
   if (rc) return rc;
   return make_tmap_bf16(&p->b, W, (uint64_t)K, (uint64_t)N, (uint64_t)ldw * 2, kBK, bn);
 }
 
-int gemm_bf16_launch(const GemmPlan& p, cudaStream_t stream) {
-  if (p.M == 0) return SR_OK;
-  return p.bn == 256 ? launch_bn<256>(p, stream) : launch_bn<128>(p, stream);
+int gemm_bf16_launch(const GemmPlan& p, cudaStream_t stream, int m_override) {
+  const int M = m_override >= 0 ? m_override : p.M;
+  if (M == 0) return SR_OK;
+  return p.bn == 256 ? launch_bn<256>(p, M, stream) : launch_bn<128>(p, M, stream);
 }
+
+int gemm_num_n_tiles(int N, int bn) { return (N + bn - 1) / bn; }
 
 // ---------------------------------------------------------------------------
 // fp32 parity GEMM (CUDA cores).  64x64 tile, 256 threads, 4x4 per thread,
@@ -422,16 +448,17 @@ int gemm_f32(int M, int N, int K, const float* A, int lda, const float* W, int l
 
 extern "C" int sr_gemm(int dtype, int M, int N, int K, const void* A, int lda, const void* W,
                        int ldw, void* C, int ldc, int epilogue, const float* bias, int bn,
-                       sr_stream_t stream) {
+                       int32_t* aux, sr_stream_t stream) {
   if (dtype == 1) {
     sr::GemmPlan plan;
     int rc = sr::gemm_bf16_plan(&plan, M, N, K, reinterpret_cast<const __nv_bfloat16*>(A), lda,
                                 reinterpret_cast<const __nv_bfloat16*>(W), ldw, C, ldc, epilogue,
-                                bias, bn);
+                                bias, bn, aux);
     if (rc) return rc;
     return sr::gemm_bf16_launch(plan, (cudaStream_t)stream);
   }
   SR_REQUIRE(dtype == 0, "dtype must be 0 (f32) or 1 (bf16)");
+  SR_REQUIRE(epilogue != sr::kEpiArgmax, "argmax epilogue is bf16-only; use sr_argmax_rows");
   return sr::gemm_f32(M, N, K, reinterpret_cast<const float*>(A), lda,
                       reinterpret_cast<const float*>(W), ldw, C, ldc, epilogue, bias,
                       (cudaStream_t)stream);

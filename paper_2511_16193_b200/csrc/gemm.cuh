@@ -12,6 +12,8 @@ enum GemmEpilogue : int {
   kEpiSwiGLU = 2,       // C bf16 [M, N/2] = silu(gate) * up; W rows interleaved
                         //   in blocks of 32: 16 gate rows then 16 up rows
   kEpiStoreF32 = 3,     // C f32 = acc (+ bias)     (logits)
+  kEpiArgmax = 4,       // per (row, N tile): max value -> C f32 [M, tiles],
+                        //   its lowest column index -> aux [M, tiles]
 };
 
 // Host: encode a 2D bf16 tensor map (inner dim contiguous) with 128B swizzle.
@@ -24,13 +26,17 @@ struct GemmPlan {
   void* c;
   int ldc;
   const float* bias;
+  int32_t* aux;
 };
 
 // Build a plan (tensor maps) once; launch many times (graph-capturable).
 int gemm_bf16_plan(GemmPlan* plan, int M, int N, int K, const __nv_bfloat16* A, int lda,
                    const __nv_bfloat16* W, int ldw, void* C, int ldc, int epi,
-                   const float* bias, int bn);
-int gemm_bf16_launch(const GemmPlan& plan, cudaStream_t stream);
+                   const float* bias, int bn, int32_t* aux = nullptr);
+// Launch with the plan's tensor maps; m_override >= 0 replaces plan.M (rows
+// beyond it are computed from stale memory and discarded).
+int gemm_bf16_launch(const GemmPlan& plan, cudaStream_t stream, int m_override = -1);
+int gemm_num_n_tiles(int N, int bn);
 
 // fp32 parity path (CUDA cores, fixed k order): same epilogues, f32 activations.
 int gemm_f32(int M, int N, int K, const float* A, int lda, const float* W, int ldw, void* C,

@@ -1,0 +1,215 @@
+// K6 helpers of the verify forward; see layers.cuh.
+#include "common.cuh"
+#include "layers.cuh"
+
+namespace sr {
+
+namespace {
+
+template <typename T> __device__ __forceinline__ float to_f(T v);
+template <> __device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T> __device__ __forceinline__ T from_f(float v);
+template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+template <typename T>
+__global__ void embed_kernel(const T* __restrict__ table, const int32_t* __restrict__ ids, int H,
+                             float* __restrict__ x) {
+  const int row = blockIdx.x;
+  const T* src = table + (int64_t)ids[row] * H;
+  float* dst = x + (int64_t)row * H;
+  for (int i = threadIdx.x; i < H; i += blockDim.x) dst[i] = to_f(src[i]);
+}
+
+// One warp per row: lane-strided sum of squares, xor-shuffle tree (fixed
+// order), then scale.  Matches oracle: y = x * rsqrt(mean(x^2) + eps) * w.
+template <typename T>
+__global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ w, int M,
+                               int H, float eps, T* __restrict__ out) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float* xr = x + (int64_t)row * H;
+  float ss = 0.0f;
+  for (int i = lane; i < H; i += 32) ss = fmaf(xr[i], xr[i], ss);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float r = rsqrtf(ss / (float)H + eps);
+  T* orow = out + (int64_t)row * H;
+  for (int i = lane; i < H; i += 32) orow[i] = from_f<T>(xr[i] * r * w[i]);
+}
+
+template <typename T>
+__global__ void rope_scatter_kernel(const T* __restrict__ qkv, const int32_t* __restrict__ positions,
+                                    const SeqInfo* __restrict__ seqs, const float* __restrict__ cos_t,
+                                    const float* __restrict__ sin_t, int nq, int layer, KvLayout kv,
+                                    T* __restrict__ q_out) {
+  const SeqInfo sq = seqs[blockIdx.y];
+  const int j = blockIdx.x;
+  if (j >= sq.q_len) return;
+  const int tok = sq.q_start + j;
+  const int hd = kv.head_dim, half = hd / 2, nkv = kv.kv_heads;
+  const int width = (nq + 2 * nkv) * hd;
+  const int pos = positions[tok];
+  const T* row = qkv + (int64_t)tok * width;
+  const float* cr = cos_t + (int64_t)pos * half;
+  const float* sr_ = sin_t + (int64_t)pos * half;
+
+  T* kdst;
+  T* vdst;
+  int64_t head_stride;  // elements between consecutive kv heads at this slot
+  if (sq.branch < 0) {
+    const int page = kv.block_table[(int64_t)sq.request * kv.max_pages + pos / kv.page];
+    const int slot = pos % kv.page;
+    T* base = reinterpret_cast<T*>(kv.cache) + layer * kv.cache_layer_elems() +
+              (int64_t)page * 2 * nkv * kv.page * hd;
+    kdst = base + (int64_t)slot * hd;
+    vdst = kdst + (int64_t)nkv * kv.page * hd;
+    head_stride = (int64_t)kv.page * hd;
+  } else {
+    T* base = reinterpret_cast<T*>(kv.window) + layer * kv.window_layer_elems() +
+              (int64_t)sq.branch * 2 * nkv * kv.window_max * hd;
+    kdst = base + (int64_t)j * hd;
+    vdst = kdst + (int64_t)nkv * kv.window_max * hd;
+    head_stride = (int64_t)kv.window_max * hd;
+  }
+  // rotate q heads and k heads (NeoX halves), copy v
+  for (int e = threadIdx.x; e < (nq + nkv) * half; e += blockDim.x) {
+    const int h = e / half, i = e % half;
+    const float c = cr[i], s = sr_[i];
+    const float x1 = to_f(row[h * hd + i]), x2 = to_f(row[h * hd + i + half]);
+    const float y1 = x1 * c - x2 * s, y2 = x2 * c + x1 * s;
+    if (h < nq) {
+      T* q = q_out + (int64_t)tok * nq * hd + h * hd;
+      q[i] = from_f<T>(y1);
+      q[i + half] = from_f<T>(y2);
+    } else {
+      T* k = kdst + (h - nq) * head_stride;
+      k[i] = from_f<T>(y1);
+      k[i + half] = from_f<T>(y2);
+    }
+  }
+  for (int e = threadIdx.x; e < nkv * hd; e += blockDim.x) {
+    const int h = e / hd, d = e % hd;
+    vdst[h * head_stride + d] = row[(nq + nkv + h) * hd + d];
+  }
+}
+
+__device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
+  return v > bv || (v == bv && i < bi);
+}
+
+__global__ void argmax_reduce_kernel(const float* __restrict__ pv, const int32_t* __restrict__ pi,
+                                     int M, int tiles, int32_t* __restrict__ ids,
+                                     float* __restrict__ vals) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int t = lane; t < tiles; t += 32) {
+    const float v = pv[(int64_t)row * tiles + t];
+    const int i = pi[(int64_t)row * tiles + t];
+    if (better(v, i, bv, bi)) { bv = v; bi = i; }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float v = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int i = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (better(v, i, bv, bi)) { bv = v; bi = i; }
+  }
+  if (lane == 0) {
+    ids[row] = bi;
+    if (vals) vals[row] = bv;
+  }
+}
+
+__global__ void argmax_rows_kernel(const float* __restrict__ logits, int V, int ld,
+                                   int32_t* __restrict__ ids, float* __restrict__ vals) {
+  const int row = blockIdx.x;
+  const float* r = logits + (int64_t)row * ld;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const float v = r[i];
+    if (better(v, i, bv, bi)) { bv = v; bi = i; }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float v = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int i = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (better(v, i, bv, bi)) { bv = v; bi = i; }
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { sv[w] = bv; si[w] = bi; }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    bv = lane < nw ? sv[lane] : -INFINITY;
+    bi = lane < nw ? si[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float v = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int i = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(v, i, bv, bi)) { bv = v; bi = i; }
+    }
+    if (lane == 0) {
+      ids[row] = bi;
+      if (vals) vals[row] = bv;
+    }
+  }
+}
+
+}  // namespace
+
+template <typename T>
+int embed_rows(const T* table, const int32_t* ids, int M, int H, float* x, cudaStream_t s) {
+  if (M == 0) return SR_OK;
+  embed_kernel<T><<<M, 256, 0, s>>>(table, ids, H, x);
+  return check_launch("embed_kernel");
+}
+
+template <typename T>
+int rmsnorm_rows(const float* x, const float* w, int M, int H, float eps, T* out, cudaStream_t s) {
+  if (M == 0) return SR_OK;
+  rmsnorm_kernel<T><<<ceil_div(M, 8), 256, 0, s>>>(x, w, M, H, eps, out);
+  return check_launch("rmsnorm_kernel");
+}
+
+template <typename T>
+int rope_scatter(const T* qkv, const int32_t* positions, const SeqInfo* seqs, int num_seqs,
+                 int max_q_len, const float* cos_t, const float* sin_t, int nq, int layer,
+                 const KvLayout& kv, T* q_out, cudaStream_t s) {
+  if (num_seqs == 0 || max_q_len == 0) return SR_OK;
+  dim3 grid(max_q_len, num_seqs);
+  rope_scatter_kernel<T><<<grid, 128, 0, s>>>(qkv, positions, seqs, cos_t, sin_t, nq, layer, kv, q_out);
+  return check_launch("rope_scatter_kernel");
+}
+
+int argmax_reduce(const float* pv, const int32_t* pi, int M, int tiles, int32_t* ids, float* vals,
+                  cudaStream_t s) {
+  if (M == 0) return SR_OK;
+  argmax_reduce_kernel<<<ceil_div(M, 8), 256, 0, s>>>(pv, pi, M, tiles, ids, vals);
+  return check_launch("argmax_reduce_kernel");
+}
+
+int argmax_rows(const float* logits, int M, int V, int ld, int32_t* ids, float* vals, cudaStream_t s) {
+  if (M == 0) return SR_OK;
+  argmax_rows_kernel<<<M, 512, 0, s>>>(logits, V, ld, ids, vals);
+  return check_launch("argmax_rows_kernel");
+}
+
+template int embed_rows<float>(const float*, const int32_t*, int, int, float*, cudaStream_t);
+template int embed_rows<__nv_bfloat16>(const __nv_bfloat16*, const int32_t*, int, int, float*, cudaStream_t);
+template int rmsnorm_rows<float>(const float*, const float*, int, int, float, float*, cudaStream_t);
+template int rmsnorm_rows<__nv_bfloat16>(const float*, const float*, int, int, float, __nv_bfloat16*, cudaStream_t);
+template int rope_scatter<float>(const float*, const int32_t*, const SeqInfo*, int, int, const float*,
+                                 const float*, int, int, const KvLayout&, float*, cudaStream_t);
+template int rope_scatter<__nv_bfloat16>(const __nv_bfloat16*, const int32_t*, const SeqInfo*, int, int,
+                                         const float*, const float*, int, int, const KvLayout&,
+                                         __nv_bfloat16*, cudaStream_t);
+
+}  // namespace sr

@@ -1,0 +1,310 @@
+// Verification forward of the target model (K1 + K2 + K6), C++ runtime.
+//
+// `sr_model_create` takes device pointers to weights, the paged KV cache and
+// a caller-owned workspace, builds every GEMM plan (TMA tensor maps) once,
+// and `sr_model_forward` enqueues the whole Qwen2-style decoder on one
+// stream with no host synchronization and no allocation, so a step can be
+// captured in a CUDA graph.  Layer sequence (per layer):
+//
+//   h   = RMSNorm(x) * ln1                       rmsnorm_rows
+//   qkv = h Wqkv^T + b                           tcgen05 GEMM, bias epilogue
+//   q,k,v -> RoPE, k/v into paged cache/window   rope_scatter
+//   o   = attention(q, cache)                    paged GQA attention
+//   x  += o Wo^T                                 GEMM, residual epilogue
+//   h   = RMSNorm(x) * ln2
+//   a   = silu(h Wg^T) * (h Wu^T)                GEMM, SwiGLU epilogue
+//   x  += a Wd^T                                 GEMM, residual epilogue
+//
+// then the final norm and the lm_head GEMM with a fused vocabulary argmax
+// epilogue (logits never reach HBM) or an fp32 logits epilogue.
+#include "common.cuh"
+#include "gemm.cuh"
+#include "layers.cuh"
+
+#include <cuda_bf16.h>
+#include <new>
+#include <vector>
+
+namespace sr {
+
+size_t attention_partial_floats(int num_seqs, int kv_heads, int qblocks, int splits, int hd);
+int attention_bf16(const __nv_bfloat16* q, const SeqInfo* seqs, int num_seqs, int max_q_len, int max_key,
+                   const KvLayout& kv, int layer, int nq, float* partials, size_t partial_floats,
+                   __nv_bfloat16* out, cudaStream_t stream);
+int attention_f32(const float* q, const SeqInfo* seqs, int num_seqs, int max_q_len, const KvLayout& kv,
+                  int layer, int nq, float* out, cudaStream_t stream);
+int kv_commit(int B, int N, const SeqInfo* seqs, const int32_t* outcome, const int32_t* bon,
+              const KvLayout& kv, int dtype, cudaStream_t s);
+
+namespace {
+
+constexpr int kLayerPtrs = 7;  // ln1, w_qkv, b_qkv, w_o, ln2, w_gu, w_down
+constexpr int kLmBn = 128;
+
+__global__ void gather_rows_kernel(const void* __restrict__ src, const int32_t* __restrict__ rows, int H,
+                                   int esize, void* __restrict__ dst) {
+  const int r = blockIdx.x;
+  const char* s = reinterpret_cast<const char*>(src) + (int64_t)rows[r] * H * esize;
+  char* d = reinterpret_cast<char*>(dst) + (int64_t)r * H * esize;
+  for (int i = threadIdx.x * 4; i < H * esize; i += blockDim.x * 4)
+    *reinterpret_cast<uint32_t*>(d + i) = *reinterpret_cast<const uint32_t*>(s + i);
+}
+
+struct Carve {
+  char* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+}  // namespace
+
+struct Model {
+  sr_model_desc d;
+  std::vector<const void*> layer_ptrs;
+  KvLayout kv;
+  int esize;
+  int qkv_width;
+  int lm_tiles;
+  int splits_max;
+  size_t partial_floats;
+  // workspace views
+  float* x;
+  void* h;
+  void* qkv;
+  void* q;
+  void* attn;
+  void* act;
+  void* h_sel;
+  float* logits;       // only when desc.logits_capacity > 0
+  float* part_val;
+  int32_t* part_idx;
+  float* attn_part;
+  // plans (bf16)
+  std::vector<GemmPlan> p_qkv, p_o, p_gu, p_down;
+  GemmPlan p_lm_argmax, p_lm_logits;
+};
+
+static size_t carve(const sr_model_desc& d, Model* m, char* base) {
+  Carve c{base};
+  const int T = d.max_tokens, H = d.hidden;
+  const int esize = d.dtype == 1 ? 2 : 4;
+  const int qkv_w = (d.q_heads + 2 * d.kv_heads) * d.head_dim;
+  const int G = d.q_heads / d.kv_heads;
+  const int lm_tiles = (d.vocab + kLmBn - 1) / kLmBn;
+  const int splits = ((d.max_key / 64 + 1) + 15) / 16;
+  const size_t pf = attention_partial_floats(1, d.kv_heads, (d.max_seqs + (T * G + 63) / 64), splits,
+                                             d.head_dim);
+  float* x = c.take<float>((size_t)T * H);
+  char* h = c.take<char>((size_t)T * H * esize);
+  char* qkv = c.take<char>((size_t)T * qkv_w * esize);
+  char* q = c.take<char>((size_t)T * d.q_heads * d.head_dim * esize);
+  char* attn = c.take<char>((size_t)T * d.q_heads * d.head_dim * esize);
+  char* act = c.take<char>((size_t)T * d.intermediate * esize);
+  char* h_sel = c.take<char>((size_t)T * H * esize);
+  const int vpad = (d.vocab + 7) / 8 * 8;  // 16-byte aligned logit rows
+  float* logits = d.logits_capacity > 0 ? c.take<float>((size_t)d.logits_capacity * vpad) : nullptr;
+  float* pv = c.take<float>((size_t)T * lm_tiles);
+  int32_t* pi = c.take<int32_t>((size_t)T * lm_tiles);
+  float* ap = c.take<float>(d.dtype == 1 ? pf : 0);
+  if (m != nullptr) {
+    m->x = x; m->h = h; m->qkv = qkv; m->q = q; m->attn = attn; m->act = act; m->h_sel = h_sel;
+    m->logits = logits; m->part_val = pv; m->part_idx = pi; m->attn_part = ap;
+    m->esize = esize; m->qkv_width = qkv_w; m->lm_tiles = lm_tiles; m->splits_max = splits;
+    m->partial_floats = d.dtype == 1 ? pf : 0;
+  }
+  return c.off + 256;
+}
+
+static int validate(const sr_model_desc& d) {
+  SR_REQUIRE(d.dtype == 0 || d.dtype == 1, "dtype must be 0 (fp32) or 1 (bf16)");
+  SR_REQUIRE(d.hidden > 0 && d.intermediate > 0 && d.layers > 0 && d.vocab > 0, "bad model shape");
+  SR_REQUIRE(d.q_heads > 0 && d.kv_heads > 0 && d.q_heads % d.kv_heads == 0, "q_heads % kv_heads != 0");
+  SR_REQUIRE(d.head_dim % 16 == 0 && d.head_dim <= 128, "head_dim must be a multiple of 16, <= 128");
+  SR_REQUIRE(d.intermediate % 16 == 0, "intermediate must be a multiple of 16");
+  SR_REQUIRE(d.page_size == 64, "page_size must be 64");
+  SR_REQUIRE(d.max_tokens > 0 && d.max_seqs > 0, "max_tokens / max_seqs must be > 0");
+  SR_REQUIRE(d.max_key < d.max_pos, "max_key must be < max_pos (RoPE table)");
+  SR_REQUIRE(d.q_heads / d.kv_heads * 1 <= 64, "group size too large");
+  return SR_OK;
+}
+
+}  // namespace sr
+
+using sr::Model;
+
+extern "C" {
+
+uint64_t sr_model_workspace_bytes(const sr_model_desc* desc) {
+  if (desc == nullptr || sr::validate(*desc) != SR_OK) return 0;
+  return (uint64_t)sr::carve(*desc, nullptr, nullptr);
+}
+
+int sr_model_create(const sr_model_desc* desc, void** handle) {
+  SR_REQUIRE(desc && handle, "null pointer");
+  int rc = sr::validate(*desc);
+  if (rc) return rc;
+  const sr_model_desc& d = *desc;
+  SR_REQUIRE(d.embed && d.lm_head && d.final_norm && d.layer_weights && d.rope_cos && d.rope_sin &&
+                 d.kv_cache && d.block_table && d.workspace,
+             "null model pointer");
+  const size_t need = sr::carve(d, nullptr, nullptr);
+  SR_REQUIRE(d.workspace_bytes >= need, "workspace too small (see sr_model_workspace_bytes)");
+  Model* m = new (std::nothrow) Model();
+  if (m == nullptr) return sr::config_error("out of host memory");
+  m->d = d;
+  m->layer_ptrs.assign(d.layer_weights, d.layer_weights + (size_t)d.layers * sr::kLayerPtrs);
+  m->d.layer_weights = m->layer_ptrs.data();
+  sr::carve(d, m, reinterpret_cast<char*>(d.workspace));
+  sr::KvLayout& kv = m->kv;
+  kv.cache = d.kv_cache;
+  kv.block_table = d.block_table;
+  kv.max_pages = d.max_pages_per_req;
+  kv.page = d.page_size;
+  kv.num_pages = d.num_pages;
+  kv.window = d.window_kv;
+  kv.window_max = d.window_max;
+  kv.branches = d.max_branches;
+  kv.kv_heads = d.kv_heads;
+  kv.head_dim = d.head_dim;
+  kv.layers = d.layers;
+  if (d.dtype == 1) {
+    using bf = __nv_bfloat16;
+    const int T = d.max_tokens, H = d.hidden, I = d.intermediate;
+    const int nqd = d.q_heads * d.head_dim;
+    m->p_qkv.resize(d.layers);
+    m->p_o.resize(d.layers);
+    m->p_gu.resize(d.layers);
+    m->p_down.resize(d.layers);
+    for (int l = 0; l < d.layers; ++l) {
+      const void* const* w = m->layer_ptrs.data() + (size_t)l * sr::kLayerPtrs;
+      rc = sr::gemm_bf16_plan(&m->p_qkv[l], T, m->qkv_width, H, (const bf*)m->h, H, (const bf*)w[1], H,
+                              m->qkv, m->qkv_width, sr::kEpiStoreBf16, (const float*)w[2], 0);
+      if (!rc) rc = sr::gemm_bf16_plan(&m->p_o[l], T, H, nqd, (const bf*)m->attn, nqd, (const bf*)w[3], nqd,
+                                       m->x, H, sr::kEpiResidualF32, nullptr, 0);
+      if (!rc) rc = sr::gemm_bf16_plan(&m->p_gu[l], T, 2 * I, H, (const bf*)m->h, H, (const bf*)w[5], H,
+                                       m->act, I, sr::kEpiSwiGLU, nullptr, 0);
+      if (!rc) rc = sr::gemm_bf16_plan(&m->p_down[l], T, H, I, (const bf*)m->act, I, (const bf*)w[6], I,
+                                       m->x, H, sr::kEpiResidualF32, nullptr, 0);
+      if (rc) { delete m; return rc; }
+    }
+    rc = sr::gemm_bf16_plan(&m->p_lm_argmax, T, d.vocab, H, (const bf*)m->h_sel, H, (const bf*)d.lm_head, H,
+                            m->part_val, m->lm_tiles, sr::kEpiArgmax, nullptr, sr::kLmBn, m->part_idx);
+    if (!rc && m->logits)
+      rc = sr::gemm_bf16_plan(&m->p_lm_logits, T, d.vocab, H, (const bf*)m->h_sel, H, (const bf*)d.lm_head, H,
+                              m->logits, (d.vocab + 7) / 8 * 8, sr::kEpiStoreF32, nullptr, 0);
+    if (rc) { delete m; return rc; }
+  }
+  *handle = m;
+  return SR_OK;
+}
+
+int sr_model_destroy(void* handle) {
+  delete reinterpret_cast<Model*>(handle);
+  return SR_OK;
+}
+
+int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_) {
+  SR_REQUIRE(handle && a, "null pointer");
+  Model* m = reinterpret_cast<Model*>(handle);
+  const sr_model_desc& d = m->d;
+  cudaStream_t st = (cudaStream_t)stream_;
+  const int M = a->num_tokens, S = a->num_seqs;
+  SR_REQUIRE(M >= 0 && M <= d.max_tokens, "num_tokens exceeds max_tokens");
+  SR_REQUIRE(S >= 0 && S <= d.max_seqs, "num_seqs exceeds max_seqs");
+  SR_REQUIRE(a->max_key >= 0 && a->max_key <= d.max_key, "max_key exceeds the model's max_key");
+  SR_REQUIRE(a->token_ids && a->positions && a->seqs && a->out, "null forward pointer");
+  const int R = a->logit_rows ? a->num_logit_rows : M;
+  SR_REQUIRE(R >= 0 && R <= d.max_tokens, "bad logit row count");
+  SR_REQUIRE(a->output == 0 || (a->output == 1 && m->logits != nullptr && R <= d.logits_capacity) ||
+                 a->output == 2,
+             "logits output needs logits_capacity >= rows");
+  if (M == 0) return SR_OK;
+  const auto* seqs = reinterpret_cast<const sr::SeqInfo*>(a->seqs);
+  const int H = d.hidden, I = d.intermediate, nqd = d.q_heads * d.head_dim;
+  int rc;
+#define SR_TRY(x) do { rc = (x); if (rc) return rc; } while (0)
+  if (d.dtype == 1) {
+    using bf = __nv_bfloat16;
+    SR_TRY(sr::embed_rows<bf>((const bf*)d.embed, a->token_ids, M, H, m->x, st));
+    for (int l = 0; l < d.layers; ++l) {
+      const void* const* w = m->layer_ptrs.data() + (size_t)l * sr::kLayerPtrs;
+      SR_TRY(sr::rmsnorm_rows<bf>(m->x, (const float*)w[0], M, H, d.rms_eps, (bf*)m->h, st));
+      SR_TRY(sr::gemm_bf16_launch(m->p_qkv[l], st, M));
+      SR_TRY(sr::rope_scatter<bf>((const bf*)m->qkv, a->positions, seqs, S, a->max_q_len, d.rope_cos,
+                                  d.rope_sin, d.q_heads, l, m->kv, (bf*)m->q, st));
+      SR_TRY(sr::attention_bf16((const bf*)m->q, seqs, S, a->max_q_len, a->max_key, m->kv, l, d.q_heads,
+                                m->attn_part, m->partial_floats, (bf*)m->attn, st));
+      SR_TRY(sr::gemm_bf16_launch(m->p_o[l], st, M));
+      SR_TRY(sr::rmsnorm_rows<bf>(m->x, (const float*)w[4], M, H, d.rms_eps, (bf*)m->h, st));
+      SR_TRY(sr::gemm_bf16_launch(m->p_gu[l], st, M));
+      SR_TRY(sr::gemm_bf16_launch(m->p_down[l], st, M));
+    }
+    SR_TRY(sr::rmsnorm_rows<bf>(m->x, d.final_norm, M, H, d.rms_eps, (bf*)m->h, st));
+    if (a->logit_rows) {
+      sr::gather_rows_kernel<<<R, 256, 0, st>>>(m->h, a->logit_rows, H, 2, m->h_sel);
+      SR_TRY(sr::check_launch("gather_rows_kernel"));
+    } else {
+      SR_CHECK_CUDA(cudaMemcpyAsync(m->h_sel, m->h, (size_t)M * H * 2, cudaMemcpyDeviceToDevice, st));
+    }
+    if (a->output == 1) {
+      SR_TRY(sr::gemm_bf16_launch(m->p_lm_logits, st, R));
+      const size_t vpad = (size_t)(d.vocab + 7) / 8 * 8;
+      SR_CHECK_CUDA(cudaMemcpy2DAsync(a->out, (size_t)d.vocab * 4, m->logits, vpad * 4, (size_t)d.vocab * 4, R,
+                                      cudaMemcpyDeviceToDevice, st));
+    } else {
+      SR_TRY(sr::gemm_bf16_launch(m->p_lm_argmax, st, R));
+      SR_TRY(sr::argmax_reduce(m->part_val, m->part_idx, R, m->lm_tiles, (int32_t*)a->out, a->out_val, st));
+    }
+  } else {
+    SR_TRY(sr::embed_rows<float>((const float*)d.embed, a->token_ids, M, H, m->x, st));
+    for (int l = 0; l < d.layers; ++l) {
+      const void* const* w = m->layer_ptrs.data() + (size_t)l * sr::kLayerPtrs;
+      float* h = (float*)m->h;
+      SR_TRY(sr::rmsnorm_rows<float>(m->x, (const float*)w[0], M, H, d.rms_eps, h, st));
+      SR_TRY(sr::gemm_f32(M, m->qkv_width, H, h, H, (const float*)w[1], H, m->qkv, m->qkv_width,
+                          sr::kEpiStoreF32, (const float*)w[2], st));
+      SR_TRY(sr::rope_scatter<float>((const float*)m->qkv, a->positions, seqs, S, a->max_q_len, d.rope_cos,
+                                     d.rope_sin, d.q_heads, l, m->kv, (float*)m->q, st));
+      SR_TRY(sr::attention_f32((const float*)m->q, seqs, S, a->max_q_len, m->kv, l, d.q_heads,
+                               (float*)m->attn, st));
+      SR_TRY(sr::gemm_f32(M, H, nqd, (const float*)m->attn, nqd, (const float*)w[3], nqd, m->x, H,
+                          sr::kEpiResidualF32, nullptr, st));
+      SR_TRY(sr::rmsnorm_rows<float>(m->x, (const float*)w[4], M, H, d.rms_eps, h, st));
+      SR_TRY(sr::gemm_f32(M, 2 * I, H, h, H, (const float*)w[5], H, m->act, I, sr::kEpiSwiGLU, nullptr, st));
+      SR_TRY(sr::gemm_f32(M, H, I, (const float*)m->act, I, (const float*)w[6], I, m->x, H,
+                          sr::kEpiResidualF32, nullptr, st));
+    }
+    SR_TRY(sr::rmsnorm_rows<float>(m->x, d.final_norm, M, H, d.rms_eps, (float*)m->h, st));
+    if (a->logit_rows) {
+      sr::gather_rows_kernel<<<R, 256, 0, st>>>(m->h, a->logit_rows, H, 4, m->h_sel);
+      SR_TRY(sr::check_launch("gather_rows_kernel"));
+    } else {
+      SR_CHECK_CUDA(cudaMemcpyAsync(m->h_sel, m->h, (size_t)M * H * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    float* logits = a->output == 1 ? (float*)a->out : m->logits;
+    SR_REQUIRE(logits != nullptr && R <= (a->output == 1 ? d.max_tokens : d.logits_capacity),
+               "fp32 path needs logits_capacity >= rows for argmax");
+    SR_TRY(sr::gemm_f32(R, d.vocab, H, (const float*)m->h_sel, H, (const float*)d.lm_head, H, logits, d.vocab,
+                        sr::kEpiStoreF32, nullptr, st));
+    if (a->output != 1) SR_TRY(sr::argmax_rows(logits, R, d.vocab, d.vocab, (int32_t*)a->out, a->out_val, st));
+  }
+#undef SR_TRY
+  return SR_OK;
+}
+
+int sr_kv_commit(void* handle, int num_requests, int num_drafters, const void* seqs, const int32_t* outcome,
+                 const int32_t* bon, sr_stream_t stream) {
+  SR_REQUIRE(handle, "null model");
+  Model* m = reinterpret_cast<Model*>(handle);
+  if (num_drafters > 1) SR_REQUIRE(m->d.window_kv != nullptr, "drafter branches need a window buffer");
+  return sr::kv_commit(num_requests, num_drafters, reinterpret_cast<const sr::SeqInfo*>(seqs), outcome, bon,
+                       m->kv, m->d.dtype, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,197 @@
+"""Model-mode speculative rollout on one GPU (the hot path of BASELINE.json).
+
+One :meth:`RolloutEngine.step` is one speculation window for every live
+request of the batch, entirely on device:
+
+    sr_ngram_propose      K4  n-gram drafts from the token buffer
+    sr_build_verify_batch     verify rows [last token, d_1..d_k] per drafter
+    sr_model_forward      K1+K2+K6  target verify forward, fused argmax
+    sr_accept_commit      K3  accepted prefix, Best-of-N select, commit
+    sr_kv_commit              winning branch KV -> paged cache (N > 1)
+
+This replaces one ``_Executor.begin_round``/``end_round`` pair of the
+reference (``sim.py:834-1092``) with real drafting and verification; the
+outcome rows carry the reference's ``VerificationOutcome`` fields.  The step
+needs no host synchronization; the host only reads outcome rows when asked.
+Steps can be captured into a CUDA graph (:meth:`capture`).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .errors import ConfigError
+from .model import DeviceModel, seq_table
+
+
+@dataclass(frozen=True)
+class NgramDrafter:
+    """vLLM-style prompt-lookup drafter (``ngram_proposer.py:198-285``)."""
+
+    min_n: int = 1
+    max_n: int = 3
+    name: str = "ngram"
+
+
+class RolloutEngine:
+    """Batch state (token buffer, lengths, budgets) + per-step device work."""
+
+    def __init__(self, target: DeviceModel, prompts: list[np.ndarray], max_new: list[int], *, k: int = 4,
+                 drafters: tuple = (NgramDrafter(),), bonus_token: bool = False, history: int = 0):
+        if not prompts:
+            raise ConfigError("empty batch")
+        if len(prompts) != len(max_new):
+            raise ConfigError("prompts / max_new length mismatch")
+        self.m = target
+        self.lib = target.lib
+        self.dev = target.dev
+        self.k = k
+        self.drafters = tuple(drafters)
+        self.N = len(self.drafters)
+        self.B = len(prompts)
+        self.bonus = 1 if bonus_token else 0
+        if self.N > 1 and target.branches < self.B * (self.N - 1):
+            raise ConfigError("target model needs max_branches >= B*(N-1) for Best-of-N")
+        if self.B * self.N > target.max_seqs or self.B * self.N * (k + 1) > target.max_tokens:
+            raise ConfigError("batch exceeds the model's max_seqs / max_tokens")
+        lens = [len(p) for p in prompts]
+        need = max(l + n for l, n in zip(lens, max_new)) + k + 2
+        if need > target.max_len:
+            raise ConfigError(f"prompt + generation ({need}) exceeds model max_len {target.max_len}")
+        self.stride = int(math.ceil(need / 16) * 16)
+        dev = self.dev
+        tok = np.zeros((self.B, self.stride), dtype=np.int32)
+        for i, p in enumerate(prompts):
+            tok[i, : len(p)] = p
+        self.prompt_lens = lens
+        self.tokens = torch.from_numpy(tok).to(dev)
+        self.seq_len = torch.tensor(lens, dtype=torch.int32, device=dev)
+        self.gen_len = torch.zeros(self.B, dtype=torch.int32, device=dev)
+        self.max_new = torch.tensor(max_new, dtype=torch.int32, device=dev)
+        S, R = self.B * self.N, self.B * self.N * (k + 1)
+        self.drafts = torch.full((self.N, self.B, k), -1, dtype=torch.int32, device=dev)
+        self.ndraft = torch.zeros((self.N, self.B), dtype=torch.int32, device=dev)
+        self.ngram_scratch = torch.zeros(2 * self.B, dtype=torch.int64, device=dev)
+        self.token_ids = torch.zeros(R, dtype=torch.int32, device=dev)
+        self.positions = torch.zeros(R, dtype=torch.int32, device=dev)
+        self.seqs = torch.zeros((S, 8), dtype=torch.int32, device=dev)
+        self.target_ids = torch.zeros(R, dtype=torch.int32, device=dev)
+        self.history = torch.zeros((max(history, 1), S, 4), dtype=torch.int32, device=dev)
+        self.bon = torch.zeros(self.B, dtype=torch.int32, device=dev)
+        self.steps = 0
+        self.max_key = need - 1
+        self.graph = None
+
+    # -- prefill -------------------------------------------------------------
+
+    def prefill(self) -> None:
+        """Prompt forward (KV straight into the paged cache) + first token."""
+        m = self.m
+        order = list(range(self.B))
+        i = 0
+        while i < len(order):
+            rows, tok_rows, pos_rows, last = [], [], [], []
+            start = 0
+            max_q = 0
+            while i < len(order):
+                b = order[i]
+                L = self.prompt_lens[b]
+                if rows and (start + L > m.max_tokens or len(rows) + 1 > m.max_prefill_seqs(max(max_q, L))):
+                    break
+                rows.append((start, L, b, 0, -1))
+                tok_rows.append(self.tokens[b, :L])
+                pos_rows.append(torch.arange(L, dtype=torch.int32, device=self.dev))
+                last.append(start + L - 1)
+                start += L
+                max_q = max(max_q, L)
+                i += 1
+            ids = torch.cat(tok_rows)
+            pos = torch.cat(pos_rows)
+            seqs = seq_table(rows, self.dev)
+            lr = torch.tensor(last, dtype=torch.int32, device=self.dev)
+            out = torch.empty(len(rows), dtype=torch.int32, device=self.dev)
+            m.forward(ids, pos, seqs, num_seqs=len(rows), max_q_len=max_q, max_key=max_q - 1,
+                      out=out, logit_rows=lr)
+            for j, r in enumerate(rows):
+                b = r[2]
+                self.tokens[b, self.prompt_lens[b]] = out[j]
+        self.seq_len += 1
+        self.gen_len += 1
+
+    # -- one speculation window ------------------------------------------------
+
+    def _enqueue_step(self, slot: int) -> None:
+        lib, st = self.lib, _native.stream_handle()
+        drafts_ptr, nd_ptr = None, None
+        if self.k > 0:
+            for n, d in enumerate(self.drafters):
+                _native.check(lib.sr_ngram_propose(
+                    self.B, self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(), d.min_n, d.max_n,
+                    self.k, self.drafts[n].data_ptr(), self.ndraft[n].data_ptr(),
+                    self.ngram_scratch.data_ptr(), st), "sr_ngram_propose")
+            drafts_ptr, nd_ptr = self.drafts.data_ptr(), self.ndraft.data_ptr()
+        _native.check(lib.sr_build_verify_batch(
+            self.B, self.N, self.k, self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(),
+            self.gen_len.data_ptr(), self.max_new.data_ptr(), drafts_ptr, nd_ptr,
+            self.token_ids.data_ptr(), self.positions.data_ptr(), self.seqs.data_ptr(), st),
+            "sr_build_verify_batch")
+        self.m.forward(self.token_ids, self.positions, self.seqs, num_seqs=self.B * self.N,
+                       max_q_len=self.k + 1, max_key=self.max_key, out=self.target_ids)
+        out = self.history[slot]
+        _native.check(lib.sr_accept_commit(
+            self.B, self.N, self.seqs.data_ptr(), self.token_ids.data_ptr(), self.target_ids.data_ptr(),
+            self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(), self.gen_len.data_ptr(),
+            self.max_new.data_ptr(), self.bonus, out.data_ptr(), self.bon.data_ptr(), st),
+            "sr_accept_commit")
+        if self.N > 1:
+            _native.check(lib.sr_kv_commit(self.m.handle, self.B, self.N, self.seqs.data_ptr(),
+                                           out.data_ptr(), self.bon.data_ptr(), st), "sr_kv_commit")
+
+    def step(self) -> None:
+        slot = self.steps % self.history.shape[0]
+        if self.graph is not None and slot == 0:
+            self.graph.replay()
+        else:
+            self._enqueue_step(slot)
+        self.steps += 1
+
+    def capture(self) -> None:
+        """Capture one step (history slot 0) into a CUDA graph."""
+        if self.history.shape[0] != 1:
+            raise ConfigError("graph capture needs history=0/1 (the graph writes slot 0)")
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            g.capture_begin()
+            self._enqueue_step(0)
+            g.capture_end()
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = g
+
+    # -- host views -------------------------------------------------------------
+
+    def done(self) -> bool:
+        return bool((self.gen_len >= self.max_new).all().item())
+
+    def run(self, max_steps: int = 1_000_000) -> int:
+        n = 0
+        while n < max_steps and not self.done():
+            self.step()
+            n += 1
+        return n
+
+    def outputs(self) -> list[list[int]]:
+        tok = self.tokens.cpu().numpy()
+        lens = self.seq_len.cpu().numpy()
+        return [tok[b, self.prompt_lens[b]: lens[b]].tolist() for b in range(self.B)]
+
+    def outcome_rows(self, steps: int | None = None) -> np.ndarray:
+        h = self.history.cpu().numpy()
+        return h[: steps] if steps is not None else h

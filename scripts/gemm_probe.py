@@ -58,7 +58,7 @@ def main():
 
             def run():
                 _native.check(lib.sr_gemm(1, M, N, K, A.data_ptr(), K, W.data_ptr(), K,
-                                          C.data_ptr(), C.stride(0), epi, None, bn, st), "gemm")
+                                          C.data_ptr(), C.stride(0), epi, None, bn, None, st), "gemm")
             ms = time_it(run)
             tf = 2 * M * N * K / ms / 1e9
             print(f"{name:8s} M={M} N={N} K={K} bn={bn}: {ms*1e3:8.1f} us  {tf:7.1f} TFLOP/s")

@@ -21,7 +21,7 @@ def sr_gemm(A, W, C, epi, bias=None, bn=0):
     N = W.shape[0]
     _native.check(lib.sr_gemm(dtype, M, N, K, A.data_ptr(), A.stride(0), W.data_ptr(),
                               W.stride(0), C.data_ptr(), C.stride(0), epi,
-                              bias.data_ptr() if bias is not None else None, bn,
+                              bias.data_ptr() if bias is not None else None, bn, None,
                               _native.stream_handle()), "sr_gemm")
     torch.cuda.synchronize()
 

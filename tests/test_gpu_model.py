@@ -1,0 +1,230 @@
+"""GPU parity of the model-mode rollout: verify-forward logits vs the CPU
+oracle (1e-5 fp32, 1e-2 bf16, as BASELINE.json's north star states), greedy
+outputs vs the oracle, and the exactness invariant: plain decode, n-gram
+speculation and Best-of-N commit byte-identical sequences."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ngram_oracle
+from oracle.qwen2_oracle import Qwen2Oracle, margin
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+BF16_TOL = 1e-2
+
+
+def rel_err(got: torch.Tensor, exp: torch.Tensor) -> float:
+    return float((got.double() - exp.double()).abs().max() / exp.double().abs().max())
+
+
+def prompts_for(vocab: int, n: int, seed: int, lo=20, hi=90, alphabet=40):
+    rng = np.random.default_rng(seed)
+    words = rng.integers(0, vocab, size=alphabet)
+    return [words[rng.integers(0, alphabet, size=int(rng.integers(lo, hi)))].astype(np.int32)
+            for _ in range(n)]
+
+
+def make(shape_name, dtype, layers=None, B=4, max_len=512, branches=0, logits=0, max_tokens=None):
+    from paper_2511_16193_b200.model import DeviceModel, init_weights, shape
+
+    s = shape(shape_name, layers)
+    w = init_weights(s, seed=0)
+    m = DeviceModel(s, w, dtype=dtype, max_requests=B, max_len=max_len,
+                    max_tokens=max_tokens or max(B * 8 * 3, 512), max_seqs=B * 3,
+                    branches=branches, logits_capacity=logits)
+    return s, w, m
+
+
+def prefill_logits(m, prompts):
+    """Logits of every prompt position through the GPU prefill path."""
+    from paper_2511_16193_b200.model import seq_table
+
+    rows, ids, pos, start = [], [], [], 0
+    for b, p in enumerate(prompts):
+        rows.append((start, len(p), b, 0, -1))
+        ids.append(torch.from_numpy(p))
+        pos.append(torch.arange(len(p), dtype=torch.int32))
+        start += len(p)
+    ids = torch.cat(ids).cuda()
+    pos = torch.cat(pos).cuda()
+    out = torch.empty(start, m.s.vocab, device="cuda")
+    m.forward(ids, pos, seq_table(rows, "cuda"), num_seqs=len(rows),
+              max_q_len=max(len(p) for p in prompts), max_key=max(len(p) for p in prompts) - 1,
+              out=out, output=1)
+    torch.cuda.synchronize()
+    res, start = [], 0
+    for p in prompts:
+        res.append(out[start:start + len(p)].cpu())
+        start += len(p)
+    return res
+
+
+@pytest.mark.parametrize("dtype,tol", [("fp32", FP32_TOL), ("bf16", BF16_TOL)])
+def test_tiny_prefill_logits_vs_oracle(dtype, tol):
+    s, w, m = make("tiny", dtype, logits=4096)
+    ora = Qwen2Oracle(s, w, dtype)
+    prompts = prompts_for(s.vocab, 3, 1)
+    for p, got in zip(prompts, prefill_logits(m, prompts)):
+        assert rel_err(got, ora.logits(p.tolist())) <= tol
+
+
+def test_qwen15b_shape_bf16_logits_vs_oracle():
+    # real Qwen2.5-1.5B widths (hidden 1536, 12/2 heads, hd 128, vocab 151936), 2 layers
+    s, w, m = make("qwen2.5-1.5b", "bf16", layers=2, B=2, logits=512)
+    ora = Qwen2Oracle(s, w, "bf16")
+    prompts = prompts_for(s.vocab, 2, 2, lo=70, hi=140)
+    for p, got in zip(prompts, prefill_logits(m, prompts)):
+        assert rel_err(got, ora.logits(p.tolist())) <= BF16_TOL
+
+
+def run_engine(m, prompts, max_new, k, drafters=None, bonus=False):
+    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine
+
+    eng = RolloutEngine(m, prompts, max_new, k=k, drafters=drafters or (NgramDrafter(),),
+                        bonus_token=bonus, history=512)
+    eng.prefill()
+    steps = eng.run()
+    return eng, steps
+
+
+@pytest.mark.parametrize("bonus", [False, True])
+def test_tiny_fp32_spec_decode_matches_oracle(bonus):
+    s, w, m = make("tiny", "fp32", logits=64)
+    ora = Qwen2Oracle(s, w, "fp32")
+    prompts = prompts_for(s.vocab, 4, 3)
+    max_new = [40, 17, 33, 5]
+    eng, steps = run_engine(m, prompts, max_new, k=4, bonus=bonus)
+    outs = eng.outputs()
+    rows = eng.outcome_rows(steps)
+    for b, p in enumerate(prompts):
+        exp, exp_rows = ora.spec_decode(p.tolist(), max_new[b], 4, bonus=bonus,
+                                        max_model_len=eng.stride)
+        assert outs[b] == exp, f"request {b}"
+        got_rows = [tuple(r) for r in rows[:, b, :] if r[0] or r[2]]
+        assert got_rows == exp_rows, f"request {b} outcomes"
+
+
+def test_tiny_fp32_greedy_margins():
+    # parity above is only meaningful if greedy choices are not near-ties
+    s, w, _ = make("tiny", "fp32")
+    ora = Qwen2Oracle(s, w, "fp32")
+    p = prompts_for(s.vocab, 1, 3)[0].tolist()
+    lg = ora.logits(p + ora.greedy(p, 8))
+    assert min(margin(r) for r in lg[len(p) - 1:]) > 1e-4
+
+
+@pytest.mark.parametrize("shape_name,layers", [("tiny", None), ("qwen2.5-1.5b", 2)])
+def test_bf16_spec_equals_plain_bit_exact(shape_name, layers):
+    """Exactness invariant: plain decode, k=4 n-gram speculation
+    and Best-of-N (3 n-gram drafters) commit identical sequences."""
+    from paper_2511_16193_b200.engine import NgramDrafter
+
+    B = 4
+    s, w, m = make(shape_name, "bf16", layers=layers, B=B, branches=2 * B, max_len=512)
+    prompts = prompts_for(s.vocab, B, 4)
+    max_new = [60, 31, 47, 12]
+    plain, _ = run_engine(m, prompts, max_new, k=0)
+    ref = plain.outputs()
+    spec, _ = run_engine(m, prompts, max_new, k=4)
+    assert spec.outputs() == ref
+    bon, _ = run_engine(m, prompts, max_new, k=4,
+                        drafters=(NgramDrafter(1, 3), NgramDrafter(2, 4), NgramDrafter(1, 1)))
+    assert bon.outputs() == ref
+
+
+def test_verify_logits_equal_decode_logits_bit_exact():
+    """A position's logits are bit-identical in a 5-row verify window and in
+    a 1-row decode step (batch-invariant GEMM + absolute-position attention)."""
+    from paper_2511_16193_b200.model import seq_table
+
+    s, w, m = make("tiny", "bf16", B=1, logits=256)
+    p = prompts_for(s.vocab, 1, 5)[0]
+    L = len(p)
+    ids = torch.from_numpy(p).cuda()
+    pos = torch.arange(L, dtype=torch.int32, device="cuda")
+    full = torch.empty(L, s.vocab, device="cuda")
+    # prefill the first L-5 tokens, then verify the last 5 as one window
+    P = L - 5
+    m.forward(ids[:P], pos[:P], seq_table([(0, P, 0, 0, -1)], "cuda"), num_seqs=1, max_q_len=P,
+              max_key=P - 1, out=full[:P], output=1)
+    win = torch.empty(5, s.vocab, device="cuda")
+    m.forward(ids[P:], pos[P:], seq_table([(0, 5, 0, P, -1)], "cuda"), num_seqs=1, max_q_len=5,
+              max_key=L - 1, out=win, output=1)
+    # now decode the same 5 positions one at a time (KV rewritten in place)
+    for j in range(5):
+        one = torch.empty(1, s.vocab, device="cuda")
+        m.forward(ids[P + j:P + j + 1], pos[P + j:P + j + 1], seq_table([(0, 1, 0, P + j, -1)], "cuda"),
+                  num_seqs=1, max_q_len=1, max_key=P + j, out=one, output=1)
+        torch.cuda.synchronize()
+        assert torch.equal(one[0], win[j]), f"slot {j}"
+
+
+def test_accept_commit_kernel_vs_python():
+    """K3 on random verify batches (N=3 drafters, budgets, bonus) vs a direct
+    restatement of sim.py:983-1042 + longest-prefix Best-of-N."""
+    from paper_2511_16193_b200 import _native
+
+    lib = _native.lib()
+    rng = np.random.default_rng(7)
+    B, N, k = 37, 3, 5
+    for bonus in (0, 1):
+        S = B * N
+        seqs = np.zeros((S, 8), np.int32)
+        token_ids = rng.integers(0, 4, size=S * (k + 1)).astype(np.int32)
+        target = rng.integers(0, 4, size=S * (k + 1)).astype(np.int32)
+        stride = 64
+        tokens = np.zeros((B, stride), np.int32)
+        seq_len = rng.integers(5, 20, size=B).astype(np.int32)
+        gen_len = rng.integers(0, 10, size=B).astype(np.int32)
+        max_new = gen_len + rng.integers(0, 8, size=B).astype(np.int32)
+        for s_ in range(S):
+            seqs[s_, :5] = (s_ * (k + 1), int(rng.integers(0, k + 2)), s_ // N, 0, -1)
+        dev = {n: torch.from_numpy(v).cuda() for n, v in dict(
+            seqs=seqs, token_ids=token_ids, target=target, tokens=tokens, seq_len=seq_len,
+            gen_len=gen_len, max_new=max_new).items()}
+        outcome = torch.zeros((S, 4), dtype=torch.int32, device="cuda")
+        bon = torch.zeros(B, dtype=torch.int32, device="cuda")
+        _native.check(lib.sr_accept_commit(B, N, dev["seqs"].data_ptr(), dev["token_ids"].data_ptr(),
+                                           dev["target"].data_ptr(), dev["tokens"].data_ptr(), stride,
+                                           dev["seq_len"].data_ptr(), dev["gen_len"].data_ptr(),
+                                           dev["max_new"].data_ptr(), bonus, outcome.data_ptr(),
+                                           bon.data_ptr(), _native.stream_handle()), "accept")
+        torch.cuda.synchronize()
+        got_out, got_bon = outcome.cpu().numpy(), bon.cpu().numpy()
+        got_tok, got_len = dev["tokens"].cpu().numpy(), dev["seq_len"].cpu().numpy()
+        for b in range(B):
+            rem = int(max_new[b] - gen_len[b])
+            acc = []
+            for n in range(N):
+                q0, ql = seqs[b * N + n, 0], seqs[b * N + n, 1]
+                if ql == 0 or rem <= 0:
+                    acc.append(None)
+                    continue
+                nd, a = ql - 1, 0
+                while a < nd and token_ids[q0 + a + 1] == target[q0 + a]:
+                    a += 1
+                acc.append((a, nd, q0))
+            live = [(x[0], -n) for n, x in enumerate(acc) if x is not None]
+            if not live:
+                assert got_bon[b] == -1 and got_len[b] == seq_len[b]
+                continue
+            win = -max(live)[1]
+            a, nd, q0 = acc[win]
+            c = 1 if nd == 0 else (nd + bonus if a == nd else a + 1)
+            c = min(c, rem)
+            assert got_bon[b] == win
+            assert got_len[b] == seq_len[b] + c
+            assert got_tok[b, seq_len[b]:seq_len[b] + c].tolist() == target[q0:q0 + c].tolist()
+            for n in range(N):
+                row = got_out[b * N + n]
+                if acc[n] is None:
+                    assert row.tolist() == [0, 0, 0, 0]
+                    continue
+                an, ndn, _ = acc[n]
+                exp_w = (0 if an == ndn else max(ndn - an - 1, 0)) if n == win else ndn
+                assert row.tolist() == [ndn, an, c if n == win else 0, exp_w]

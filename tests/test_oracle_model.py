@@ -1,0 +1,85 @@
+"""CPU: pin the model oracle.  The reference has no model, so the PyTorch-CPU
+restatement (oracle/qwen2_oracle.py) is cross-checked against an independent
+implementation of the same architecture -- transformers' Qwen2ForCausalLM --
+on identical random-init weights; plus host-side model utilities."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.qwen2_oracle import Qwen2Oracle
+
+
+def hf_model(s, w):
+    from transformers import Qwen2Config, Qwen2ForCausalLM
+
+    cfg = Qwen2Config(vocab_size=s.vocab, hidden_size=s.hidden, intermediate_size=s.intermediate,
+                      num_hidden_layers=s.layers, num_attention_heads=s.q_heads,
+                      num_key_value_heads=s.kv_heads, head_dim=s.head_dim, rms_norm_eps=s.rms_eps,
+                      tie_word_embeddings=s.tied, max_position_embeddings=4096,
+                      rope_parameters={"rope_type": "default", "rope_theta": s.rope_theta})
+    cfg._attn_implementation = "eager"
+    m = Qwen2ForCausalLM(cfg).double().eval()
+    sd = {"model.embed_tokens.weight": w["embed"], "model.norm.weight": w["final_norm"],
+          "lm_head.weight": w["lm_head"]}
+    for i, L in enumerate(w["layers"]):
+        p = f"model.layers.{i}."
+        sd.update({
+            p + "input_layernorm.weight": L["ln1"], p + "post_attention_layernorm.weight": L["ln2"],
+            p + "self_attn.q_proj.weight": L["wq"], p + "self_attn.q_proj.bias": L["bq"],
+            p + "self_attn.k_proj.weight": L["wk"], p + "self_attn.k_proj.bias": L["bk"],
+            p + "self_attn.v_proj.weight": L["wv"], p + "self_attn.v_proj.bias": L["bv"],
+            p + "self_attn.o_proj.weight": L["wo"], p + "mlp.gate_proj.weight": L["wg"],
+            p + "mlp.up_proj.weight": L["wu"], p + "mlp.down_proj.weight": L["wd"],
+        })
+    m.load_state_dict({k: v.double() for k, v in sd.items()}, strict=False)
+    return m
+
+
+def test_oracle_fp32_matches_transformers_qwen2():
+    from paper_2511_16193_b200.model import init_weights, shape
+
+    s = shape("tiny")
+    w = init_weights(s, seed=0)
+    ora = Qwen2Oracle(s, w, "fp32")
+    hf = hf_model(s, w)
+    toks = np.random.default_rng(0).integers(0, s.vocab, size=57).tolist()
+    with torch.no_grad():
+        exp = hf(torch.tensor([toks])).logits[0]
+    got = ora.logits(toks)
+    err = float((got - exp).abs().max() / exp.abs().max())
+    assert err < 1e-6, err
+
+
+def test_oracle_bf16_close_to_fp32():
+    from paper_2511_16193_b200.model import init_weights, shape
+
+    s = shape("tiny")
+    w = init_weights(s, seed=1)
+    toks = list(range(100, 160))
+    a = Qwen2Oracle(s, w, "fp32").logits(toks)
+    b = Qwen2Oracle(s, w, "bf16").logits(toks)
+    assert float((a - b.double()).abs().max() / a.abs().max()) < 3e-2
+
+
+def test_interleave_gate_up_layout():
+    from paper_2511_16193_b200.model import interleave_gate_up
+
+    g = torch.arange(32 * 3).view(32, 3).float()
+    u = -g
+    w = interleave_gate_up(g, u)
+    assert torch.equal(w[:16], g[:16]) and torch.equal(w[16:32], u[:16])
+    assert torch.equal(w[32:48], g[16:32]) and torch.equal(w[48:64], u[16:32])
+
+
+def test_shapes_and_roofline_params():
+    from paper_2511_16193_b200.model import SHAPES
+
+    # SURVEY §8d P_lin figures (linear params incl. lm_head)
+    assert abs(SHAPES["qwen2.5-1.5b"].linear_params() / 1.544e9 - 1) < 0.01
+    assert abs(SHAPES["qwen2.5-7b"].linear_params() / 7.070e9 - 1) < 0.01
+    assert abs(SHAPES["qwen2.5-32b"].linear_params() / 31.98e9 - 1) < 0.01
+    assert SHAPES["qwen2.5-1.5b"].kv_bytes_per_token() == 28672
+    assert SHAPES["qwen2.5-7b"].kv_bytes_per_token() == 57344
