@@ -1,0 +1,383 @@
+"""Benchmark of the B200 speculative-rollout hot path (BASELINE.json metric:
+rollout accepted tokens/s; mean accepted length; roofline %).
+
+Workload (BASELINE.json configs[1]): Qwen2.5-1.5B-shaped random-init target,
+256 prompts per GPU, k=4 n-gram drafter (vLLM prompt-lookup semantics,
+min_n=1, max_n=3), greedy exact-match verification, bonus token on.  Prompt
+lengths come from the reference trace generator (default_trace_spec: U[128,
+1024]), prompt tokens from the keyed stream (seed, rid, "prompt").  A step is
+one speculation window over the whole batch: n-gram draft -> verify forward
+(M = 256 x 5 rows through 28 layers + lm_head with fused argmax) -> accept /
+commit.  The batch is kept full (no request reaches its budget during the
+run), i.e. steady-state throughput.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N > 1 runs under torchrun, one rank per GPU, 256 prompts per rank (weak
+scaling by prompt sharding, no data-path collective).  Timing: CUDA events
+on the launching stream, barrier + synchronize on both sides, max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+MODEL = "qwen2.5-1.5b"
+BATCH = 256
+K = 4
+METRIC = "rollout accepted tokens/sec (Qwen2.5-1.5B-shaped target, batch 256, k=4, n-gram drafter, greedy)"
+UNIT = "tokens/s"
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch", type=int, default=BATCH, help="prompts per GPU")
+    ap.add_argument("--model", default=MODEL)
+    ap.add_argument("--layers", type=int, default=None, help="debug only: truncate depth")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="replay steps from a CUDA graph")
+    return ap.parse_args()
+
+
+# -- workload -------------------------------------------------------------------
+
+
+def workload(rank: int, batch: int, steps_total: int, vocab: int):
+    from paper_2511_16193_b200 import scenarios
+    from paper_2511_16193_b200.streams import stream
+    from paper_2511_16193_b200.workload import gen_trace
+
+    trace = gen_trace(scenarios.default_trace_spec(batch=batch * (rank + 1), seed=0))[rank * batch:]
+    prompts = [stream(0, r.id, "prompt").integers(0, vocab, size=r.prompt_len).astype(np.int32)
+               for r in trace]
+    # budget large enough that no request leaves the batch during the run
+    budget = 8 + (K + 1) * steps_total
+    return trace, prompts, [budget] * len(trace)
+
+
+# -- clocks -----------------------------------------------------------------------
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# -- our arm -------------------------------------------------------------------------
+
+
+def peaks():
+    if PEAKS.exists():
+        d = json.loads(PEAKS.read_text())
+        return d["bf16_tflops"], d["bf16_tflops_sustained"], d["hbm_gbs"], "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def run_ours(args, rank, world, dist):
+    import torch
+
+    from paper_2511_16193_b200 import _native
+    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine
+    from paper_2511_16193_b200.model import DeviceModel, init_weights, shape
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    lib = _native.lib()
+    s = shape(args.model, args.layers)
+    steps_total = args.warmup + 2 * args.steps + 2
+    trace, prompts, budget = workload(rank, args.batch, steps_total, s.vocab)
+    max_len = max(len(p) for p in prompts) + budget[0] + K + 8
+    w = init_weights(s, seed=0, device="cuda")
+    B = len(prompts)
+    model = DeviceModel(s, w, dtype="bf16", max_requests=B, max_len=max_len,
+                        max_tokens=max(B * (K + 1), 2048), max_seqs=B)
+    del w
+    torch.cuda.empty_cache()
+    eng = RolloutEngine(model, prompts, budget, k=K, drafters=(NgramDrafter(1, 3),),
+                        bonus_token=True, history=1)
+    eng.prefill()
+    if args.graph:
+        eng.capture()
+    for _ in range(args.warmup):
+        eng.step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region: K device-resident steps (inputs already in HBM)
+    hist = torch.zeros((args.steps, B, 4), dtype=torch.int32, device="cuda")
+    gen0 = eng.gen_len.sum()
+    launches0 = lib.sr_launch_count()
+    lib.sr_model_profile(model.handle, 0 if args.graph else 1, None, None)
+    st = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clocks:
+        ev0.record(st)
+        for i in range(args.steps):
+            eng.step()
+            hist[i].copy_(eng.history[0])
+        ev1.record(st)
+        barrier()
+    launches = lib.sr_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    committed = int((eng.gen_len.sum() - gen0).item())
+    cat_ms = (ctypes.c_float * 7)()
+    cat_n = (ctypes.c_int32 * 7)()
+    lib.sr_model_profile(model.handle, 0, cat_ms, cat_n)
+    h = hist.cpu().numpy().reshape(-1, 4)
+    live = h[h[:, 0] + h[:, 2] > 0]
+    accepted_mean = float(live[:, 1].mean()) if len(live) else 0.0
+    committed_per_window = float(live[:, 2].mean()) if len(live) else 0.0
+    proposed_mean = float(live[:, 0].mean()) if len(live) else 0.0
+
+    # ---- e2e: same steps through the public API with host buffers each step
+    budget_h = torch.tensor(budget, dtype=torch.int32).pin_memory()
+    out_h = torch.empty((B, 4 + K + 2), dtype=torch.int32).pin_memory()
+    e2e_in = budget_h.numel() * 4
+    e2e_out = out_h.numel() * 4
+    lib.sr_model_profile(model.handle, 0, None, None)
+    gen1 = eng.gen_len.sum()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        eng.max_new.copy_(budget_h, non_blocking=True)          # H2D: per-step request budgets
+        seq_before = eng.seq_len.clone()
+        eng.step()
+        idx = (seq_before[:, None] + torch.arange(K + 2, device="cuda")[None, :]).clamp(max=eng.stride - 1)
+        res = torch.cat([eng.history[0], torch.gather(eng.tokens, 1, idx.long())], 1)
+        out_h.copy_(res, non_blocking=True)                     # D2H: outcomes + new tokens
+        st.synchronize()
+    e1.record(st)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    e2e_committed = int((eng.gen_len.sum() - gen1).item())
+
+    # ---- cross-rank reduction
+    t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device="cuda")
+    c = torch.tensor([committed, e2e_committed], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+    ms_max, e2e_max = float(t[0]), float(t[1])
+    tot_committed, tot_e2e = float(c[0]), float(c[1])
+
+    # ---- roofline of the dominant kernel family: the verify GEMMs (tensor-bound)
+    gemm_ms = sum(cat_ms[i] for i in range(5))
+    rows = B * (K + 1)
+    flops_step = 2.0 * rows * s.linear_params()
+    burst, sustained, hbm, src = peaks()
+    achieved = flops_step * args.steps / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    attn_ms = cat_ms[5]
+    step_ms = ms / args.steps
+    result = {
+        "metric": METRIC, "value": tot_committed / (ms_max * 1e-3), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init N(0,0.02) weights; keyed-stream prompt tokens; reference trace lengths)",
+        "config": {"workload": f"configs[1]: {args.model}-shaped target, batch {B}/GPU, k={K}, "
+                               "single n-gram drafter (min_n=1,max_n=3), greedy exact match, bonus token",
+                   "model": args.model, "layers": s.layers, "batch_per_gpu": B, "global_batch": B * world,
+                   "k": K, "verify_rows_per_step": rows, "prompt_len": "U[128,1024] (default_trace_spec)",
+                   "parallelism": f"prompt-sharded x{world} (no data-path collective)",
+                   "l2": "inputs larger than L2 (3.1 GB weights + paged KV per step)",
+                   "graph": bool(args.graph)},
+        "mean_accepted_length": accepted_mean,
+        "mean_proposed": proposed_mean,
+        "tokens_per_window": committed_per_window,
+        "roofline": {"bound": "tensor", "kernel": "verify GEMMs (qkv, o, gate_up+SwiGLU, down, lm_head+argmax)",
+                     "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
+                     "frac": (achieved / sustained) if achieved else None,
+                     "peak_source": f"{src} bf16_tflops_sustained (kernels timed inside the step)",
+                     "traffic": None,
+                     "algorithmic_flops_per_step": flops_step,
+                     "gemm_ms_per_step": gemm_ms / args.steps,
+                     "gemm_share_of_step": (gemm_ms / args.steps) / step_ms,
+                     "attention_ms_per_step": attn_ms / args.steps,
+                     "other_ms_per_step": cat_ms[6] / args.steps,
+                     "per_gemm_ms_per_step": {n: cat_ms[i] / args.steps for i, n in
+                                              enumerate(["qkv", "o", "gate_up", "down", "lm_head"])}},
+        "e2e": {"value": tot_e2e / (e2e_max * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": e2e_in, "d2h_bytes_per_step": e2e_out},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+    }
+    return result, (s, model, prompts)
+
+
+# -- CPU baseline (oracle port of the same path) ----------------------------------------
+
+
+def cpu_baseline(s, model, prompts, requests=2, prompt_cap=128, windows=6):
+    """Bounded sample of the same workload through the CPU oracle port."""
+    import torch
+
+    from oracle.qwen2_oracle import CachedRollout, Qwen2Oracle
+
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    w = weights_to_cpu(s, model)
+    runner = CachedRollout(Qwen2Oracle(s, w, "bf16"))
+    ps = [p[:prompt_cap].tolist() for p in prompts[:requests]]
+    seqs = runner.prefill(ps)
+    t0 = time.perf_counter()
+    committed = 0
+    for _ in range(windows):
+        for r in range(requests):
+            c, _, _ = runner.step(r, seqs[r], K)
+            committed += c
+    dt = time.perf_counter() - t0
+    return {"value": committed / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{requests} requests x {windows} windows (k={K}, n-gram) of the full "
+                      f"{s.layers}-layer {s.name} model on CPU (oracle/qwen2_oracle.py CachedRollout, "
+                      f"bf16-emulated torch, prompts truncated to {prompt_cap} tokens), {dt:.1f} s"}
+
+
+def weights_to_cpu(s, model):
+    """Canonical fp32 weights rebuilt from the device model (identical values)."""
+    w = {"embed": model.embed.float().cpu(), "final_norm": model.final_norm.cpu(), "layers": []}
+    w["lm_head"] = w["embed"] if s.tied else model.lm_head.float().cpu()
+    nq, nkv, hd, I = s.q_heads * s.head_dim, s.kv_heads * s.head_dim, s.head_dim, s.intermediate
+    for t in model.layer_tensors:
+        qkv, b = t["w_qkv"].float().cpu(), t["b_qkv"].cpu()
+        gu = t["w_gu"].float().cpu().view(I // 16, 2, 16, s.hidden)
+        w["layers"].append({
+            "ln1": t["ln1"].cpu(), "ln2": t["ln2"].cpu(),
+            "wq": qkv[:nq], "wk": qkv[nq:nq + nkv], "wv": qkv[nq + nkv:],
+            "bq": b[:nq], "bk": b[nq:nq + nkv], "bv": b[nq + nkv:],
+            "wo": t["w_o"].float().cpu(), "wg": gu[:, 0].reshape(I, s.hidden),
+            "wu": gu[:, 1].reshape(I, s.hidden), "wd": t["w_down"].float().cpu()})
+    return w
+
+
+def run_reference(args):
+    """The reference arm: the CPU implementation of the path (oracle port;
+    the reference itself is a Python simulator with no model arithmetic)."""
+    import torch
+
+    from paper_2511_16193_b200.model import init_weights, shape
+
+    s = shape(args.model, args.layers)
+    torch.set_num_threads(os.cpu_count() or 1)
+    _, prompts, _ = workload(0, args.batch, 1, s.vocab)
+    from oracle.qwen2_oracle import CachedRollout, Qwen2Oracle
+
+    w = init_weights(s, seed=0, device="cpu")
+    runner = CachedRollout(Qwen2Oracle(s, w, "bf16"))
+    del w
+    reqs = 2
+    seqs = runner.prefill([p[:128].tolist() for p in prompts[:reqs]])
+    for _ in range(max(args.warmup, 1)):
+        for r in range(reqs):
+            runner.step(r, seqs[r], K)
+    times, committed = [], 0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        for r in range(reqs):
+            c, _, _ = runner.step(r, seqs[r], K)
+            committed += c
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = committed / total
+    sample = (f"{reqs} requests x {args.steps} windows (k={K}, n-gram) through the full {s.layers}-layer "
+              f"{s.name} model, oracle port (torch CPU, bf16-emulated), prompts truncated to 128 tokens")
+    return {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic", "config": {"workload": "configs[1] bounded CPU sample", "model": s.name},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        tdist.init_process_group("nccl")
+        dist = tdist
+    result, ctx = run_ours(args, rank, world, dist)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            result["cpu_baseline"] = cpu_baseline(*ctx)
+        else:
+            result["cpu_baseline"] = None
+        print(json.dumps(result), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

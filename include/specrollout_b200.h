@@ -40,6 +40,9 @@ const char* sr_last_error(void);
 /* Number of SMs of the current device (for grid sizing by callers). */
 int sr_device_sm_count(void);
 
+/* Kernels launched by this library since load (bench evidence). */
+long long sr_launch_count(void);
+
 /* ---------------------------------------------------------------------------
  * a1/a2  Keyed draws.  Replaces `streams.stream` + `_Sim.true_token`
  * (sim.py:313-320, generate_true_sequence sim.py:45-56) and
@@ -190,6 +193,13 @@ uint64_t sr_model_workspace_bytes(const sr_model_desc* desc);
 int sr_model_create(const sr_model_desc* desc, void** handle);
 int sr_model_destroy(void* handle);
 int sr_model_forward(void* handle, const sr_forward_args* args, sr_stream_t stream);
+
+/* Launch timing: while enabled, every forward brackets its launches with
+ * CUDA events on the launching stream.  A call with ms_out/count_out set
+ * waits for the recorded work and returns per-category totals over
+ * [qkv, o, gate_up, down, lm_head, attention, other] (7 entries), then
+ * clears the record and sets the enable state for the following forwards. */
+int sr_model_profile(void* handle, int enable, float* ms_out, int32_t* count_out);
 
 /* ---------------------------------------------------------------------------
  * K3  Acceptance + Best-of-N + write-back (model mode).  Replaces

@@ -143,3 +143,67 @@ def margin(logits_row: torch.Tensor) -> float:
     """Gap between the top-1 and top-2 logit (tie safety of greedy parity)."""
     top = torch.topk(logits_row.double(), 2).values
     return float(top[0] - top[1])
+
+
+class CachedRollout:
+    """KV-cached CPU speculative rollout with the oracle's arithmetic: the CPU
+    port of the hot path timed by bench.py's cpu_baseline / --impl reference
+    legs (prefill once, then n-gram draft -> verify window -> exact-match
+    accept per request, sim.py:983-1042 semantics)."""
+
+    def __init__(self, oracle: Qwen2Oracle):
+        self.o = oracle
+        self.k_cache: list[list[torch.Tensor]] = []
+        self.v_cache: list[list[torch.Tensor]] = []
+
+    @torch.no_grad()
+    def _forward(self, req: int, tokens, start: int) -> torch.Tensor:
+        """Positions [start, start+len(tokens)) with cached keys [0, start)."""
+        o, s = self.o, self.o.s
+        T = len(tokens)
+        pos = torch.arange(start, start + T)
+        x = o.embed[torch.as_tensor(tokens, dtype=torch.long)].to(o.acc)
+        nq, nkv, hd = s.q_heads, s.kv_heads, s.head_dim
+        G = nq // nkv
+        mask = torch.ones(T, start + T, dtype=torch.bool).triu(start + 1)
+        for li, L in enumerate(o.layers):
+            h = o._norm(x, L["ln1"])
+            qkv = o._r(h @ L["wqkv"].t() + L["bqkv"])
+            q = o._rope(qkv[:, : nq * hd].view(T, nq, hd), pos)
+            k = o._rope(qkv[:, nq * hd: (nq + nkv) * hd].view(T, nkv, hd), pos)
+            v = qkv[:, (nq + nkv) * hd:].view(T, nkv, hd)
+            kc = torch.cat([self.k_cache[req][li][:start], k]) if start else k
+            vc = torch.cat([self.v_cache[req][li][:start], v]) if start else v
+            self.k_cache[req][li], self.v_cache[req][li] = kc, vc
+            kk, vv = kc.repeat_interleave(G, 1), vc.repeat_interleave(G, 1)
+            sc = torch.einsum("qhd,khd->hqk", q, kk) / float(np.sqrt(hd))
+            sc = sc.masked_fill(mask, float("-inf"))
+            p = torch.exp(sc - sc.amax(-1, keepdim=True))
+            l = p.sum(-1, keepdim=True)
+            att = torch.einsum("hqk,khd->qhd", o._r(p), vv) / l.permute(1, 0, 2)
+            x = x + o._r(att.reshape(T, nq * hd)) @ L["wo"].t()
+            h = o._norm(x, L["ln2"])
+            g, u = h @ L["wg"].t(), h @ L["wu"].t()
+            x = x + o._r(g / (1.0 + torch.exp(-g)) * u) @ L["wd"].t()
+        return o._norm(x, o.final_norm) @ o.lm_head.t()
+
+    def prefill(self, prompts) -> list[list[int]]:
+        seqs = []
+        for p in prompts:
+            self.k_cache.append([None] * len(self.o.layers))
+            self.v_cache.append([None] * len(self.o.layers))
+            lg = self._forward(len(seqs), list(p), 0)
+            seqs.append(list(p) + [int(torch.argmax(lg[-1]))])
+        return seqs
+
+    def step(self, req: int, seq: list[int], k: int, min_n=1, max_n=3, bonus=True):
+        """One speculation window for one request; returns committed tokens."""
+        d = ngram_oracle.propose(seq, min_n, max_n, k)
+        lg = self._forward(req, [seq[-1]] + d, len(seq) - 1)
+        y = [int(t) for t in torch.argmax(lg, -1)]
+        a = 0
+        while a < len(d) and d[a] == y[a]:
+            a += 1
+        c = (len(d) + (1 if bonus else 0)) if a == len(d) and d else (a + 1)
+        seq += y[:c]
+        return c, len(d), a

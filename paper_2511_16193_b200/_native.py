@@ -34,12 +34,15 @@ SIGNATURES: dict[str, list] = {
     "sr_model_create": [_vp, _vp],
     "sr_model_destroy": [_vp],
     "sr_model_forward": [_vp, _vp, _vp],
+    "sr_model_profile": [_vp, _i32, _vp, _vp],
+    "sr_launch_count": [],
     "sr_accept_commit": [_i32, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp],
     "sr_kv_commit": [_vp, _i32, _i32, _vp, _vp, _vp, _vp],
     "sr_build_verify_batch": [_i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               _vp, _vp],
 }
-_RESTYPES = {"sr_last_error": ctypes.c_char_p, "sr_model_workspace_bytes": ctypes.c_uint64}
+_RESTYPES = {"sr_last_error": ctypes.c_char_p, "sr_model_workspace_bytes": ctypes.c_uint64,
+             "sr_launch_count": ctypes.c_longlong}
 
 
 class SeqInfo(ctypes.Structure):

@@ -1,11 +1,15 @@
 // C-ABI plumbing: version, thread-local last error, device queries.
 #include "common.cuh"
 
+#include <atomic>
 #include <cstring>
 
 namespace sr {
 
 static thread_local char g_last_error[1024] = {0};
+static std::atomic<long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -19,6 +23,8 @@ void set_error(const char* fmt, ...) {
 extern "C" {
 
 int sr_version(void) { return 100; }
+
+long long sr_launch_count(void) { return sr::g_launches.load(); }
 
 const char* sr_last_error(void) { return sr::g_last_error; }
 

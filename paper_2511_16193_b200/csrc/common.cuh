@@ -13,6 +13,7 @@
 namespace sr {
 
 void set_error(const char* fmt, ...);
+void count_launch();
 
 inline int config_error(const char* what) {
   set_error("config: %s", what);
@@ -20,6 +21,7 @@ inline int config_error(const char* what) {
 }
 
 inline int check_launch(const char* kernel) {
+  count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("%s: %s", kernel, cudaGetErrorString(e));

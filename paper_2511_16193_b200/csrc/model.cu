@@ -64,7 +64,39 @@ struct Carve {
 
 }  // namespace
 
+// Per-category CUDA-event timing of the forward's launches (bench.py's
+// roofline evidence): events bracket each launch on the launching stream.
+enum ProfCat { kProfQkv, kProfO, kProfGateUp, kProfDown, kProfLmHead, kProfAttn, kProfOther, kProfCats };
+
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<int, int>> marks;  // (category, first event index)
+  size_t next = 0;
+  cudaEvent_t take() {
+    if (next == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[next++];
+  }
+  void begin(int cat, cudaStream_t st) {
+    if (!on) return;
+    marks.push_back({cat, (int)next});
+    cudaEventRecord(take(), st);
+  }
+  void end(cudaStream_t st) {
+    if (!on) return;
+    cudaEventRecord(take(), st);
+  }
+  ~Profiler() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
 struct Model {
+  Profiler prof;
   sr_model_desc d;
   std::vector<const void*> layer_ptrs;
   KvLayout kv;
@@ -234,16 +266,33 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
     SR_TRY(sr::embed_rows<bf>((const bf*)d.embed, a->token_ids, M, H, m->x, st));
     for (int l = 0; l < d.layers; ++l) {
       const void* const* w = m->layer_ptrs.data() + (size_t)l * sr::kLayerPtrs;
+      auto& P = m->prof;
+      P.begin(sr::kProfOther, st);
       SR_TRY(sr::rmsnorm_rows<bf>(m->x, (const float*)w[0], M, H, d.rms_eps, (bf*)m->h, st));
+      P.end(st);
+      P.begin(sr::kProfQkv, st);
       SR_TRY(sr::gemm_bf16_launch(m->p_qkv[l], st, M));
+      P.end(st);
+      P.begin(sr::kProfOther, st);
       SR_TRY(sr::rope_scatter<bf>((const bf*)m->qkv, a->positions, seqs, S, a->max_q_len, d.rope_cos,
                                   d.rope_sin, d.q_heads, l, m->kv, (bf*)m->q, st));
+      P.end(st);
+      P.begin(sr::kProfAttn, st);
       SR_TRY(sr::attention_bf16((const bf*)m->q, seqs, S, a->max_q_len, a->max_key, m->kv, l, d.q_heads,
                                 m->attn_part, m->partial_floats, (bf*)m->attn, st));
+      P.end(st);
+      P.begin(sr::kProfO, st);
       SR_TRY(sr::gemm_bf16_launch(m->p_o[l], st, M));
+      P.end(st);
+      P.begin(sr::kProfOther, st);
       SR_TRY(sr::rmsnorm_rows<bf>(m->x, (const float*)w[4], M, H, d.rms_eps, (bf*)m->h, st));
+      P.end(st);
+      P.begin(sr::kProfGateUp, st);
       SR_TRY(sr::gemm_bf16_launch(m->p_gu[l], st, M));
+      P.end(st);
+      P.begin(sr::kProfDown, st);
       SR_TRY(sr::gemm_bf16_launch(m->p_down[l], st, M));
+      P.end(st);
     }
     SR_TRY(sr::rmsnorm_rows<bf>(m->x, d.final_norm, M, H, d.rms_eps, (bf*)m->h, st));
     if (a->logit_rows) {
@@ -258,8 +307,12 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
       SR_CHECK_CUDA(cudaMemcpy2DAsync(a->out, (size_t)d.vocab * 4, m->logits, vpad * 4, (size_t)d.vocab * 4, R,
                                       cudaMemcpyDeviceToDevice, st));
     } else {
+      m->prof.begin(sr::kProfLmHead, st);
       SR_TRY(sr::gemm_bf16_launch(m->p_lm_argmax, st, R));
+      m->prof.end(st);
+      m->prof.begin(sr::kProfOther, st);
       SR_TRY(sr::argmax_reduce(m->part_val, m->part_idx, R, m->lm_tiles, (int32_t*)a->out, a->out_val, st));
+      m->prof.end(st);
     }
   } else {
     SR_TRY(sr::embed_rows<float>((const float*)d.embed, a->token_ids, M, H, m->x, st));
@@ -295,6 +348,29 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
     if (a->output != 1) SR_TRY(sr::argmax_rows(logits, R, d.vocab, d.vocab, (int32_t*)a->out, a->out_val, st));
   }
 #undef SR_TRY
+  return SR_OK;
+}
+
+int sr_model_profile(void* handle, int enable, float* ms_out, int32_t* count_out) {
+  SR_REQUIRE(handle, "null model");
+  Model* m = reinterpret_cast<Model*>(handle);
+  auto& P = m->prof;
+  if (ms_out || count_out) {
+    for (int c = 0; c < sr::kProfCats; ++c) {
+      if (ms_out) ms_out[c] = 0.0f;
+      if (count_out) count_out[c] = 0;
+    }
+    if (!P.marks.empty()) SR_CHECK_CUDA(cudaEventSynchronize(P.pool[P.next - 1]));
+    for (auto& mk : P.marks) {
+      float ms = 0.0f;
+      SR_CHECK_CUDA(cudaEventElapsedTime(&ms, P.pool[mk.second], P.pool[mk.second + 1]));
+      if (ms_out) ms_out[mk.first] += ms;
+      if (count_out) count_out[mk.first] += 1;
+    }
+  }
+  P.marks.clear();
+  P.next = 0;
+  P.on = enable != 0;
   return SR_OK;
 }
 
