@@ -47,7 +47,7 @@ PEAKS = ROOT / "MEASURED_PEAKS.json"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=BATCH, help="prompts per GPU")
@@ -55,6 +55,12 @@ def parse():
     ap.add_argument("--layers", type=int, default=None, help="debug only: truncate depth")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action="store_true", help="replay steps from a CUDA graph")
+    ap.add_argument("--drafter", choices=["synthetic", "ngram"], default="synthetic",
+                    help="synthetic: reference accept_draw law over the target's own greedy "
+                         "continuation (SURVEY 7.1e); ngram: vLLM prompt lookup")
+    ap.add_argument("--accept-method", default="draft-0.5b",
+                    help="reference drafting method whose latent acceptance/keyed draws drive the "
+                         "synthetic drafter (scenarios.METHODS)")
     return ap.parse_args()
 
 
@@ -134,7 +140,7 @@ def run_ours(args, rank, world, dist):
     import torch
 
     from paper_2511_16193_b200 import _native
-    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine
+    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine, SyntheticDrafter
     from paper_2511_16193_b200.model import DeviceModel, init_weights, shape
 
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
@@ -149,11 +155,24 @@ def run_ours(args, rank, world, dist):
                         max_tokens=max(B * (K + 1), 2048), max_seqs=B)
     del w
     torch.cuda.empty_cache()
-    eng = RolloutEngine(model, prompts, budget, k=K, drafters=(NgramDrafter(1, 3),),
-                        bonus_token=True, history=1)
+    # untimed: the target's greedy continuation (plain decode), which the
+    # synthetic drafter proposes under the reference's keyed acceptance law
+    plain = RolloutEngine(model, prompts, budget, k=0, history=1)
+    plain.prefill()
+    plain.run()
+    truth = plain.outputs()
+    ngram_probe = None
+    if args.drafter == "synthetic":
+        drafter = SyntheticDrafter(truth, trace, args.accept_method, seed=0)
+        ngram_probe = probe_ngram(RolloutEngine, NgramDrafter, model, prompts, budget, truth)
+    else:
+        drafter = NgramDrafter(1, 3)
+    del plain
+    eng = RolloutEngine(model, prompts, budget, k=K, drafters=(drafter,), bonus_token=True, history=1)
     eng.prefill()
     if args.graph:
         eng.capture()
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", 0))).__enter__()
     for _ in range(args.warmup):
         eng.step()
     torch.cuda.synchronize()
@@ -171,19 +190,20 @@ def run_ours(args, rank, world, dist):
     st = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clocks:
-        ev0.record(st)
-        for i in range(args.steps):
-            eng.step()
-            hist[i].copy_(eng.history[0])
-        ev1.record(st)
-        barrier()
+    ev0.record(st)
+    for i in range(args.steps):
+        eng.step()
+        hist[i].copy_(eng.history[0])
+    ev1.record(st)
+    barrier()
+    clocks.__exit__(None, None, None)
     launches = lib.sr_launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
     committed = int((eng.gen_len.sum() - gen0).item())
-    cat_ms = (ctypes.c_float * 7)()
-    cat_n = (ctypes.c_int32 * 7)()
+    cat_ms = (ctypes.c_float * 8)()
+    cat_n = (ctypes.c_int32 * 8)()
     lib.sr_model_profile(model.handle, 0, cat_ms, cat_n)
+    outs_ok = all(o == t[: len(o)] for o, t in zip(eng.outputs(), truth))
     h = hist.cpu().numpy().reshape(-1, 4)
     live = h[h[:, 0] + h[:, 2] > 0]
     accepted_mean = float(live[:, 1].mean()) if len(live) else 0.0
@@ -228,7 +248,7 @@ def run_ours(args, rank, world, dist):
     flops_step = 2.0 * rows * s.linear_params()
     burst, sustained, hbm, src = peaks()
     achieved = flops_step * args.steps / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
-    attn_ms = cat_ms[5]
+    attn_ms = cat_ms[5] + cat_ms[7]
     step_ms = ms / args.steps
     result = {
         "metric": METRIC, "value": tot_committed / (ms_max * 1e-3), "unit": UNIT,
@@ -244,6 +264,11 @@ def run_ours(args, rank, world, dist):
                    "l2": "inputs larger than L2 (3.1 GB weights + paged KV per step)",
                    "graph": bool(args.graph)},
         "mean_accepted_length": accepted_mean,
+        "drafter": (f"synthetic: target's greedy continuation, accepted iff reference keyed "
+                    f"accept_draw u < latent_accept['{args.accept_method}'] (sim.py:322-336)"
+                    if args.drafter == "synthetic" else "n-gram (vLLM prompt lookup, min_n=1, max_n=3)"),
+        "outputs_equal_plain_greedy": outs_ok,
+        "ngram_probe": ngram_probe,
         "mean_proposed": proposed_mean,
         "tokens_per_window": committed_per_window,
         "roofline": {"bound": "tensor", "kernel": "verify GEMMs (qkv, o, gate_up+SwiGLU, down, lm_head+argmax)",
@@ -255,6 +280,7 @@ def run_ours(args, rank, world, dist):
                      "gemm_ms_per_step": gemm_ms / args.steps,
                      "gemm_share_of_step": (gemm_ms / args.steps) / step_ms,
                      "attention_ms_per_step": attn_ms / args.steps,
+                     "attention_combine_ms_per_step": cat_ms[7] / args.steps,
                      "other_ms_per_step": cat_ms[6] / args.steps,
                      "per_gemm_ms_per_step": {n: cat_ms[i] / args.steps for i, n in
                                               enumerate(["qkv", "o", "gate_up", "down", "lm_head"])}},
@@ -264,6 +290,23 @@ def run_ours(args, rank, world, dist):
         "clocks": clocks.summary(),
     }
     return result, (s, model, prompts)
+
+
+def probe_ngram(RolloutEngine, NgramDrafter, model, prompts, budget, truth, steps=8):
+    """Measured acceptance of the real n-gram drafter on this workload (not timed)."""
+    import torch
+
+    eng = RolloutEngine(model, prompts, budget, k=K, drafters=(NgramDrafter(1, 3),), bonus_token=True,
+                        history=steps)
+    eng.prefill()
+    for _ in range(steps):
+        eng.step()
+    torch.cuda.synchronize()
+    h = eng.outcome_rows().reshape(-1, 4)
+    live = h[h[:, 0] + h[:, 2] > 0]
+    same = all(o == t[: len(o)] for o, t in zip(eng.outputs(), truth))
+    return {"steps": steps, "mean_proposed": float(live[:, 0].mean()), "mean_accepted": float(live[:, 1].mean()),
+            "tokens_per_window": float(live[:, 2].mean()), "outputs_equal_plain_greedy": same}
 
 
 # -- CPU baseline (oracle port of the same path) ----------------------------------------

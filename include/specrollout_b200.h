@@ -197,7 +197,8 @@ int sr_model_forward(void* handle, const sr_forward_args* args, sr_stream_t stre
 /* Launch timing: while enabled, every forward brackets its launches with
  * CUDA events on the launching stream.  A call with ms_out/count_out set
  * waits for the recorded work and returns per-category totals over
- * [qkv, o, gate_up, down, lm_head, attention, other] (7 entries), then
+ * [qkv, o, gate_up, down, lm_head, attention, other, attention_combine]
+ * (8 entries), then
  * clears the record and sets the enable state for the following forwards. */
 int sr_model_profile(void* handle, int enable, float* ms_out, int32_t* count_out);
 
@@ -222,6 +223,17 @@ int sr_accept_commit(int num_requests, int num_drafters, const void* seqs, const
 /* Copy the winning branch's window KV into the paged cache (all layers). */
 int sr_kv_commit(void* model, int num_requests, int num_drafters, const void* seqs,
                  const int32_t* outcome, const int32_t* bon, sr_stream_t stream);
+
+/* Reference-acceptance drafter: for output position
+ * g = gen_len[b] + j propose truth[b, g] (the target's own greedy token) when
+ * uniforms[b, g] < accept_p[b] -- the reference's keyed `accept_draw`
+ * (sim.py:322-336) -- else (truth + 1) % vocab.  Exact-match verification then
+ * accepts exactly the reference's `_verify_prefix` run (sim.py:977-981).
+ * drafts [B, k] (-1 padded), ndraft [B] = min(k, truth_len - gen_len). */
+int sr_synthetic_draft(int num_requests, int k, const int32_t* truth, int64_t truth_stride,
+                       const int32_t* truth_len, const double* uniforms, int64_t u_stride,
+                       const double* accept_p, const int32_t* gen_len, int vocab, int32_t* drafts,
+                       int32_t* ndraft, sr_stream_t stream);
 
 /* Next verify batch from device state: for drafter n of request b, rows
  * [(b*N+n)*(k+1), +nd+1) = last committed token then the drafts.  drafts

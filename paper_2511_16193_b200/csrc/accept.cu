@@ -141,6 +141,33 @@ __global__ void build_verify_kernel(int B, int N, int k, const int32_t* __restri
   }
 }
 
+// Reference-acceptance drafter: proposes the target's own continuation
+// truth[g] for output position g when the reference's keyed acceptance draw
+// u[g] < p (sim.py:322-336), else a deterministic wrong token, so the
+// exact-match verifier accepts exactly the reference's `_verify_prefix` run
+// (sim.py:977-981) while every committed token is a real model output.
+__global__ void synthetic_draft_kernel(int B, int k, const int32_t* __restrict__ truth, int64_t truth_stride,
+                                       const int32_t* __restrict__ truth_len, const double* __restrict__ u,
+                                       int64_t u_stride, const double* __restrict__ p,
+                                       const int32_t* __restrict__ gen_len, int vocab,
+                                       int32_t* __restrict__ drafts, int32_t* __restrict__ ndraft) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int g0 = gen_len[b];
+  const int nd = max(0, min(k, truth_len[b] - g0));
+  const double pb = p[b];
+  for (int j = 0; j < k; ++j) {
+    int tok = -1;
+    if (j < nd) {
+      const int g = g0 + j;
+      const int t = truth[(int64_t)b * truth_stride + g];
+      tok = u[(int64_t)b * u_stride + g] < pb ? t : (t + 1) % vocab;
+    }
+    drafts[(int64_t)b * k + j] = tok;
+  }
+  ndraft[b] = nd;
+}
+
 }  // namespace
 
 int kv_commit(int B, int N, const SeqInfo* seqs, const int32_t* outcome, const int32_t* bon,
@@ -170,6 +197,19 @@ extern "C" int sr_accept_commit(int num_requests, int num_drafters, const void* 
       num_requests, num_drafters, reinterpret_cast<const sr::SeqInfo*>(seqs), token_ids, target, tokens,
       tok_stride, seq_len, gen_len, max_new, bonus_token, outcome, bon);
   return sr::check_launch("accept_commit_kernel");
+}
+
+extern "C" int sr_synthetic_draft(int num_requests, int k, const int32_t* truth, int64_t truth_stride,
+                                  const int32_t* truth_len, const double* uniforms, int64_t u_stride,
+                                  const double* accept_p, const int32_t* gen_len, int vocab, int32_t* drafts,
+                                  int32_t* ndraft, sr_stream_t stream) {
+  SR_REQUIRE(num_requests >= 0 && k >= 1 && vocab >= 2, "bad synthetic draft shape");
+  if (num_requests == 0) return SR_OK;
+  SR_REQUIRE(truth && truth_len && uniforms && accept_p && gen_len && drafts && ndraft, "null pointer");
+  sr::synthetic_draft_kernel<<<sr::ceil_div(num_requests, 128), 128, 0, (cudaStream_t)stream>>>(
+      num_requests, k, truth, truth_stride, truth_len, uniforms, u_stride, accept_p, gen_len, vocab, drafts,
+      ndraft);
+  return sr::check_launch("synthetic_draft_kernel");
 }
 
 extern "C" int sr_build_verify_batch(int num_requests, int num_drafters, int k, const int32_t* tokens,

@@ -1,21 +1,22 @@
 // K2: verification attention over the paged KV cache.
 //
-// One CTA = (sequence, kv head, query block of 64 rows, KV split).  Rows are
+// One CTA = (sequence, kv head, query block of 32 rows, KV split).  Rows are
 // (window position j, group head g) pairs, r = j*G + g, so all query heads
 // sharing a kv head read each K/V tile once (GQA).  Keys are walked in
 // tiles of 64 *absolute* positions (tile t = keys [64t, 64t+64)); a key comes
 // from the paged cache when it is committed (pos < ctx_len) or written in
 // place, else from the drafter-branch window buffer.  Splits are fixed
-// 1024-key ranges merged by a combine kernel in split order.  Because the
+// 512-key ranges merged by a combine kernel in split order.  Because the
 // tiling depends only on absolute positions, a query's arithmetic is the
 // same in a 5-position verify window and in a 1-position decode step: the
 // speculative and plain paths produce bit-identical logits.
 //
-// Per tile: cp.async (16-byte, XOR-swizzled) double-buffered K/V staging;
-// S = Q K^T with mma.sync m16n8k16 bf16 (warp w owns keys 16w..16w+15);
-// fp32 online softmax in shared memory (2 threads per row, exp2); O += P V
-// with mma.sync (warp w owns head-dim columns w*HD/4..).  HBM-bound: the
-// kernel's algorithmic bytes are the K/V tiles it reads.
+// Per tile: 3-stage cp.async ring (16-byte, XOR-swizzled) for K/V; warp w
+// owns keys 16w..16w+15 of each tile: S = Q K^T with mma.sync m16n8k16 bf16,
+// warp-level online softmax in registers (quad shuffles, exp2), P re-used as
+// the A fragment of O += P V without touching shared memory.  The 4 warps'
+// states merge once per CTA.  HBM-bound: the kernel's algorithmic bytes are
+// the K/V tiles it reads.
 #include "common.cuh"
 #include "layers.cuh"
 
@@ -26,8 +27,9 @@ namespace sr {
 namespace {
 
 constexpr int kKT = 64;          // keys per tile (= page size)
-constexpr int kRows = 64;        // query rows per CTA
-constexpr int kSplitTiles = 16;  // tiles per KV split (1024 keys)
+constexpr int kRows = 32;        // query rows per CTA
+constexpr int kSplitTiles = 8;   // tiles per KV split (512 keys)
+constexpr int kStages = 3;       // cp.async ring depth
 constexpr int kAttnThreads = 128;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -36,7 +38,8 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -72,26 +75,28 @@ struct AttnArgs {
   float* part_o;   // [S*nkv, qblocks, splits, 64, HD]
   float* part_ml;  // [S*nkv, qblocks, splits, 64, 2]
   int qblocks, splits;
+  __nv_bfloat16* out;  // [M, nq, HD]
 };
 
 __device__ __forceinline__ int block_max_key(const SeqInfo& sq, int r0, int rows, int G) {
   return sq.ctx_len + (r0 + rows - 1) / G;
 }
 
+// FA2-style split-K inside the CTA: warp w owns keys [16w, 16w+16) of every
+// 64-key tile, keeps its own online-softmax state and O accumulator in
+// registers (no block barrier inside the math), and the 4 warps merge in a
+// fixed order at the end.  One __syncthreads per tile guards the 3-stage
+// cp.async ring.
 template <int HD>
 __global__ void __launch_bounds__(kAttnThreads)
 attn_bf16_kernel(AttnArgs A) {
-  constexpr int CH = HD / 8;                 // 16-byte chunks per row
-  constexpr int NT = HD / 32;                // n8 tiles of O per warp
+  constexpr int CH = HD / 8;       // 16-byte chunks per row
+  constexpr int NO = HD / 8;       // n8 tiles of O per m-tile
+  constexpr int MT = kRows / 16;   // m-tiles per CTA (2)
+  constexpr uint32_t kTileBytes = kKT * HD * 2;
   extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + kRows * HD * 2;         // [2][64][HD]
-  uint8_t* sV = sK + 2 * kKT * HD * 2;       // [2][64][HD]
-  float* sS = reinterpret_cast<float*>(sV + 2 * kKT * HD * 2);   // [64][68]
-  __nv_bfloat16* sP = reinterpret_cast<__nv_bfloat16*>(sS + kRows * 68);  // [64][72]
-  float* sAlpha = reinterpret_cast<float*>(sP + kRows * 72);
-  float* sM = sAlpha + kRows;
-  float* sL = sM + kRows;
+  uint8_t* sQ = smem;                              // [kRows][HD]
+  uint8_t* sKV = sQ + kRows * HD * 2;              // [stages][K tile, V tile]
 
   const int nkv = A.kv.kv_heads;
   const int sp = blockIdx.x, qb = blockIdx.y;
@@ -116,198 +121,232 @@ attn_bf16_kernel(AttnArgs A) {
   const int32_t* btab = A.kv.block_table + (int64_t)sq.request * A.kv.max_pages;
   const int psz = A.kv.page;
 
-  // ---- Q block -> smem (zeros for padding rows)
   for (int e = tid; e < kRows * CH; e += kAttnThreads) {
     const int r = e / CH, c = e % CH;
     uint8_t* dst = sQ + swz<HD>(r, c);
     if (r < rows) {
       const int gr = r0 + r, j = gr / G, g = gr % G;
-      const __nv_bfloat16* src = A.q + ((int64_t)(sq.q_start + j) * A.nq + h * G + g) * HD + c * 8;
-      cp_async16(dst, src);
+      cp_async16(dst, A.q + ((int64_t)(sq.q_start + j) * A.nq + h * G + g) * HD + c * 8);
     } else {
       *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
     }
   }
-  if (tid < kRows) {
-    sM[tid] = -INFINITY;
-    sL[tid] = 0.0f;
-  }
 
   auto load_tile = [&](int t, int stage) {
-    uint8_t* k_dst = sK + stage * kKT * HD * 2;
-    uint8_t* v_dst = sV + stage * kKT * HD * 2;
-    for (int e = tid; e < kKT * CH; e += kAttnThreads) {
-      const int r = e / CH, c = e % CH;
-      const int kp = t * kKT + r;
-      const uint32_t off = swz<HD>(r, c);
-      if (kp > max_key) {
-        *reinterpret_cast<uint4*>(k_dst + off) = make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(v_dst + off) = make_uint4(0, 0, 0, 0);
-        continue;
+    if (t < t_end) {
+      uint8_t* k_dst = sKV + stage * 2 * kTileBytes;
+      uint8_t* v_dst = k_dst + kTileBytes;
+      const int last = t * kKT + kKT - 1;
+      if (last <= max_key && (sq.branch < 0 || last < sq.ctx_len)) {
+        // fast path: the tile is exactly one committed page -> two contiguous
+        // 16 KB blocks (K, V of head h); uniform base, unrolled copies
+        const __nv_bfloat16* kb = cache + ((int64_t)btab[t] * 2 * nkv + h) * psz * HD;
+        const __nv_bfloat16* vb = kb + (int64_t)nkv * psz * HD;
+#pragma unroll
+        for (int i = 0; i < kKT * CH / kAttnThreads; ++i) {
+          const int e = tid + i * kAttnThreads;
+          const int r = e / CH, c = e % CH;
+          const uint32_t off = swz<HD>(r, c);
+          cp_async16(k_dst + off, kb + e * 8);
+          cp_async16(v_dst + off, vb + e * 8);
+        }
+        cp_async_commit();
+        return;
       }
-      const __nv_bfloat16* ksrc;
-      int64_t vstep;
-      if (sq.branch < 0 || kp < sq.ctx_len) {
-        const int page = btab[kp / psz];
-        ksrc = cache + (((int64_t)page * 2 * nkv + h) * psz + kp % psz) * HD;
-        vstep = (int64_t)nkv * psz * HD;
-      } else {
-        ksrc = win + (((int64_t)sq.branch * 2 * nkv + h) * A.kv.window_max + (kp - sq.ctx_len)) * HD;
-        vstep = (int64_t)nkv * A.kv.window_max * HD;
+      for (int e = tid; e < kKT * CH; e += kAttnThreads) {
+        const int r = e / CH, c = e % CH;
+        const int kp = t * kKT + r;
+        const uint32_t off = swz<HD>(r, c);
+        if (kp > max_key) {
+          *reinterpret_cast<uint4*>(k_dst + off) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(v_dst + off) = make_uint4(0, 0, 0, 0);
+          continue;
+        }
+        const __nv_bfloat16* ksrc;
+        int64_t vstep;
+        if (sq.branch < 0 || kp < sq.ctx_len) {
+          const int page = btab[kp / psz];
+          ksrc = cache + (((int64_t)page * 2 * nkv + h) * psz + kp % psz) * HD;
+          vstep = (int64_t)nkv * psz * HD;
+        } else {
+          ksrc = win + (((int64_t)sq.branch * 2 * nkv + h) * A.kv.window_max + (kp - sq.ctx_len)) * HD;
+          vstep = (int64_t)nkv * A.kv.window_max * HD;
+        }
+        cp_async16(k_dst + off, ksrc + c * 8);
+        cp_async16(v_dst + off, ksrc + vstep + c * 8);
       }
-      cp_async16(k_dst + off, ksrc + c * 8);
-      cp_async16(v_dst + off, ksrc + vstep + c * 8);
     }
-    cp_async_commit();
+    cp_async_commit();  // always one group per tile slot: simple wait counting
   };
 
-  float o[4][NT][4];
+  // per-thread state: rows g=lane/4 and g+8 of each m-tile
+  float o[MT][NO][4];
+  float m_run[MT][2], l_run[MT][2];
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+  for (int mt = 0; mt < MT; ++mt) {
+    m_run[mt][0] = m_run[mt][1] = -INFINITY;
+    l_run[mt][0] = l_run[mt][1] = 0.0f;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+    for (int nt = 0; nt < NO; ++nt)
 #pragma unroll
       for (int i = 0; i < 4; ++i) o[mt][nt][i] = 0.0f;
+  }
+  // query position of this thread's rows (for the causal mask)
+  int qpos[MT][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi) {
+      const int r = mt * 16 + (lane >> 2) + hi * 8;
+      qpos[mt][hi] = r < rows ? sq.ctx_len + (r0 + r) / G : -1;  // -1: padding row, all masked
+    }
 
   load_tile(t_begin, 0);
+  load_tile(t_begin + 1, 1);
   const uint32_t q_base = (uint32_t)__cvta_generic_to_shared(sQ);
   for (int t = t_begin; t < t_end; ++t) {
-    const int stage = (t - t_begin) & 1;
-    cp_async_wait0();
-    __syncthreads();  // tile t (and Q) visible; previous P/alpha consumers done
-    if (t + 1 < t_end) load_tile(t + 1, stage ^ 1);
-    const uint32_t k_base = (uint32_t)__cvta_generic_to_shared(sK + stage * kKT * HD * 2);
-    const uint32_t v_base = (uint32_t)__cvta_generic_to_shared(sV + stage * kKT * HD * 2);
+    const int stage = (t - t_begin) % kStages;
+    cp_async_wait<kStages - 2>();
+    __syncthreads();  // tile t visible to all; every warp is done with tile t-1's slot
+    load_tile(t + 2, (t - t_begin + 2) % kStages);
+    const uint32_t k_base = (uint32_t)__cvta_generic_to_shared(sKV + stage * 2 * kTileBytes);
+    const uint32_t v_base = k_base + kTileBytes;
+    const int key0 = t * kKT + warp * 16;
 
-    // ---- S = Q K^T for keys [16w, 16w+16)
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
+    for (int mt = 0; mt < MT; ++mt) {
       if (mt >= mtv) break;
-      float acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+      // S = Q K^T for this warp's 16 keys
+      float sacc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk) {
         uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
-        {
-          const int mi = lane >> 3;
-          const int row = mt * 16 + (mi & 1) * 8 + (lane & 7);
-          ldsm_x4(q_base + swz<HD>(row, kk * 2 + (mi >> 1)), a0, a1, a2, a3);
-        }
-        {
-          const int mi = lane >> 3;
-          const int key = warp * 16 + (mi >> 1) * 8 + (lane & 7);
-          ldsm_x4(k_base + swz<HD>(key, kk * 2 + (mi & 1)), b0, b1, b2, b3);
-        }
-        mma_bf16(acc[0], a0, a1, a2, a3, b0, b1);
-        mma_bf16(acc[1], a0, a1, a2, a3, b2, b3);
+        const int mi = lane >> 3;
+        ldsm_x4(q_base + swz<HD>(mt * 16 + (mi & 1) * 8 + (lane & 7), kk * 2 + (mi >> 1)), a0, a1, a2, a3);
+        ldsm_x4(k_base + swz<HD>(warp * 16 + (mi >> 1) * 8 + (lane & 7), kk * 2 + (mi & 1)), b0, b1, b2, b3);
+        mma_bf16(sacc[0], a0, a1, a2, a3, b0, b1);
+        mma_bf16(sacc[1], a0, a1, a2, a3, b2, b3);
       }
+      // mask + scale, row max over the quad
+      float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int r = mt * 16 + (lane >> 2) + (i >> 1) * 8;
-          const int col = warp * 16 + nt * 8 + 2 * (lane & 3) + (i & 1);
-          const int kp = t * kKT + col;
-          const int qpos = sq.ctx_len + (r0 + r) / G;
-          const bool ok = r < rows && kp <= qpos;
-          sS[r * 68 + col] = ok ? acc[nt][i] * A.scale_log2 : -INFINITY;
+          const int kp = key0 + nt * 8 + 2 * (lane & 3) + (i & 1);
+          const int hi = i >> 1;
+          const float v = kp <= qpos[mt][hi] ? sacc[nt][i] * A.scale_log2 : -INFINITY;
+          sacc[nt][i] = v;
+          mx[hi] = fmaxf(mx[hi], v);
         }
-    }
-    __syncthreads();
-
-    // ---- online softmax: 2 threads per row
-    {
-      const int r = tid >> 1, half = tid & 1;
-      if (r < mtv * 16) {
-        const float* srow = sS + r * 68 + half * 32;
-        float mx = -INFINITY;
+      uint32_t pa[4];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) mx = fmaxf(mx, srow[c]);
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        const float m_old = sM[r];
-        const float m_new = fmaxf(m_old, mx);
+      for (int hi = 0; hi < 2; ++hi) {
+        mx[hi] = fmaxf(mx[hi], __shfl_xor_sync(0xffffffffu, mx[hi], 1));
+        mx[hi] = fmaxf(mx[hi], __shfl_xor_sync(0xffffffffu, mx[hi], 2));
+        const float m_new = fmaxf(m_run[mt][hi], mx[hi]);
         const float m_use = m_new == -INFINITY ? 0.0f : m_new;
-        float sum = 0.0f;
-        __nv_bfloat16* prow = sP + r * 72 + half * 32;
+        const float alpha = exp2f(m_run[mt][hi] - m_use);
+        m_run[mt][hi] = m_new;
+        float rs = 0.0f;
+        float p[4];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const float p = exp2f(srow[c] - m_use);
-          prow[c] = __float2bfloat16_rn(p);
-          sum += p;
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            p[nt * 2 + c] = exp2f(sacc[nt][hi * 2 + c] - m_use);
+            rs += p[nt * 2 + c];
+          }
+        l_run[mt][hi] = l_run[mt][hi] * alpha + rs;
+#pragma unroll
+        for (int nt = 0; nt < NO; ++nt) {
+          o[mt][nt][hi * 2] *= alpha;
+          o[mt][nt][hi * 2 + 1] *= alpha;
         }
-        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-        const float alpha = exp2f(m_old - m_use);
-        const float l_old = sL[r];
-        __syncwarp();
-        if (half == 0) {
-          sM[r] = m_new;
-          sL[r] = l_old * alpha + sum;
-          sAlpha[r] = alpha;
-        }
+        // C fragment -> A fragment (k = this warp's 16 keys)
+        __nv_bfloat162 lo = __floats2bfloat162_rn(p[0], p[1]);
+        __nv_bfloat162 hi2 = __floats2bfloat162_rn(p[2], p[3]);
+        pa[hi] = *reinterpret_cast<uint32_t*>(&lo);       // a0 (row g) / a1 (row g+8)
+        pa[2 + hi] = *reinterpret_cast<uint32_t*>(&hi2);  // a2 / a3
+      }
+      // O += P V over the warp's 16 keys
+#pragma unroll
+      for (int np = 0; np < NO / 2; ++np) {
+        uint32_t b0, b1, b2, b3;
+        const int mi = lane >> 3;
+        ldsm_x4_t(v_base + swz<HD>(warp * 16 + (mi & 1) * 8 + (lane & 7), np * 2 + (mi >> 1)), b0, b1, b2, b3);
+        mma_bf16(o[mt][2 * np], pa[0], pa[1], pa[2], pa[3], b0, b1);
+        mma_bf16(o[mt][2 * np + 1], pa[0], pa[1], pa[2], pa[3], b2, b3);
       }
     }
-    __syncthreads();
+  }
+  cp_async_wait<0>();
+  __syncthreads();
 
-    // ---- O = alpha * O + P V for head-dim columns [w*HD/4, (w+1)*HD/4)
-    const uint32_t p_base = (uint32_t)__cvta_generic_to_shared(sP);
+  // ---- merge the 4 warps (fixed order) through smem, write the split partial
+  float* sO = reinterpret_cast<float*>(sKV);                 // [4][kRows][HD]
+  float* sML = sO + 4 * kRows * HD;                          // [4][kRows][2]
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      if (mt >= mtv) break;
-      const float a_lo = sAlpha[mt * 16 + (lane >> 2)], a_hi = sAlpha[mt * 16 + (lane >> 2) + 8];
+  for (int mt = 0; mt < MT; ++mt) {
+    if (mt >= mtv) break;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        o[mt][nt][0] *= a_lo; o[mt][nt][1] *= a_lo;
-        o[mt][nt][2] *= a_hi; o[mt][nt][3] *= a_hi;
+    for (int hi = 0; hi < 2; ++hi) {
+      float l = l_run[mt][hi];
+      l += __shfl_xor_sync(0xffffffffu, l, 1);
+      l += __shfl_xor_sync(0xffffffffu, l, 2);
+      const int r = mt * 16 + (lane >> 2) + hi * 8;
+      if ((lane & 3) == 0) {
+        sML[(warp * kRows + r) * 2] = m_run[mt][hi];
+        sML[(warp * kRows + r) * 2 + 1] = l;
       }
 #pragma unroll
-      for (int kk = 0; kk < kKT / 16; ++kk) {
-        uint32_t a0, a1, a2, a3;
-        {
-          const int mi = lane >> 3;
-          const int row = mt * 16 + (mi & 1) * 8 + (lane & 7);
-          const int col = kk * 16 + (mi >> 1) * 8;
-          ldsm_x4(p_base + (uint32_t)(row * 72 + col) * 2, a0, a1, a2, a3);
-        }
-#pragma unroll
-        for (int np = 0; np < NT / 2; ++np) {
-          uint32_t b0, b1, b2, b3;
-          const int mi = lane >> 3;
-          const int key = kk * 16 + (mi & 1) * 8 + (lane & 7);
-          const int dim0 = warp * (HD / 4) + np * 16 + (mi >> 1) * 8;
-          ldsm_x4_t(v_base + swz<HD>(key, dim0 / 8), b0, b1, b2, b3);
-          mma_bf16(o[mt][2 * np], a0, a1, a2, a3, b0, b1);
-          mma_bf16(o[mt][2 * np + 1], a0, a1, a2, a3, b2, b3);
-        }
+      for (int nt = 0; nt < NO; ++nt) {
+        const int col = nt * 8 + 2 * (lane & 3);
+        *reinterpret_cast<float2*>(&sO[(warp * kRows + r) * HD + col]) =
+            make_float2(o[mt][nt][hi * 2], o[mt][nt][hi * 2 + 1]);
       }
     }
   }
   __syncthreads();
-
-  // ---- partials
   const int64_t pidx = ((int64_t)blockIdx.z * A.qblocks + qb) * A.splits + sp;
   float* po = A.part_o + pidx * kRows * HD;
+  float* pml = A.part_ml + pidx * kRows * 2;
+  // A block whose keys fit one split finishes here: out = O / l is exactly
+  // what the combine computes for a single split (weight exp2(0) = 1).
+  const bool single = ntiles <= kSplitTiles;
+  for (int e = tid; e < rows * HD; e += kAttnThreads) {
+    const int r = e / HD, d = e % HD;
+    float M = -INFINITY;
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
-    if (mt >= mtv) break;
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, sML[(w * kRows + r) * 2]);
+    const float Mu = M == -INFINITY ? 0.0f : M;
+    float acc = 0.0f, l = 0.0f;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const int col = warp * (HD / 4) + nt * 8 + 2 * (lane & 3);
-      const int r = mt * 16 + (lane >> 2);
-      *reinterpret_cast<float2*>(po + r * HD + col) = make_float2(o[mt][nt][0], o[mt][nt][1]);
-      *reinterpret_cast<float2*>(po + (r + 8) * HD + col) = make_float2(o[mt][nt][2], o[mt][nt][3]);
+    for (int w = 0; w < 4; ++w) {
+      const float wt = exp2f(sML[(w * kRows + r) * 2] - Mu);
+      acc += wt * sO[(w * kRows + r) * HD + d];
+      l += wt * sML[(w * kRows + r) * 2 + 1];
     }
-  }
-  if (tid < kRows) {
-    float* pml = A.part_ml + pidx * kRows * 2;
-    pml[tid * 2] = sM[tid];
-    pml[tid * 2 + 1] = sL[tid];
+    if (single) {
+      const int gr = r0 + r, j = gr / G, g = gr % G;
+      A.out[((int64_t)(sq.q_start + j) * A.nq + h * G + g) * HD + d] = __float2bfloat16_rn(acc / l);
+      continue;
+    }
+    po[r * HD + d] = acc;
+    if (d == 0) {
+      pml[r * 2] = M;
+      pml[r * 2 + 1] = l;
+    }
   }
 }
 
+// Multi-split blocks only: one thread per (row, head-dim) output element,
+// splits merged in split order.
 template <int HD>
-__global__ void __launch_bounds__(HD)
-attn_combine_kernel(AttnArgs A, __nv_bfloat16* out) {
+__global__ void __launch_bounds__(256)
+attn_combine_kernel(AttnArgs A) {
   const int nkv = A.kv.kv_heads;
-  const int qb = blockIdx.x, z = blockIdx.y;
+  const int qb = blockIdx.y, z = blockIdx.z;
   const int s = z / nkv, h = z % nkv;
   const SeqInfo sq = A.seqs[s];
   const int G = A.G;
@@ -316,22 +355,22 @@ attn_combine_kernel(AttnArgs A, __nv_bfloat16* out) {
   if (r0 >= rows_total) return;
   const int rows = min(kRows, rows_total - r0);
   const int ntiles = block_max_key(sq, r0, rows, G) / kKT + 1;
+  if (ntiles <= kSplitTiles) return;  // written directly by the attention kernel
   const int nsplit = (ntiles + kSplitTiles - 1) / kSplitTiles;
-  const int d = threadIdx.x;
-  for (int r = 0; r < rows; ++r) {
-    const int64_t base = ((int64_t)z * A.qblocks + qb) * A.splits;
-    float M = -INFINITY;
-    for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, A.part_ml[((base + sp) * kRows + r) * 2]);
-    float den = 0.0f, num = 0.0f;
-    for (int sp = 0; sp < nsplit; ++sp) {
-      const float m = A.part_ml[((base + sp) * kRows + r) * 2];
-      const float w = exp2f(m - M);
-      den += w * A.part_ml[((base + sp) * kRows + r) * 2 + 1];
-      num += w * A.part_o[((base + sp) * kRows + r) * HD + d];
-    }
-    const int gr = r0 + r, j = gr / G, g = gr % G;
-    out[((int64_t)(sq.q_start + j) * A.nq + h * G + g) * HD + d] = __float2bfloat16_rn(num / den);
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * HD) return;
+  const int r = e / HD, d = e % HD;
+  const int64_t base = ((int64_t)z * A.qblocks + qb) * A.splits;
+  float M = -INFINITY;
+  for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, A.part_ml[((base + sp) * kRows + r) * 2]);
+  float den = 0.0f, num = 0.0f;
+  for (int sp = 0; sp < nsplit; ++sp) {
+    const float w = exp2f(A.part_ml[((base + sp) * kRows + r) * 2] - M);
+    den += w * A.part_ml[((base + sp) * kRows + r) * 2 + 1];
+    num += w * A.part_o[((base + sp) * kRows + r) * HD + d];
   }
+  const int gr = r0 + r, j = gr / G, g = gr % G;
+  A.out[((int64_t)(sq.q_start + j) * A.nq + h * G + g) * HD + d] = __float2bfloat16_rn(num / den);
 }
 
 // fp32 parity attention: one warp per (token, q head), keys in position
@@ -379,7 +418,9 @@ __global__ void attn_f32_kernel(const float* __restrict__ q, const SeqInfo* __re
 
 template <int HD>
 size_t attn_smem() {
-  return (size_t)kRows * HD * 2 + 4 * (size_t)kKT * HD * 2 + kRows * 68 * 4 + kRows * 72 * 2 + 3 * kRows * 4;
+  const size_t ring = (size_t)kStages * 2 * kKT * HD * 2;
+  const size_t merge = (size_t)4 * kRows * (HD + 2) * 4;
+  return (size_t)kRows * HD * 2 + (ring > merge ? ring : merge);
 }
 
 }  // namespace
@@ -388,15 +429,23 @@ size_t attention_partial_floats(int num_seqs, int kv_heads, int qblocks, int spl
   return (size_t)num_seqs * kv_heads * qblocks * splits * kRows * (hd + 2);
 }
 
+// Partial-buffer bound for a model: sum over sequences of query blocks is at
+// most max_seqs + max_tokens*G/kRows; splits cover keys [0, max_key].
+size_t attention_workspace_floats(int max_seqs, int max_tokens, int G, int kv_heads, int max_key, int hd) {
+  const int qblocks = max_seqs + (max_tokens * G + kRows - 1) / kRows;
+  const int splits = ceil_div(max_key / kKT + 1, kSplitTiles);
+  return attention_partial_floats(1, kv_heads, qblocks, splits, hd);
+}
+
 int attention_bf16(const __nv_bfloat16* q, const SeqInfo* seqs, int num_seqs, int max_q_len, int max_key,
                    const KvLayout& kv, int layer, int nq, float* partials, size_t partial_floats,
-                   __nv_bfloat16* out, cudaStream_t stream) {
+                   __nv_bfloat16* out, cudaStream_t stream, int phase) {
   if (num_seqs == 0) return SR_OK;
   const int hd = kv.head_dim, G = nq / kv.kv_heads;
   SR_REQUIRE(hd == 64 || hd == 128, "bf16 attention supports head_dim 64 or 128");
   SR_REQUIRE(kv.page == kKT, "paged cache page size must be 64 tokens");
   AttnArgs a;
-  a.q = q; a.seqs = seqs; a.kv = kv; a.layer = layer; a.nq = nq; a.G = G;
+  a.q = q; a.seqs = seqs; a.kv = kv; a.layer = layer; a.nq = nq; a.G = G; a.out = out;
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
   a.qblocks = ceil_div(max_q_len * G, kRows);
   a.splits = ceil_div(max_key / kKT + 1, kSplitTiles);
@@ -404,30 +453,31 @@ int attention_bf16(const __nv_bfloat16* q, const SeqInfo* seqs, int num_seqs, in
   SR_REQUIRE(need <= partial_floats, "attention partial workspace too small");
   a.part_o = partials;
   a.part_ml = partials + (size_t)num_seqs * kv.kv_heads * a.qblocks * a.splits * kRows * hd;
-  dim3 grid(a.splits, a.qblocks, num_seqs * kv.kv_heads);
-  if (hd == 128) {
-    static bool set = false;
-    if (!set) {
-      SR_CHECK_CUDA(cudaFuncSetAttribute(attn_bf16_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)attn_smem<128>()));
-      set = true;
+  const dim3 grid(a.splits, a.qblocks, num_seqs * kv.kv_heads);
+  if (phase == 0) {
+    if (hd == 128) {
+      static bool set = false;
+      if (!set) {
+        SR_CHECK_CUDA(cudaFuncSetAttribute(attn_bf16_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)attn_smem<128>()));
+        set = true;
+      }
+      attn_bf16_kernel<128><<<grid, kAttnThreads, attn_smem<128>(), stream>>>(a);
+    } else {
+      static bool set = false;
+      if (!set) {
+        SR_CHECK_CUDA(cudaFuncSetAttribute(attn_bf16_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)attn_smem<64>()));
+        set = true;
+      }
+      attn_bf16_kernel<64><<<grid, kAttnThreads, attn_smem<64>(), stream>>>(a);
     }
-    attn_bf16_kernel<128><<<grid, kAttnThreads, attn_smem<128>(), stream>>>(a);
-    int rc = check_launch("attn_bf16_kernel<128>");
-    if (rc) return rc;
-    attn_combine_kernel<128><<<dim3(a.qblocks, num_seqs * kv.kv_heads), 128, 0, stream>>>(a, out);
-  } else {
-    static bool set = false;
-    if (!set) {
-      SR_CHECK_CUDA(cudaFuncSetAttribute(attn_bf16_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)attn_smem<64>()));
-      set = true;
-    }
-    attn_bf16_kernel<64><<<grid, kAttnThreads, attn_smem<64>(), stream>>>(a);
-    int rc = check_launch("attn_bf16_kernel<64>");
-    if (rc) return rc;
-    attn_combine_kernel<64><<<dim3(a.qblocks, num_seqs * kv.kv_heads), 64, 0, stream>>>(a, out);
+    return check_launch("attn_bf16_kernel");
   }
+  if (a.splits <= 1) return SR_OK;  // every block finished in the main kernel
+  const dim3 cgrid(ceil_div(kRows * hd, 256), a.qblocks, num_seqs * kv.kv_heads);
+  if (hd == 128) attn_combine_kernel<128><<<cgrid, 256, 0, stream>>>(a);
+  else attn_combine_kernel<64><<<cgrid, 256, 0, stream>>>(a);
   return check_launch("attn_combine_kernel");
 }
 

@@ -27,10 +27,10 @@
 
 namespace sr {
 
-size_t attention_partial_floats(int num_seqs, int kv_heads, int qblocks, int splits, int hd);
+size_t attention_workspace_floats(int max_seqs, int max_tokens, int G, int kv_heads, int max_key, int hd);
 int attention_bf16(const __nv_bfloat16* q, const SeqInfo* seqs, int num_seqs, int max_q_len, int max_key,
                    const KvLayout& kv, int layer, int nq, float* partials, size_t partial_floats,
-                   __nv_bfloat16* out, cudaStream_t stream);
+                   __nv_bfloat16* out, cudaStream_t stream, int phase);
 int attention_f32(const float* q, const SeqInfo* seqs, int num_seqs, int max_q_len, const KvLayout& kv,
                   int layer, int nq, float* out, cudaStream_t stream);
 int kv_commit(int B, int N, const SeqInfo* seqs, const int32_t* outcome, const int32_t* bon,
@@ -66,7 +66,8 @@ struct Carve {
 
 // Per-category CUDA-event timing of the forward's launches (bench.py's
 // roofline evidence): events bracket each launch on the launching stream.
-enum ProfCat { kProfQkv, kProfO, kProfGateUp, kProfDown, kProfLmHead, kProfAttn, kProfOther, kProfCats };
+enum ProfCat { kProfQkv, kProfO, kProfGateUp, kProfDown, kProfLmHead, kProfAttn, kProfOther, kProfCombine,
+               kProfCats };
 
 struct Profiler {
   bool on = false;
@@ -103,7 +104,6 @@ struct Model {
   int esize;
   int qkv_width;
   int lm_tiles;
-  int splits_max;
   size_t partial_floats;
   // workspace views
   float* x;
@@ -129,9 +129,7 @@ static size_t carve(const sr_model_desc& d, Model* m, char* base) {
   const int qkv_w = (d.q_heads + 2 * d.kv_heads) * d.head_dim;
   const int G = d.q_heads / d.kv_heads;
   const int lm_tiles = (d.vocab + kLmBn - 1) / kLmBn;
-  const int splits = ((d.max_key / 64 + 1) + 15) / 16;
-  const size_t pf = attention_partial_floats(1, d.kv_heads, (d.max_seqs + (T * G + 63) / 64), splits,
-                                             d.head_dim);
+  const size_t pf = attention_workspace_floats(d.max_seqs, T, G, d.kv_heads, d.max_key, d.head_dim);
   float* x = c.take<float>((size_t)T * H);
   char* h = c.take<char>((size_t)T * H * esize);
   char* qkv = c.take<char>((size_t)T * qkv_w * esize);
@@ -147,7 +145,7 @@ static size_t carve(const sr_model_desc& d, Model* m, char* base) {
   if (m != nullptr) {
     m->x = x; m->h = h; m->qkv = qkv; m->q = q; m->attn = attn; m->act = act; m->h_sel = h_sel;
     m->logits = logits; m->part_val = pv; m->part_idx = pi; m->attn_part = ap;
-    m->esize = esize; m->qkv_width = qkv_w; m->lm_tiles = lm_tiles; m->splits_max = splits;
+    m->esize = esize; m->qkv_width = qkv_w; m->lm_tiles = lm_tiles;
     m->partial_floats = d.dtype == 1 ? pf : 0;
   }
   return c.off + 256;
@@ -279,7 +277,11 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
       P.end(st);
       P.begin(sr::kProfAttn, st);
       SR_TRY(sr::attention_bf16((const bf*)m->q, seqs, S, a->max_q_len, a->max_key, m->kv, l, d.q_heads,
-                                m->attn_part, m->partial_floats, (bf*)m->attn, st));
+                                m->attn_part, m->partial_floats, (bf*)m->attn, st, 0));
+      P.end(st);
+      P.begin(sr::kProfCombine, st);
+      SR_TRY(sr::attention_bf16((const bf*)m->q, seqs, S, a->max_q_len, a->max_key, m->kv, l, d.q_heads,
+                                m->attn_part, m->partial_floats, (bf*)m->attn, st, 1));
       P.end(st);
       P.begin(sr::kProfO, st);
       SR_TRY(sr::gemm_bf16_launch(m->p_o[l], st, M));

@@ -38,6 +38,39 @@ class NgramDrafter:
     name: str = "ngram"
 
 
+class SyntheticDrafter:
+    """Drafter whose acceptance follows the reference's keyed Bernoulli law.
+
+    ``truth[b]`` is the target model's greedy continuation of request b
+    (from a plain-decode pass), ``method`` names the reference acceptance
+    stream: draft token g is the true token iff
+    ``stream(seed, rid, "accept_draw", method, g // 256).random(256)[g % 256]
+    < latent_accept[method]`` (``sim.py:322-336``), generated on device by
+    ``sr_keyed_uniforms``.
+    """
+
+    name = "synthetic"
+
+    def __init__(self, truth: list[list[int]], requests, method: str, seed: int, device="cuda"):
+        from .verify import CHUNK, entropy_words, keyed_fill
+
+        B = len(truth)
+        L = max(len(t) for t in truth)
+        chunks = max(1, math.ceil(L / CHUNK))
+        self.stride = chunks * CHUNK
+        tt = np.zeros((B, self.stride), dtype=np.int32)
+        for b, t in enumerate(truth):
+            tt[b, : len(t)] = t
+        self.truth = torch.from_numpy(tt).to(device)
+        self.truth_len = torch.tensor([len(t) for t in truth], dtype=torch.int32, device=device)
+        self.uniforms = torch.empty((B, self.stride), dtype=torch.float64, device=device)
+        keyed_fill("uniforms", [entropy_words(seed, r.id, "accept_draw", method, c)
+                                for r in requests for c in range(chunks)], CHUNK, self.uniforms)
+        self.p = torch.tensor([r.latent_accept[method] for r in requests], dtype=torch.float64,
+                              device=device)
+        self.method = method
+
+
 class RolloutEngine:
     """Batch state (token buffer, lengths, budgets) + per-step device work."""
 
@@ -130,6 +163,13 @@ class RolloutEngine:
         drafts_ptr, nd_ptr = None, None
         if self.k > 0:
             for n, d in enumerate(self.drafters):
+                if isinstance(d, SyntheticDrafter):
+                    _native.check(lib.sr_synthetic_draft(
+                        self.B, self.k, d.truth.data_ptr(), d.stride, d.truth_len.data_ptr(),
+                        d.uniforms.data_ptr(), d.stride, d.p.data_ptr(), self.gen_len.data_ptr(),
+                        self.m.s.vocab, self.drafts[n].data_ptr(), self.ndraft[n].data_ptr(), st),
+                        "sr_synthetic_draft")
+                    continue
                 _native.check(lib.sr_ngram_propose(
                     self.B, self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(), d.min_n, d.max_n,
                     self.k, self.drafts[n].data_ptr(), self.ndraft[n].data_ptr(),

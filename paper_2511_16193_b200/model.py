@@ -220,8 +220,8 @@ class DeviceModel:
 
     def max_prefill_seqs(self, q_len: int) -> int:
         """How many q_len-token sequences one forward can attend for."""
-        budget = self.max_seqs + (self.max_tokens * self.group + 63) // 64
-        return max(1, budget // max(1, math.ceil(q_len * self.group / 64)))
+        budget = self.max_seqs + (self.max_tokens * self.group + 31) // 32
+        return max(1, budget // max(1, math.ceil(q_len * self.group / 32)))
 
 
 def seq_table(rows: list[tuple[int, int, int, int, int]], device) -> torch.Tensor:

@@ -228,3 +228,41 @@ def test_accept_commit_kernel_vs_python():
                 an, ndn, _ = acc[n]
                 exp_w = (0 if an == ndn else max(ndn - an - 1, 0)) if n == win else ndn
                 assert row.tolist() == [ndn, an, c if n == win else 0, exp_w]
+
+
+def test_synthetic_drafter_follows_reference_accept_law():
+    """The reference-acceptance drafter accepts exactly the reference's
+    `_verify_prefix` run (sim.py:977-981) on keyed draws, while the committed
+    tokens stay the target's greedy output."""
+    from oracle import rollout_oracle
+    from paper_2511_16193_b200 import scenarios
+    from paper_2511_16193_b200.engine import RolloutEngine, SyntheticDrafter
+    from paper_2511_16193_b200.workload import gen_trace
+
+    B, k, method = 4, 4, "draft-0.5b"
+    s, w, m = make("tiny", "bf16", B=B)
+    prompts = prompts_for(s.vocab, B, 6)
+    reqs = gen_trace(scenarios.default_trace_spec(batch=B, seed=0))
+    max_new = [70, 45, 90, 30]
+    plain, _ = run_engine(m, prompts, max_new, k=0)
+    truth = plain.outputs()
+    eng = RolloutEngine(m, prompts, max_new, k=k, drafters=(SyntheticDrafter(truth, reqs, method, 0),),
+                        bonus_token=True, history=256)
+    eng.prefill()
+    steps = eng.run()
+    assert eng.outputs() == truth
+    rows = eng.outcome_rows(steps)
+    for b, r in enumerate(reqs):
+        u = rollout_oracle.accept_uniforms(0, r.id, method, max_new[b] + 8)
+        p = r.latent_accept[method]
+        g = 1
+        for step in range(steps):
+            n, a, c, _ = rows[step, b]
+            if n == 0 and c == 0:
+                continue
+            exp_a = 0
+            while exp_a < n and u[g + exp_a] < p:
+                exp_a += 1
+            assert a == exp_a, (b, step, g)
+            g += c
+        assert g == max_new[b]
