@@ -39,7 +39,7 @@ sys.path.insert(0, str(ROOT))
 MODEL = "qwen2.5-1.5b"
 BATCH = 256
 K = 4
-METRIC = "rollout accepted tokens/sec (Qwen2.5-1.5B-shaped target, batch 256, k=4, n-gram drafter, greedy)"
+METRIC = "rollout accepted tokens/sec (Qwen2.5-1.5B-shaped target, batch 256/GPU, k=4, greedy)"
 UNIT = "tokens/s"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 
@@ -54,7 +54,8 @@ def parse():
     ap.add_argument("--model", default=MODEL)
     ap.add_argument("--layers", type=int, default=None, help="debug only: truncate depth")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--graph", action="store_true", help="replay steps from a CUDA graph")
+    ap.add_argument("--eager", action="store_true",
+                    help="launch every kernel from the host instead of replaying a CUDA graph")
     ap.add_argument("--drafter", choices=["synthetic", "ngram"], default="synthetic",
                     help="synthetic: reference accept_draw law over the target's own greedy "
                          "continuation (SURVEY 7.1e); ngram: vLLM prompt lookup")
@@ -146,7 +147,7 @@ def run_ours(args, rank, world, dist):
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
     lib = _native.lib()
     s = shape(args.model, args.layers)
-    steps_total = args.warmup + 2 * args.steps + 2
+    steps_total = args.warmup + 2 * args.steps + 12
     trace, prompts, budget = workload(rank, args.batch, steps_total, s.vocab)
     max_len = max(len(p) for p in prompts) + budget[0] + K + 8
     w = init_weights(s, seed=0, device="cuda")
@@ -170,7 +171,7 @@ def run_ours(args, rank, world, dist):
     del plain
     eng = RolloutEngine(model, prompts, budget, k=K, drafters=(drafter,), bonus_token=True, history=1)
     eng.prefill()
-    if args.graph:
+    if not args.eager:
         eng.capture()
     clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", 0))).__enter__()
     for _ in range(args.warmup):
@@ -186,7 +187,7 @@ def run_ours(args, rank, world, dist):
     hist = torch.zeros((args.steps, B, 4), dtype=torch.int32, device="cuda")
     gen0 = eng.gen_len.sum()
     launches0 = lib.sr_launch_count()
-    lib.sr_model_profile(model.handle, 0 if args.graph else 1, None, None)
+    lib.sr_model_profile(model.handle, 1 if args.eager else 0, None, None)
     st = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -203,6 +204,25 @@ def run_ours(args, rank, world, dist):
     cat_ms = (ctypes.c_float * 8)()
     cat_n = (ctypes.c_int32 * 8)()
     lib.sr_model_profile(model.handle, 0, cat_ms, cat_n)
+    if not args.eager:
+        # kernel durations: the same steps launched eagerly with CUDA events
+        # bracketing each launch on the launching stream (a graph replay
+        # cannot host per-kernel events); durations do not depend on how the
+        # launch was issued
+        prof_steps = min(args.steps, 10)
+        graph, eng.graph = eng.graph, None
+        lib.sr_model_profile(model.handle, 1, None, None)
+        l0 = lib.sr_launch_count()
+        for _ in range(prof_steps):
+            eng.step()
+        per_step_launches = (lib.sr_launch_count() - l0) / prof_steps
+        lib.sr_model_profile(model.handle, 0, cat_ms, cat_n)
+        # every replay launches the captured kernels once
+        launches = int(round(per_step_launches * args.steps))
+        eng.graph = graph
+        scale = args.steps / prof_steps
+        for i in range(8):
+            cat_ms[i] *= scale
     outs_ok = all(o == t[: len(o)] for o, t in zip(eng.outputs(), truth))
     h = hist.cpu().numpy().reshape(-1, 4)
     live = h[h[:, 0] + h[:, 2] > 0]
@@ -262,7 +282,7 @@ def run_ours(args, rank, world, dist):
                    "k": K, "verify_rows_per_step": rows, "prompt_len": "U[128,1024] (default_trace_spec)",
                    "parallelism": f"prompt-sharded x{world} (no data-path collective)",
                    "l2": "inputs larger than L2 (3.1 GB weights + paged KV per step)",
-                   "graph": bool(args.graph)},
+                   "cuda_graph": not args.eager},
         "mean_accepted_length": accepted_mean,
         "drafter": (f"synthetic: target's greedy continuation, accepted iff reference keyed "
                     f"accept_draw u < latent_accept['{args.accept_method}'] (sim.py:322-336)"

@@ -189,6 +189,20 @@ typedef struct sr_forward_args {
   float* out_val;           /* optional max logit per row (argmax output) */
 } sr_forward_args;
 
+/* K2 alone: paged GQA attention of the verify rows described by seqs over
+ * one layer of the KV cache (layouts as above; bf16 rows pre-swizzled in
+ * 16-byte chunks by slot & 7).  q, out [M, q_heads, head_dim]; partials is
+ * fp32 scratch for multi-split blocks. */
+int sr_paged_attention(int dtype, const void* q, const void* seqs, int num_seqs, int max_q_len, int max_key,
+                       int q_heads, int kv_heads, int head_dim, int layer, int layers, void* kv_cache,
+                       int num_pages, const int32_t* block_table, int max_pages, void* window, int branches,
+                       int window_max, float* partials, uint64_t partial_floats, void* out,
+                       sr_stream_t stream);
+
+/* KV split size of K2 in 64-key tiles (default 32).  Part of the numerics:
+ * keep it fixed for a model so verify and decode stay bit-identical. */
+int sr_set_attention_split(int tiles);
+
 uint64_t sr_model_workspace_bytes(const sr_model_desc* desc);
 int sr_model_create(const sr_model_desc* desc, void** handle);
 int sr_model_destroy(void* handle);

@@ -30,6 +30,9 @@ SIGNATURES: dict[str, list] = {
     "sr_ngram_propose": [_i32, _vp, _i64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
     "sr_gemm": [_i32, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _i32, _vp, _i32,
                 _vp, _vp],
+    "sr_paged_attention": [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _i32,
+                           _vp, _i32, _vp, _i32, _i32, _vp, ctypes.c_uint64, _vp, _vp],
+    "sr_set_attention_split": [_i32],
     "sr_model_workspace_bytes": [_vp],
     "sr_model_create": [_vp, _vp],
     "sr_model_destroy": [_vp],

@@ -100,8 +100,9 @@ __global__ void kv_commit_kernel(int N, const SeqInfo* __restrict__ seqs, const 
     const int kvsel = r / (nkv * hd), h = (r / hd) % nkv, d = r % hd;
     const int pos = sq.ctx_len + j;
     const int page = btab[pos / kv.page];
-    cbase[(((int64_t)page * 2 + kvsel) * nkv + h) * kv.page * hd + (int64_t)(pos % kv.page) * hd + d] =
-        wbase[((int64_t)kvsel * nkv + h) * kv.window_max * hd + (int64_t)j * hd + d];
+    const int slot = pos % kv.page;
+    cbase[(((int64_t)page * 2 + kvsel) * nkv + h) * kv.page * hd + (int64_t)slot * hd + kv_phys<T>(slot, d)] =
+        wbase[((int64_t)kvsel * nkv + h) * kv.window_max * hd + (int64_t)j * hd + kv_phys<T>(j, d)];
   }
 }
 

@@ -6,7 +6,8 @@
 // tiles of 64 *absolute* positions (tile t = keys [64t, 64t+64)); a key comes
 // from the paged cache when it is committed (pos < ctx_len) or written in
 // place, else from the drafter-branch window buffer.  Splits are fixed
-// 512-key ranges merged by a combine kernel in split order.  Because the
+// 2048-key ranges (sr_set_attention_split) merged by a combine kernel in
+// split order.  Because the
 // tiling depends only on absolute positions, a query's arithmetic is the
 // same in a 5-position verify window and in a 1-position decode step: the
 // speculative and plain paths produce bit-identical logits.
@@ -19,6 +20,7 @@
 // the K/V tiles it reads.
 #include "common.cuh"
 #include "layers.cuh"
+#include "sm100.cuh"
 
 #include <cuda_bf16.h>
 
@@ -28,9 +30,8 @@ namespace {
 
 constexpr int kKT = 64;          // keys per tile (= page size)
 constexpr int kRows = 32;        // query rows per CTA
-constexpr int kSplitTiles = 8;   // tiles per KV split (512 keys)
 constexpr int kStages = 3;       // cp.async ring depth
-constexpr int kAttnThreads = 128;
+constexpr int kAttnThreads = 256;  // 8 warps: (m-tile, 16-key slice) pairs
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
@@ -75,8 +76,11 @@ struct AttnArgs {
   float* part_o;   // [S*nkv, qblocks, splits, 64, HD]
   float* part_ml;  // [S*nkv, qblocks, splits, 64, 2]
   int qblocks, splits;
+  int split_tiles;     // tiles per KV split (fixed per model: batch invariance)
   __nv_bfloat16* out;  // [M, nq, HD]
 };
+
+int g_split_tiles = 32;  // 2048-key splits
 
 __device__ __forceinline__ int block_max_key(const SeqInfo& sq, int r0, int rows, int G) {
   return sq.ctx_len + (r0 + rows - 1) / G;
@@ -88,11 +92,10 @@ __device__ __forceinline__ int block_max_key(const SeqInfo& sq, int r0, int rows
 // fixed order at the end.  One __syncthreads per tile guards the 3-stage
 // cp.async ring.
 template <int HD>
-__global__ void __launch_bounds__(kAttnThreads)
+__global__ void __launch_bounds__(kAttnThreads, 2)
 attn_bf16_kernel(AttnArgs A) {
   constexpr int CH = HD / 8;       // 16-byte chunks per row
   constexpr int NO = HD / 8;       // n8 tiles of O per m-tile
-  constexpr int MT = kRows / 16;   // m-tiles per CTA (2)
   constexpr uint32_t kTileBytes = kKT * HD * 2;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* sQ = smem;                              // [kRows][HD]
@@ -109,7 +112,7 @@ attn_bf16_kernel(AttnArgs A) {
   const int rows = min(kRows, rows_total - r0);
   const int max_key = block_max_key(sq, r0, rows, G);
   const int ntiles = max_key / kKT + 1;
-  const int t_begin = sp * kSplitTiles, t_end = min(ntiles, t_begin + kSplitTiles);
+  const int t_begin = sp * A.split_tiles, t_end = min(ntiles, t_begin + A.split_tiles);
   if (t_begin >= t_end) return;
   const int mtv = (rows + 15) / 16;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -132,90 +135,97 @@ attn_bf16_kernel(AttnArgs A) {
     }
   }
 
+  // K/V ring: stage = [K tile | V tile]; full[stage] completes when both land.
+  __shared__ __align__(8) uint64_t full[kStages];
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) sm100::mbar_init(&full[i], 1);
+    sm100::fence_barrier_init();
+  }
+  __syncthreads();
+
+  // Called by all threads (uniform control flow).
   auto load_tile = [&](int t, int stage) {
-    if (t < t_end) {
-      uint8_t* k_dst = sKV + stage * 2 * kTileBytes;
-      uint8_t* v_dst = k_dst + kTileBytes;
-      const int last = t * kKT + kKT - 1;
-      if (last <= max_key && (sq.branch < 0 || last < sq.ctx_len)) {
-        // fast path: the tile is exactly one committed page -> two contiguous
-        // 16 KB blocks (K, V of head h); uniform base, unrolled copies
+    if (t >= t_end) return;
+    uint8_t* k_dst = sKV + stage * 2 * kTileBytes;
+    uint8_t* v_dst = k_dst + kTileBytes;
+    const int last = t * kKT + kKT - 1;
+    if (last <= max_key && (sq.branch < 0 || last < sq.ctx_len)) {
+      // a whole committed page: K and V of head h are two contiguous 16 KB
+      // blocks stored pre-swizzled -> two TMA bulk copies, no thread work
+      if (tid == 0) {
         const __nv_bfloat16* kb = cache + ((int64_t)btab[t] * 2 * nkv + h) * psz * HD;
-        const __nv_bfloat16* vb = kb + (int64_t)nkv * psz * HD;
-#pragma unroll
-        for (int i = 0; i < kKT * CH / kAttnThreads; ++i) {
-          const int e = tid + i * kAttnThreads;
-          const int r = e / CH, c = e % CH;
-          const uint32_t off = swz<HD>(r, c);
-          cp_async16(k_dst + off, kb + e * 8);
-          cp_async16(v_dst + off, vb + e * 8);
-        }
-        cp_async_commit();
-        return;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        sm100::mbar_arrive_expect_tx(&full[stage], 2 * kTileBytes);
+        sm100::bulk_load(k_dst, kb, kTileBytes, &full[stage]);
+        sm100::bulk_load(v_dst, kb + (int64_t)nkv * psz * HD, kTileBytes, &full[stage]);
       }
-      for (int e = tid; e < kKT * CH; e += kAttnThreads) {
-        const int r = e / CH, c = e % CH;
-        const int kp = t * kKT + r;
-        const uint32_t off = swz<HD>(r, c);
-        if (kp > max_key) {
-          *reinterpret_cast<uint4*>(k_dst + off) = make_uint4(0, 0, 0, 0);
-          *reinterpret_cast<uint4*>(v_dst + off) = make_uint4(0, 0, 0, 0);
-          continue;
-        }
+      return;
+    }
+    // partial page / drafter-branch window keys: synchronous swizzle-aware copy
+    for (int e = tid; e < kKT * CH; e += kAttnThreads) {
+      const int r = e / CH, pc = e % CH;        // destination row, physical chunk
+      const int kp = t * kKT + r;
+      const uint32_t off = (uint32_t)(r * HD * 2 + pc * 16);
+      uint4 kv4 = make_uint4(0, 0, 0, 0), vv4 = make_uint4(0, 0, 0, 0);
+      if (kp <= max_key) {
         const __nv_bfloat16* ksrc;
         int64_t vstep;
+        int src_chunk;
         if (sq.branch < 0 || kp < sq.ctx_len) {
           const int page = btab[kp / psz];
           ksrc = cache + (((int64_t)page * 2 * nkv + h) * psz + kp % psz) * HD;
           vstep = (int64_t)nkv * psz * HD;
+          src_chunk = pc;  // page slot == tile row: same swizzle
         } else {
-          ksrc = win + (((int64_t)sq.branch * 2 * nkv + h) * A.kv.window_max + (kp - sq.ctx_len)) * HD;
+          const int j = kp - sq.ctx_len;
+          ksrc = win + (((int64_t)sq.branch * 2 * nkv + h) * A.kv.window_max + j) * HD;
           vstep = (int64_t)nkv * A.kv.window_max * HD;
+          src_chunk = (pc ^ (r & 7)) ^ (j & 7);  // logical chunk re-swizzled by window slot
         }
-        cp_async16(k_dst + off, ksrc + c * 8);
-        cp_async16(v_dst + off, ksrc + vstep + c * 8);
+        kv4 = *reinterpret_cast<const uint4*>(ksrc + src_chunk * 8);
+        vv4 = *reinterpret_cast<const uint4*>(ksrc + vstep + src_chunk * 8);
       }
+      *reinterpret_cast<uint4*>(k_dst + off) = kv4;
+      *reinterpret_cast<uint4*>(v_dst + off) = vv4;
     }
-    cp_async_commit();  // always one group per tile slot: simple wait counting
+    if (tid == 0) sm100::mbar_arrive(&full[stage]);
   };
 
-  // per-thread state: rows g=lane/4 and g+8 of each m-tile
-  float o[MT][NO][4];
-  float m_run[MT][2], l_run[MT][2];
+  // warp (mw, kw): m-tile mw (rows 16mw..), keys [16kw, 16kw+16) of each tile
+  const int mw = warp >> 2, kw = warp & 3;
+  const bool active = mw < mtv;
+  float o[NO][4];
+  float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
 #pragma unroll
-  for (int mt = 0; mt < MT; ++mt) {
-    m_run[mt][0] = m_run[mt][1] = -INFINITY;
-    l_run[mt][0] = l_run[mt][1] = 0.0f;
+  for (int nt = 0; nt < NO; ++nt)
 #pragma unroll
-    for (int nt = 0; nt < NO; ++nt)
+    for (int i = 0; i < 4; ++i) o[nt][i] = 0.0f;
+  // query position of this thread's rows g=lane/4 and g+8 (causal mask)
+  int qpos[2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) o[mt][nt][i] = 0.0f;
+  for (int hi = 0; hi < 2; ++hi) {
+    const int r = mw * 16 + (lane >> 2) + hi * 8;
+    qpos[hi] = r < rows ? sq.ctx_len + (r0 + r) / G : -1;  // -1: padding row, all masked
   }
-  // query position of this thread's rows (for the causal mask)
-  int qpos[MT][2];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int hi = 0; hi < 2; ++hi) {
-      const int r = mt * 16 + (lane >> 2) + hi * 8;
-      qpos[mt][hi] = r < rows ? sq.ctx_len + (r0 + r) / G : -1;  // -1: padding row, all masked
-    }
-
+  const int min_qpos = sq.ctx_len + r0 / G;  // first query row of the block
   load_tile(t_begin, 0);
   load_tile(t_begin + 1, 1);
+  cp_async_commit();
+  cp_async_wait<0>();  // Q block
   const uint32_t q_base = (uint32_t)__cvta_generic_to_shared(sQ);
   for (int t = t_begin; t < t_end; ++t) {
-    const int stage = (t - t_begin) % kStages;
-    cp_async_wait<kStages - 2>();
-    __syncthreads();  // tile t visible to all; every warp is done with tile t-1's slot
-    load_tile(t + 2, (t - t_begin + 2) % kStages);
+    const int i = t - t_begin;
+    const int stage = i % kStages;
+    sm100::mbar_wait(&full[stage], (uint32_t)((i / kStages) & 1));
+    __syncthreads();  // tile t (incl. plain smem stores) visible; tile t-1's slot is free
+    load_tile(t + 2, (i + 2) % kStages);
     const uint32_t k_base = (uint32_t)__cvta_generic_to_shared(sKV + stage * 2 * kTileBytes);
     const uint32_t v_base = k_base + kTileBytes;
-    const int key0 = t * kKT + warp * 16;
+    const int key0 = t * kKT + kw * 16;
+    if (!active) continue;
+    {
+      const int mt = mw;
 
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      if (mt >= mtv) break;
       // S = Q K^T for this warp's 16 keys
       float sacc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
 #pragma unroll
@@ -223,87 +233,104 @@ attn_bf16_kernel(AttnArgs A) {
         uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
         const int mi = lane >> 3;
         ldsm_x4(q_base + swz<HD>(mt * 16 + (mi & 1) * 8 + (lane & 7), kk * 2 + (mi >> 1)), a0, a1, a2, a3);
-        ldsm_x4(k_base + swz<HD>(warp * 16 + (mi >> 1) * 8 + (lane & 7), kk * 2 + (mi & 1)), b0, b1, b2, b3);
+        ldsm_x4(k_base + swz<HD>(kw * 16 + (mi >> 1) * 8 + (lane & 7), kk * 2 + (mi & 1)), b0, b1, b2, b3);
         mma_bf16(sacc[0], a0, a1, a2, a3, b0, b1);
         mma_bf16(sacc[1], a0, a1, a2, a3, b2, b3);
       }
-      // mask + scale, row max over the quad
+      // mask (only tiles reaching the block's first query need it), row max
+      // over the quad; scale_log2 is applied inside the exponent FFMA
+      const bool need_mask = key0 + 15 > min_qpos;
       float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int kp = key0 + nt * 8 + 2 * (lane & 3) + (i & 1);
           const int hi = i >> 1;
-          const float v = kp <= qpos[mt][hi] ? sacc[nt][i] * A.scale_log2 : -INFINITY;
-          sacc[nt][i] = v;
-          mx[hi] = fmaxf(mx[hi], v);
+          if (need_mask) {
+            const int kp = key0 + nt * 8 + 2 * (lane & 3) + (i & 1);
+            if (kp > qpos[hi]) sacc[nt][i] = -INFINITY;
+          }
+          mx[hi] = fmaxf(mx[hi], sacc[nt][i]);
         }
       uint32_t pa[4];
+      bool rescale = false;
+      float alpha[2];
 #pragma unroll
       for (int hi = 0; hi < 2; ++hi) {
         mx[hi] = fmaxf(mx[hi], __shfl_xor_sync(0xffffffffu, mx[hi], 1));
         mx[hi] = fmaxf(mx[hi], __shfl_xor_sync(0xffffffffu, mx[hi], 2));
-        const float m_new = fmaxf(m_run[mt][hi], mx[hi]);
-        const float m_use = m_new == -INFINITY ? 0.0f : m_new;
-        const float alpha = exp2f(m_run[mt][hi] - m_use);
-        m_run[mt][hi] = m_new;
+        // lazy rescaling (FA4): keep the reference max m_run (raw score units)
+        // unless the new max exceeds it by more than 8 in log2 units; p can
+        // then reach 2^8, harmless in fp32/bf16.  The decision depends only on
+        // this row's keys in tile order, so it is batch invariant.
+        const float m_old = m_run[hi];
+        float m_ref = m_old;
+        alpha[hi] = 1.0f;
+        if (mx[hi] != -INFINITY && (m_old == -INFINITY || (mx[hi] - m_old) * A.scale_log2 > 8.0f)) {
+          m_ref = mx[hi];
+          alpha[hi] = m_old == -INFINITY ? 0.0f : exp2f((m_old - m_ref) * A.scale_log2);
+          rescale = true;
+        }
+        m_run[hi] = m_ref;
+        const float neg = m_ref == -INFINITY ? 0.0f : -m_ref * A.scale_log2;
         float rs = 0.0f;
         float p[4];
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            p[nt * 2 + c] = exp2f(sacc[nt][hi * 2 + c] - m_use);
+            p[nt * 2 + c] = exp2f(fmaf(sacc[nt][hi * 2 + c], A.scale_log2, neg));
             rs += p[nt * 2 + c];
           }
-        l_run[mt][hi] = l_run[mt][hi] * alpha + rs;
-#pragma unroll
-        for (int nt = 0; nt < NO; ++nt) {
-          o[mt][nt][hi * 2] *= alpha;
-          o[mt][nt][hi * 2 + 1] *= alpha;
-        }
-        // C fragment -> A fragment (k = this warp's 16 keys)
+        l_run[hi] = l_run[hi] * alpha[hi] + rs;
         __nv_bfloat162 lo = __floats2bfloat162_rn(p[0], p[1]);
         __nv_bfloat162 hi2 = __floats2bfloat162_rn(p[2], p[3]);
         pa[hi] = *reinterpret_cast<uint32_t*>(&lo);       // a0 (row g) / a1 (row g+8)
         pa[2 + hi] = *reinterpret_cast<uint32_t*>(&hi2);  // a2 / a3
+      }
+      if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+        for (int nt = 0; nt < NO; ++nt) {
+          o[nt][0] *= alpha[0];
+          o[nt][1] *= alpha[0];
+          o[nt][2] *= alpha[1];
+          o[nt][3] *= alpha[1];
+        }
       }
       // O += P V over the warp's 16 keys
 #pragma unroll
       for (int np = 0; np < NO / 2; ++np) {
         uint32_t b0, b1, b2, b3;
         const int mi = lane >> 3;
-        ldsm_x4_t(v_base + swz<HD>(warp * 16 + (mi & 1) * 8 + (lane & 7), np * 2 + (mi >> 1)), b0, b1, b2, b3);
-        mma_bf16(o[mt][2 * np], pa[0], pa[1], pa[2], pa[3], b0, b1);
-        mma_bf16(o[mt][2 * np + 1], pa[0], pa[1], pa[2], pa[3], b2, b3);
+        ldsm_x4_t(v_base + swz<HD>(kw * 16 + (mi & 1) * 8 + (lane & 7), np * 2 + (mi >> 1)), b0, b1, b2, b3);
+        mma_bf16(o[2 * np], pa[0], pa[1], pa[2], pa[3], b0, b1);
+        mma_bf16(o[2 * np + 1], pa[0], pa[1], pa[2], pa[3], b2, b3);
       }
     }
   }
-  cp_async_wait<0>();
   __syncthreads();
 
-  // ---- merge the 4 warps (fixed order) through smem, write the split partial
-  float* sO = reinterpret_cast<float*>(sKV);                 // [4][kRows][HD]
-  float* sML = sO + 4 * kRows * HD;                          // [4][kRows][2]
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt) {
-    if (mt >= mtv) break;
+  // ---- merge the 4 key-slice warps of each m-tile (fixed order) via smem
+  constexpr int OP = HD + 8;                                 // padded row (bank spread)
+  float* sO = reinterpret_cast<float*>(sKV);                 // [4][kRows][OP]
+  float* sML = sO + 4 * kRows * OP;                          // [4][kRows][2]
+  if (active) {
 #pragma unroll
     for (int hi = 0; hi < 2; ++hi) {
-      float l = l_run[mt][hi];
+      float l = l_run[hi];
       l += __shfl_xor_sync(0xffffffffu, l, 1);
       l += __shfl_xor_sync(0xffffffffu, l, 2);
-      const int r = mt * 16 + (lane >> 2) + hi * 8;
+      const int r = mw * 16 + (lane >> 2) + hi * 8;
       if ((lane & 3) == 0) {
-        sML[(warp * kRows + r) * 2] = m_run[mt][hi];
-        sML[(warp * kRows + r) * 2 + 1] = l;
+        const float m = m_run[hi];
+        sML[(kw * kRows + r) * 2] = m == -INFINITY ? -INFINITY : m * A.scale_log2;
+        sML[(kw * kRows + r) * 2 + 1] = l;
       }
 #pragma unroll
       for (int nt = 0; nt < NO; ++nt) {
         const int col = nt * 8 + 2 * (lane & 3);
-        *reinterpret_cast<float2*>(&sO[(warp * kRows + r) * HD + col]) =
-            make_float2(o[mt][nt][hi * 2], o[mt][nt][hi * 2 + 1]);
+        *reinterpret_cast<float2*>(&sO[(kw * kRows + r) * OP + col]) =
+            make_float2(o[nt][hi * 2], o[nt][hi * 2 + 1]);
       }
     }
   }
@@ -313,20 +340,31 @@ attn_bf16_kernel(AttnArgs A) {
   float* pml = A.part_ml + pidx * kRows * 2;
   // A block whose keys fit one split finishes here: out = O / l is exactly
   // what the combine computes for a single split (weight exp2(0) = 1).
-  const bool single = ntiles <= kSplitTiles;
-  for (int e = tid; e < rows * HD; e += kAttnThreads) {
-    const int r = e / HD, d = e % HD;
+  const bool single = ntiles <= A.split_tiles;
+  float* sW = sML + 4 * kRows * 2;  // [kRows][4] warp weights, [kRows] M, [kRows] l
+  if (tid < rows) {
+    const int r = tid;
     float M = -INFINITY;
 #pragma unroll
     for (int w = 0; w < 4; ++w) M = fmaxf(M, sML[(w * kRows + r) * 2]);
     const float Mu = M == -INFINITY ? 0.0f : M;
-    float acc = 0.0f, l = 0.0f;
+    float l = 0.0f;
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       const float wt = exp2f(sML[(w * kRows + r) * 2] - Mu);
-      acc += wt * sO[(w * kRows + r) * HD + d];
+      sW[r * 4 + w] = wt;
       l += wt * sML[(w * kRows + r) * 2 + 1];
     }
+    sW[4 * kRows + r] = M;
+    sW[5 * kRows + r] = l;
+  }
+  __syncthreads();
+  for (int e = tid; e < rows * HD; e += kAttnThreads) {
+    const int r = e / HD, d = e % HD;
+    float acc = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) acc += sW[r * 4 + w] * sO[(w * kRows + r) * OP + d];
+    const float M = sW[4 * kRows + r], l = sW[5 * kRows + r];
     if (single) {
       const int gr = r0 + r, j = gr / G, g = gr % G;
       A.out[((int64_t)(sq.q_start + j) * A.nq + h * G + g) * HD + d] = __float2bfloat16_rn(acc / l);
@@ -355,8 +393,8 @@ attn_combine_kernel(AttnArgs A) {
   if (r0 >= rows_total) return;
   const int rows = min(kRows, rows_total - r0);
   const int ntiles = block_max_key(sq, r0, rows, G) / kKT + 1;
-  if (ntiles <= kSplitTiles) return;  // written directly by the attention kernel
-  const int nsplit = (ntiles + kSplitTiles - 1) / kSplitTiles;
+  if (ntiles <= A.split_tiles) return;  // written directly by the attention kernel
+  const int nsplit = (ntiles + A.split_tiles - 1) / A.split_tiles;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= rows * HD) return;
   const int r = e / HD, d = e % HD;
@@ -419,7 +457,7 @@ __global__ void attn_f32_kernel(const float* __restrict__ q, const SeqInfo* __re
 template <int HD>
 size_t attn_smem() {
   const size_t ring = (size_t)kStages * 2 * kKT * HD * 2;
-  const size_t merge = (size_t)4 * kRows * (HD + 2) * 4;
+  const size_t merge = (size_t)4 * kRows * (HD + 8 + 2) * 4 + (size_t)6 * kRows * 4;
   return (size_t)kRows * HD * 2 + (ring > merge ? ring : merge);
 }
 
@@ -433,7 +471,7 @@ size_t attention_partial_floats(int num_seqs, int kv_heads, int qblocks, int spl
 // most max_seqs + max_tokens*G/kRows; splits cover keys [0, max_key].
 size_t attention_workspace_floats(int max_seqs, int max_tokens, int G, int kv_heads, int max_key, int hd) {
   const int qblocks = max_seqs + (max_tokens * G + kRows - 1) / kRows;
-  const int splits = ceil_div(max_key / kKT + 1, kSplitTiles);
+  const int splits = ceil_div(max_key / kKT + 1, 4);  // bound for any split size >= 4 tiles
   return attention_partial_floats(1, kv_heads, qblocks, splits, hd);
 }
 
@@ -448,7 +486,8 @@ int attention_bf16(const __nv_bfloat16* q, const SeqInfo* seqs, int num_seqs, in
   a.q = q; a.seqs = seqs; a.kv = kv; a.layer = layer; a.nq = nq; a.G = G; a.out = out;
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
   a.qblocks = ceil_div(max_q_len * G, kRows);
-  a.splits = ceil_div(max_key / kKT + 1, kSplitTiles);
+  a.split_tiles = g_split_tiles;
+  a.splits = ceil_div(max_key / kKT + 1, a.split_tiles);
   const size_t need = attention_partial_floats(num_seqs, kv.kv_heads, a.qblocks, a.splits, hd);
   SR_REQUIRE(need <= partial_floats, "attention partial workspace too small");
   a.part_o = partials;
@@ -492,3 +531,42 @@ int attention_f32(const float* q, const SeqInfo* seqs, int num_seqs, int max_q_l
 }
 
 }  // namespace sr
+
+extern "C" int sr_set_attention_split(int tiles) {
+  SR_REQUIRE(tiles >= 4 && tiles <= 1024, "split tiles out of [4, 1024]");
+  sr::g_split_tiles = tiles;
+  return SR_OK;
+}
+
+extern "C" int sr_paged_attention(int dtype, const void* q, const void* seqs, int num_seqs, int max_q_len,
+                                  int max_key, int q_heads, int kv_heads, int head_dim, int layer,
+                                  int layers, void* kv_cache, int num_pages, const int32_t* block_table,
+                                  int max_pages, void* window, int branches, int window_max, float* partials,
+                                  uint64_t partial_floats, void* out, sr_stream_t stream) {
+  SR_REQUIRE(q_heads > 0 && kv_heads > 0 && q_heads % kv_heads == 0, "bad head counts");
+  SR_REQUIRE(layer >= 0 && layer < layers, "layer out of range");
+  sr::KvLayout kv;
+  kv.cache = kv_cache;
+  kv.block_table = block_table;
+  kv.max_pages = max_pages;
+  kv.page = 64;
+  kv.num_pages = num_pages;
+  kv.window = window;
+  kv.window_max = window_max;
+  kv.branches = branches;
+  kv.kv_heads = kv_heads;
+  kv.head_dim = head_dim;
+  kv.layers = layers;
+  const auto* sq = reinterpret_cast<const sr::SeqInfo*>(seqs);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == 1) {
+    int rc = sr::attention_bf16(reinterpret_cast<const __nv_bfloat16*>(q), sq, num_seqs, max_q_len, max_key, kv,
+                                layer, q_heads, partials, partial_floats, reinterpret_cast<__nv_bfloat16*>(out), st, 0);
+    if (rc) return rc;
+    return sr::attention_bf16(reinterpret_cast<const __nv_bfloat16*>(q), sq, num_seqs, max_q_len, max_key, kv,
+                              layer, q_heads, partials, partial_floats, reinterpret_cast<__nv_bfloat16*>(out), st, 1);
+  }
+  SR_REQUIRE(dtype == 0, "dtype must be 0 or 1");
+  return sr::attention_f32(reinterpret_cast<const float*>(q), sq, num_seqs, max_q_len, kv, layer, q_heads,
+                           reinterpret_cast<float*>(out), st);
+}

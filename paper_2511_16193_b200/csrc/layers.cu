@@ -59,6 +59,7 @@ __global__ void rope_scatter_kernel(const T* __restrict__ qkv, const int32_t* __
   T* kdst;
   T* vdst;
   int64_t head_stride;  // elements between consecutive kv heads at this slot
+  int slot_id;          // swizzle key of the destination row
   if (sq.branch < 0) {
     const int page = kv.block_table[(int64_t)sq.request * kv.max_pages + pos / kv.page];
     const int slot = pos % kv.page;
@@ -67,12 +68,14 @@ __global__ void rope_scatter_kernel(const T* __restrict__ qkv, const int32_t* __
     kdst = base + (int64_t)slot * hd;
     vdst = kdst + (int64_t)nkv * kv.page * hd;
     head_stride = (int64_t)kv.page * hd;
+    slot_id = slot;
   } else {
     T* base = reinterpret_cast<T*>(kv.window) + layer * kv.window_layer_elems() +
               (int64_t)sq.branch * 2 * nkv * kv.window_max * hd;
     kdst = base + (int64_t)j * hd;
     vdst = kdst + (int64_t)nkv * kv.window_max * hd;
     head_stride = (int64_t)kv.window_max * hd;
+    slot_id = j;
   }
   // rotate q heads and k heads (NeoX halves), copy v
   for (int e = threadIdx.x; e < (nq + nkv) * half; e += blockDim.x) {
@@ -86,13 +89,13 @@ __global__ void rope_scatter_kernel(const T* __restrict__ qkv, const int32_t* __
       q[i + half] = from_f<T>(y2);
     } else {
       T* k = kdst + (h - nq) * head_stride;
-      k[i] = from_f<T>(y1);
-      k[i + half] = from_f<T>(y2);
+      k[kv_phys<T>(slot_id, i)] = from_f<T>(y1);
+      k[kv_phys<T>(slot_id, i + half)] = from_f<T>(y2);
     }
   }
   for (int e = threadIdx.x; e < nkv * hd; e += blockDim.x) {
     const int h = e / hd, d = e % hd;
-    vdst[h * head_stride + d] = row[(nq + nkv + h) * hd + d];
+    vdst[h * head_stride + kv_phys<T>(slot_id, d)] = row[(nq + nkv + h) * hd + d];
   }
 }
 

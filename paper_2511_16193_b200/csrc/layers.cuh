@@ -38,6 +38,16 @@ struct KvLayout {
   }
 };
 
+// bf16 KV rows (paged cache and branch windows) keep their 16-byte chunks
+// XOR-swizzled by (slot & 7): a 64-slot page then streams into shared memory
+// with one bulk copy already in the bank-conflict-free layout ldmatrix reads.
+// fp32 (parity path) rows stay plain.
+template <typename T>
+__host__ __device__ __forceinline__ int kv_phys(int slot, int d) {
+  if constexpr (sizeof(T) == 2) return ((((d >> 3) ^ (slot & 7))) << 3) | (d & 7);
+  else return d;
+}
+
 template <typename T>
 int embed_rows(const T* table, const int32_t* ids, int M, int H, float* x, cudaStream_t s);
 

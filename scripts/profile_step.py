@@ -1,7 +1,7 @@
 """Short, profiler-friendly run of the bench workload's speculation step
 (1.5B-shaped target, 256 prompts, k=4 windows): prefill, then --steps steps.
 
-    ncu --set full -k regex:attn_bf16 -s 60 -c 2 python scripts/profile_step.py
+    ncu --profile-from-start off --set full -k regex:attn_bf16 -c 2 python scripts/profile_step.py
 """
 
 from __future__ import annotations
@@ -39,10 +39,13 @@ def main():
     eng = RolloutEngine(m, prompts, budget, k=4, drafters=(SyntheticDrafter(truth, trace, "draft-0.5b", 0),),
                         bonus_token=True, history=1)
     eng.prefill()
+    eng.step()
     torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStart()  # ncu --profile-from-start off
     for _ in range(a.steps):
         eng.step()
     torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStop()
     print("ok")
 
 
