@@ -147,13 +147,13 @@ def run_ours(args, rank, world, dist):
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
     lib = _native.lib()
     s = shape(args.model, args.layers)
-    steps_total = args.warmup + 2 * args.steps + 12
+    steps_total = args.warmup + 2 * args.steps + 8
     trace, prompts, budget = workload(rank, args.batch, steps_total, s.vocab)
     max_len = max(len(p) for p in prompts) + budget[0] + K + 8
     w = init_weights(s, seed=0, device="cuda")
     B = len(prompts)
     model = DeviceModel(s, w, dtype="bf16", max_requests=B, max_len=max_len,
-                        max_tokens=max(B * (K + 1), 2048), max_seqs=B)
+                        max_tokens=B * (K + 1), max_seqs=B)
     del w
     torch.cuda.empty_cache()
     # untimed: the target's greedy continuation (plain decode), which the
@@ -205,24 +205,21 @@ def run_ours(args, rank, world, dist):
     cat_n = (ctypes.c_int32 * 8)()
     lib.sr_model_profile(model.handle, 0, cat_ms, cat_n)
     if not args.eager:
-        # kernel durations: the same steps launched eagerly with CUDA events
-        # bracketing each launch on the launching stream (a graph replay
-        # cannot host per-kernel events); durations do not depend on how the
-        # launch was issued
-        prof_steps = min(args.steps, 10)
-        graph, eng.graph = eng.graph, None
+        # kernel durations: a second graph of the same step with CUDA event
+        # nodes bracketing every launch (captured on the launching stream);
+        # replayed after the timed region, read back from its last replay
         lib.sr_model_profile(model.handle, 1, None, None)
         l0 = lib.sr_launch_count()
-        for _ in range(prof_steps):
-            eng.step()
-        per_step_launches = (lib.sr_launch_count() - l0) / prof_steps
-        lib.sr_model_profile(model.handle, 0, cat_ms, cat_n)
-        # every replay launches the captured kernels once
-        launches = int(round(per_step_launches * args.steps))
-        eng.graph = graph
-        scale = args.steps / prof_steps
+        prof_graph = eng.capture(install=False)
+        per_step_launches = lib.sr_launch_count() - l0
+        for _ in range(3):
+            prof_graph.replay()
+        torch.cuda.synchronize()
+        _native.check(lib.sr_model_profile(model.handle, 0, cat_ms, cat_n), "sr_model_profile")
+        launches = int(per_step_launches * args.steps)  # every replay launches them once
         for i in range(8):
-            cat_ms[i] *= scale
+            cat_ms[i] *= args.steps
+        del prof_graph
     outs_ok = all(o == t[: len(o)] for o, t in zip(eng.outputs(), truth))
     h = hist.cpu().numpy().reshape(-1, 4)
     live = h[h[:, 0] + h[:, 2] > 0]

@@ -51,27 +51,27 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
 
-// Epilogue for 32 consecutive accumulator columns [col, col+32) of one row.
-template <int EPI>
-__device__ __forceinline__ void epilogue32(const uint32_t (&v)[32], int row, int col, int M,
-                                           int N, void* C, int ldc, const float* bias) {
+// Epilogue for W (16 or 32) consecutive accumulator columns [col, col+W) of one row.
+template <int EPI, int W = 32>
+__device__ __forceinline__ void epilogue_chunk(const uint32_t* v, int row, int col, int M, int N, void* C,
+                                               int ldc, const float* bias) {
   if (row >= M) return;
   if constexpr (EPI == kEpiArgmax) return;  // handled in the tile loop
-  float f[32];
+  float f[W];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-  const bool full = col + 32 <= N;
+  for (int i = 0; i < W; ++i) f[i] = __uint_as_float(v[i]);
+  const bool full = col + W <= N;
   if constexpr (EPI == kEpiStoreBf16 || EPI == kEpiStoreF32) {
     if (bias != nullptr) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) f[i] += (col + i < N) ? bias[col + i] : 0.0f;
+      for (int i = 0; i < W; ++i) f[i] += (col + i < N) ? bias[col + i] : 0.0f;
     }
   }
   if constexpr (EPI == kEpiStoreBf16) {
     __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)row * ldc + col;
     if (full) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < W / 8; ++q) {
         uint4 w;
         w.x = pack_bf16(f[8 * q + 0], f[8 * q + 1]);
         w.y = pack_bf16(f[8 * q + 2], f[8 * q + 3]);
@@ -80,30 +80,31 @@ __device__ __forceinline__ void epilogue32(const uint32_t (&v)[32], int row, int
         reinterpret_cast<uint4*>(out)[q] = w;
       }
     } else {
-      for (int i = 0; i < 32 && col + i < N; ++i) out[i] = __float2bfloat16_rn(f[i]);
+      for (int i = 0; i < W && col + i < N; ++i) out[i] = __float2bfloat16_rn(f[i]);
     }
   } else if constexpr (EPI == kEpiStoreF32) {
     float* out = reinterpret_cast<float*>(C) + (int64_t)row * ldc + col;
     if (full) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
+      for (int q = 0; q < W / 4; ++q)
         reinterpret_cast<float4*>(out)[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
     } else {
-      for (int i = 0; i < 32 && col + i < N; ++i) out[i] = f[i];
+      for (int i = 0; i < W && col + i < N; ++i) out[i] = f[i];
     }
   } else if constexpr (EPI == kEpiResidualF32) {
     float* out = reinterpret_cast<float*>(C) + (int64_t)row * ldc + col;
     if (full) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < W / 4; ++q) {
         float4 r = reinterpret_cast<float4*>(out)[q];
         r.x += f[4 * q]; r.y += f[4 * q + 1]; r.z += f[4 * q + 2]; r.w += f[4 * q + 3];
         reinterpret_cast<float4*>(out)[q] = r;
       }
     } else {
-      for (int i = 0; i < 32 && col + i < N; ++i) out[i] += f[i];
+      for (int i = 0; i < W && col + i < N; ++i) out[i] += f[i];
     }
   } else if constexpr (EPI == kEpiSwiGLU) {
+    static_assert(EPI != kEpiSwiGLU || W == 32, "SwiGLU pairs 16 gate + 16 up columns");
     // columns [col, col+16) are gate, [col+16, col+32) the matching up rows
     __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)row * ldc + col / 2;
     if (full) {
@@ -118,6 +119,12 @@ __device__ __forceinline__ void epilogue32(const uint32_t (&v)[32], int row, int
       }
     }
   }
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue32(const uint32_t (&v)[32], int row, int col, int M, int N, void* C,
+                                           int ldc, const float* bias) {
+  epilogue_chunk<EPI, 32>(v, row, col, M, N, C, ldc, bias);
 }
 
 template <int BN, int EPI>
@@ -254,6 +261,166 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): the pair computes a 256 x BN tile; each CTA
+// stages its own 128 activation rows and BN/2 weight rows per k-block, the
+// leader issues tcgen05.mma.cta_group::2 (M=256) reading both CTAs' shared
+// memory, and each CTA's TMEM holds its 128 accumulator rows.  Per SM this
+// halves the weight bytes per MAC, the bound of the 1-CTA kernel.
+
+template <int BN>
+struct PairCfg {
+  static constexpr int kBNH = BN / 2;
+  static constexpr uint32_t kABytes = kBM * kBK * 2;
+  static constexpr uint32_t kBBytes = kBNH * kBK * 2;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (196608 / kStageBytes) < 8 ? (196608 / kStageBytes) : 8;
+  static constexpr uint32_t kTmemCols = 2 * BN <= 256 ? 256 : 512;
+  static constexpr int kChunk = BN % 32 == 0 ? 32 : 16;
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * kStageBytes + 256;
+};
+
+template <int BN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 int M, int N, int K, void* C, int ldc, const float* __restrict__ bias,
+                 int32_t* __restrict__ aux) {
+  using Cfg = PairCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  constexpr int CW = Cfg::kChunk;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = sm100::cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int num_m = (M + 2 * kBM - 1) / (2 * kBM), num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch_desc(&tmA);
+    sm100::tma_prefetch_desc(&tmB);
+    for (int s = 0; s < S; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      sm100::mbar_init(&tfull[a], 1);
+      sm100::mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc_pair<Cfg::kTmemCols>(tmem_slot);
+  sm100::tc_fence_before();
+  sm100::cluster_sync();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs) {
+        const int m_blk = tile % num_m, n_blk = tile / num_m;
+        const int arow = m_blk * 2 * kBM + (int)rank * kBM;
+        const int brow = n_blk * BN + (int)rank * Cfg::kBNH;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) sm100::mbar_arrive_expect_tx(&full[stage], 2 * Cfg::kStageBytes);
+          sm100::tma_load_2d_pair(sA + stage * Cfg::kABytes, &tmA, &full[stage], kb * kBK, arow,
+                                  sm100::kEvictLast);
+          sm100::tma_load_2d_pair(sB + stage * Cfg::kBBytes, &tmB, &full[stage], kb * kBK, brow,
+                                  sm100::kEvictNormal);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = sm100::umma_idesc_bf16(2 * kBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs) {
+        sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          sm100::mbar_wait(&full[stage], phase);
+          sm100::tc_fence_after();
+          const uint32_t a0 = sm100::smem_u32(sA + stage * Cfg::kABytes);
+          const uint32_t b0 = sm100::smem_u32(sB + stage * Cfg::kBBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            sm100::umma_bf16_pair(d, sm100::umma_desc_sw128(a0 + k * 32), sm100::umma_desc_sw128(b0 + k * 32),
+                                  idesc, (kb | k) != 0);
+          sm100::umma_commit_pair(&empty[stage], 0x3);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+        sm100::umma_commit_pair(&tfull[acc], 0x3);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    const int quad = warp & 3;
+    const uint32_t leader_tempty = sm100::mapa_shared(sm100::smem_u32(tempty), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = pair; tile < num_tiles; tile += npairs) {
+      const int m_blk = tile % num_m, n_blk = tile / num_m;
+      sm100::mbar_wait(&tfull[acc], acc_phase);
+      sm100::tc_fence_after();
+      const int row = m_blk * 2 * kBM + (int)rank * kBM + quad * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      float best = -INFINITY;
+      int best_idx = 0x7fffffff;
+#pragma unroll 1
+      for (int c = 0; c < BN / CW; ++c) {
+        uint32_t v[CW];
+        if constexpr (CW == 32) sm100::tmem_ld_32x32b_x32(taddr + c * CW, *reinterpret_cast<uint32_t(*)[32]>(v));
+        else sm100::tmem_ld_32x32b_x16(taddr + c * CW, v);
+        sm100::tmem_ld_wait();
+        const int col = n_blk * BN + c * CW;
+        if constexpr (EPI == kEpiArgmax) {
+#pragma unroll
+          for (int i = 0; i < CW; ++i) {
+            const float f = __uint_as_float(v[i]);
+            if (col + i < N && f > best) { best = f; best_idx = col + i; }
+          }
+        } else {
+          if (col < N) epilogue_chunk<EPI, CW>(v, row, col, M, N, C, ldc, bias);
+        }
+      }
+      if constexpr (EPI == kEpiArgmax) {
+        if (row < M) {
+          const int tiles_n = (N + BN - 1) / BN;
+          reinterpret_cast<float*>(C)[(int64_t)row * tiles_n + n_blk] = best;
+          aux[(int64_t)row * tiles_n + n_blk] = best_idx;
+        }
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive_cluster(leader_tempty + acc * 8);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  sm100::tc_fence_before();
+  sm100::cluster_sync();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc_pair<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (fn == nullptr) {
@@ -305,6 +472,68 @@ int launch_bn(const GemmPlan& p, int M, cudaStream_t stream) {
   return config_error("unknown epilogue");
 }
 
+
+template <int BN, int EPI>
+int launch_pair_typed(const GemmPlan& p, int M, cudaStream_t stream) {
+  using Cfg = PairCfg<BN>;
+  auto kern = gemm_pair_kernel<BN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SR_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
+    attr_set = true;
+  }
+  const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * ((p.N + BN - 1) / BN);
+  const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+  kern<<<2 * pairs, kThreads, Cfg::kSmem, stream>>>(p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux);
+  return check_launch("gemm_pair_kernel");
+}
+
+template <int BN>
+int launch_pair_bn(const GemmPlan& p, int M, cudaStream_t stream) {
+  switch (p.epi) {
+    case kEpiStoreBf16: return launch_pair_typed<BN, kEpiStoreBf16>(p, M, stream);
+    case kEpiResidualF32: return launch_pair_typed<BN, kEpiResidualF32>(p, M, stream);
+    case kEpiStoreF32: return launch_pair_typed<BN, kEpiStoreF32>(p, M, stream);
+    case kEpiArgmax: return launch_pair_typed<BN, kEpiArgmax>(p, M, stream);
+    case kEpiSwiGLU:
+      if constexpr (BN % 32 == 0) return launch_pair_typed<BN, kEpiSwiGLU>(p, M, stream);
+      return config_error("SwiGLU needs a tile width that is a multiple of 32");
+  }
+  return config_error("unknown epilogue");
+}
+
+int launch_pair(const GemmPlan& p, int M, cudaStream_t stream) {
+  switch (p.bn) {
+    case 64: return launch_pair_bn<64>(p, M, stream);
+    case 96: return launch_pair_bn<96>(p, M, stream);
+    case 112: return launch_pair_bn<112>(p, M, stream);
+    case 128: return launch_pair_bn<128>(p, M, stream);
+    case 160: return launch_pair_bn<160>(p, M, stream);
+    case 192: return launch_pair_bn<192>(p, M, stream);
+    case 224: return launch_pair_bn<224>(p, M, stream);
+    case 256: return launch_pair_bn<256>(p, M, stream);
+  }
+  return config_error("unsupported pair tile width (64|96|112|128|160|192|224|256)");
+}
+
+// Pair tile width minimizing waves x per-tile time, where a k-block costs
+// max(MMA: 2*BN clk, operand ingress: (16 KB + 64*BN B) / 62 B/clk per SM).
+int choose_pair_bn(int M, int N, int epi) {
+  static const int cands[] = {256, 224, 192, 160, 128, 112, 96, 64};
+  const int pairs = num_sms() / 2;
+  const int num_m = (M + 255) / 256;
+  int best = 256;
+  double best_t = 1e30;
+  for (int bn : cands) {
+    if (epi == kEpiSwiGLU && bn % 32 != 0) continue;
+    const int tiles = num_m * ((N + bn - 1) / bn);
+    const int waves = (tiles + pairs - 1) / pairs;
+    const double kb = fmax(2.0 * bn, (16384.0 + 64.0 * bn) / 62.0);
+    const double t = waves * kb;
+    if (t < best_t * 0.999) { best_t = t; best = bn; }
+  }
+  return best;
+}
 }  // namespace
 
 int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
@@ -338,20 +567,32 @@ int gemm_bf16_plan(GemmPlan* p, int M, int N, int K, const __nv_bfloat16* A, int
   SR_REQUIRE(epi == kEpiArgmax || ldc % 8 == 0, "ldc must be a multiple of 8");
   SR_REQUIRE(((uintptr_t)A & 15) == 0 && ((uintptr_t)W & 15) == 0 && ((uintptr_t)C & 15) == 0,
              "A, W, C must be 16-byte aligned");
-  if (bn == 0) bn = N >= 4096 ? 256 : 128;
-  SR_REQUIRE(bn == 128 || bn == 256, "bn must be 128 or 256");
-  SR_REQUIRE(epi != kEpiSwiGLU || N % 32 == 0, "SwiGLU needs N % 32 == 0");
+  bool pair;
+  if (bn == 0) {
+    pair = M >= 256;
+    bn = pair ? choose_pair_bn(M, N, epi) : (N >= 4096 ? 256 : 128);
+  } else if (bn < 0) {
+    pair = true;
+    bn = -bn;
+  } else {
+    pair = false;
+    SR_REQUIRE(bn == 128 || bn == 256, "single-CTA bn must be 128 or 256");
+  }
+  if (pair) SR_REQUIRE(bn % 16 == 0 && bn >= 64 && bn <= 256, "pair bn must be a multiple of 16 in [64, 256]");
+  SR_REQUIRE(epi != kEpiSwiGLU || (N % 32 == 0 && bn % 32 == 0), "SwiGLU needs N and bn multiples of 32");
   p->M = M; p->N = N; p->K = K; p->bn = bn; p->epi = epi; p->c = C; p->ldc = ldc; p->bias = bias;
   p->aux = aux;
+  p->pair = pair;
   const int mrows = M > 0 ? M : 1;
   int rc = make_tmap_bf16(&p->a, A, (uint64_t)K, (uint64_t)mrows, (uint64_t)lda * 2, kBK, kBM);
   if (rc) return rc;
-  return make_tmap_bf16(&p->b, W, (uint64_t)K, (uint64_t)N, (uint64_t)ldw * 2, kBK, bn);
+  return make_tmap_bf16(&p->b, W, (uint64_t)K, (uint64_t)N, (uint64_t)ldw * 2, kBK, pair ? bn / 2 : bn);
 }
 
 int gemm_bf16_launch(const GemmPlan& p, cudaStream_t stream, int m_override) {
   const int M = m_override >= 0 ? m_override : p.M;
   if (M == 0) return SR_OK;
+  if (p.pair) return launch_pair(p, M, stream);
   return p.bn == 256 ? launch_bn<256>(p, M, stream) : launch_bn<128>(p, M, stream);
 }
 

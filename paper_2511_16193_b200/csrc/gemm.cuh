@@ -23,6 +23,7 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t 
 struct GemmPlan {
   CUtensorMap a, b;
   int M, N, K, bn, epi;
+  bool pair;          // CTA-pair (cta_group::2, 256-row tiles) kernel
   void* c;
   int ldc;
   const float* bias;
@@ -30,6 +31,10 @@ struct GemmPlan {
 };
 
 // Build a plan (tensor maps) once; launch many times (graph-capturable).
+// bn > 0: single-CTA kernel with that tile width (128 | 256); bn < 0: CTA-pair
+// kernel with width -bn (multiple of 16, <= 256); bn == 0: choose from
+// (M, N, K) -- M is the plan's capacity, so the choice (and hence the
+// accumulation order) never depends on how many rows a launch carries.
 int gemm_bf16_plan(GemmPlan* plan, int M, int N, int K, const __nv_bfloat16* A, int lda,
                    const __nv_bfloat16* W, int ldw, void* C, int ldc, int epi,
                    const float* bias, int bn, int32_t* aux = nullptr);

@@ -22,21 +22,56 @@ __global__ void embed_kernel(const T* __restrict__ table, const int32_t* __restr
   for (int i = threadIdx.x; i < H; i += blockDim.x) dst[i] = to_f(src[i]);
 }
 
-// One warp per row: lane-strided sum of squares, xor-shuffle tree (fixed
-// order), then scale.  Matches oracle: y = x * rsqrt(mean(x^2) + eps) * w.
+// One warp per row: float4 loads (all issued before the reduction), xor-
+// shuffle tree (fixed order), then scale.  Matches the oracle:
+// y = x * rsqrt(mean(x^2) + eps) * w.  H % 4 == 0 takes the vector path.
 template <typename T>
-__global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ w, int M,
-                               int H, float eps, T* __restrict__ out) {
+__global__ void __launch_bounds__(256)
+rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ w, int M, int H, float eps,
+               T* __restrict__ out) {
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
   const float* xr = x + (int64_t)row * H;
+  T* orow = out + (int64_t)row * H;
   float ss = 0.0f;
+  if ((H & 3) == 0) {
+    const float4* x4 = reinterpret_cast<const float4*>(xr);
+    const int n4 = H >> 2;
+    float4 buf[12];
+#pragma unroll
+    for (int i = 0; i < 12; ++i)
+      buf[i] = (lane + 32 * i < n4) ? x4[lane + 32 * i] : make_float4(0, 0, 0, 0);
+    for (int i = 12 * 32 + lane; i < n4; i += 32) {  // rows wider than 1536
+      const float4 v = x4[i];
+      ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
+    }
+#pragma unroll
+    for (int i = 0; i < 12; ++i) {
+      ss = fmaf(buf[i].x, buf[i].x, ss); ss = fmaf(buf[i].y, buf[i].y, ss);
+      ss = fmaf(buf[i].z, buf[i].z, ss); ss = fmaf(buf[i].w, buf[i].w, ss);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float r = rsqrtf(ss / (float)H + eps);
+    const float4* w4 = reinterpret_cast<const float4*>(w);
+    auto emit = [&](int i, float4 v) {
+      const float4 g = w4[i];
+      orow[4 * i + 0] = from_f<T>(v.x * r * g.x);
+      orow[4 * i + 1] = from_f<T>(v.y * r * g.y);
+      orow[4 * i + 2] = from_f<T>(v.z * r * g.z);
+      orow[4 * i + 3] = from_f<T>(v.w * r * g.w);
+    };
+#pragma unroll
+    for (int j = 0; j < 12; ++j)
+      if (lane + 32 * j < n4) emit(lane + 32 * j, buf[j]);
+    for (int i = 12 * 32 + lane; i < n4; i += 32) emit(i, x4[i]);
+    return;
+  }
   for (int i = lane; i < H; i += 32) ss = fmaf(xr[i], xr[i], ss);
 #pragma unroll
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   const float r = rsqrtf(ss / (float)H + eps);
-  T* orow = out + (int64_t)row * H;
   for (int i = lane; i < H; i += 32) orow[i] = from_f<T>(xr[i] * r * w[i]);
 }
 
@@ -77,7 +112,47 @@ __global__ void rope_scatter_kernel(const T* __restrict__ qkv, const int32_t* __
     head_stride = (int64_t)kv.window_max * hd;
     slot_id = j;
   }
-  // rotate q heads and k heads (NeoX halves), copy v
+  // rotate q heads and k heads (NeoX halves), copy v.  Vector path: a thread
+  // owns 8 consecutive dims of the first half and the matching 8 of the
+  // second half, so every load/store is one 16-byte chunk (the cache swizzle
+  // permutes whole chunks).
+  if constexpr (sizeof(T) == 2) {
+    if ((half & 7) == 0) {
+      const int cph = half / 8;  // chunks per half-head
+      for (int e = threadIdx.x; e < (nq + nkv) * cph; e += blockDim.x) {
+        const int h = e / cph, c = e % cph, i0 = c * 8;
+        const uint4 a = *reinterpret_cast<const uint4*>(row + h * hd + i0);
+        const uint4 b = *reinterpret_cast<const uint4*>(row + h * hd + i0 + half);
+        const T* pa = reinterpret_cast<const T*>(&a);
+        const T* pb = reinterpret_cast<const T*>(&b);
+        uint4 ya, yb;
+        T* qa = reinterpret_cast<T*>(&ya);
+        T* qb = reinterpret_cast<T*>(&yb);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const float cc = cr[i0 + t], ss = sr_[i0 + t];
+          const float x1 = to_f(pa[t]), x2 = to_f(pb[t]);
+          qa[t] = from_f<T>(x1 * cc - x2 * ss);
+          qb[t] = from_f<T>(x2 * cc + x1 * ss);
+        }
+        if (h < nq) {
+          T* q = q_out + (int64_t)tok * nq * hd + h * hd;
+          *reinterpret_cast<uint4*>(q + i0) = ya;
+          *reinterpret_cast<uint4*>(q + i0 + half) = yb;
+        } else {
+          T* k = kdst + (h - nq) * head_stride;
+          *reinterpret_cast<uint4*>(k + kv_phys<T>(slot_id, i0)) = ya;
+          *reinterpret_cast<uint4*>(k + kv_phys<T>(slot_id, i0 + half)) = yb;
+        }
+      }
+      for (int e = threadIdx.x; e < nkv * (hd / 8); e += blockDim.x) {
+        const int h = e / (hd / 8), d = (e % (hd / 8)) * 8;
+        *reinterpret_cast<uint4*>(vdst + h * head_stride + kv_phys<T>(slot_id, d)) =
+            *reinterpret_cast<const uint4*>(row + (nq + nkv + h) * hd + d);
+      }
+      return;
+    }
+  }
   for (int e = threadIdx.x; e < (nq + nkv) * half; e += blockDim.x) {
     const int h = e / half, i = e % half;
     const float c = cr[i], s = sr_[i];

@@ -39,7 +39,7 @@ int kv_commit(int B, int N, const SeqInfo* seqs, const int32_t* outcome, const i
 namespace {
 
 constexpr int kLayerPtrs = 7;  // ln1, w_qkv, b_qkv, w_o, ln2, w_gu, w_down
-constexpr int kLmBn = 128;
+constexpr int kLmBn = 64;  // smallest lm_head tile width: sizes the argmax partials
 
 __global__ void gather_rows_kernel(const void* __restrict__ src, const int32_t* __restrict__ rows, int H,
                                    int esize, void* __restrict__ dst) {
@@ -82,14 +82,22 @@ struct Profiler {
     }
     return pool[next++];
   }
+  // Inside stream capture the record must be an *external* event node, or
+  // the replayed graph would not time it.
+  static void record(cudaEvent_t e, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+    else cudaEventRecord(e, st);
+  }
   void begin(int cat, cudaStream_t st) {
     if (!on) return;
     marks.push_back({cat, (int)next});
-    cudaEventRecord(take(), st);
+    record(take(), st);
   }
   void end(cudaStream_t st) {
     if (!on) return;
-    cudaEventRecord(take(), st);
+    record(take(), st);
   }
   ~Profiler() {
     for (auto e : pool) cudaEventDestroy(e);
@@ -224,7 +232,8 @@ int sr_model_create(const sr_model_desc* desc, void** handle) {
       if (rc) { delete m; return rc; }
     }
     rc = sr::gemm_bf16_plan(&m->p_lm_argmax, T, d.vocab, H, (const bf*)m->h_sel, H, (const bf*)d.lm_head, H,
-                            m->part_val, m->lm_tiles, sr::kEpiArgmax, nullptr, sr::kLmBn, m->part_idx);
+                            m->part_val, m->lm_tiles, sr::kEpiArgmax, nullptr, 0, m->part_idx);
+    if (!rc) m->lm_tiles = sr::gemm_num_n_tiles(d.vocab, m->p_lm_argmax.bn);
     if (!rc && m->logits)
       rc = sr::gemm_bf16_plan(&m->p_lm_logits, T, d.vocab, H, (const bf*)m->h_sel, H, (const bf*)d.lm_head, H,
                               m->logits, (d.vocab + 7) / 8 * 8, sr::kEpiStoreF32, nullptr, 0);

@@ -200,8 +200,9 @@ class RolloutEngine:
             self._enqueue_step(slot)
         self.steps += 1
 
-    def capture(self) -> None:
-        """Capture one step (history slot 0) into a CUDA graph."""
+    def capture(self, install: bool = True):
+        """Capture one step (history slot 0) into a CUDA graph; ``install``
+        makes :meth:`step` replay it."""
         if self.history.shape[0] != 1:
             raise ConfigError("graph capture needs history=0/1 (the graph writes slot 0)")
         torch.cuda.synchronize()
@@ -213,7 +214,9 @@ class RolloutEngine:
             self._enqueue_step(0)
             g.capture_end()
         torch.cuda.current_stream().wait_stream(s)
-        self.graph = g
+        if install:
+            self.graph = g
+        return g
 
     # -- host views -------------------------------------------------------------
 

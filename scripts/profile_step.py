@@ -34,7 +34,7 @@ def main():
                for r in trace]
     budget = [64] * a.batch
     m = DeviceModel(s, init_weights(s, seed=0, device="cuda"), dtype="bf16", max_requests=a.batch,
-                    max_len=1024 + 80, max_tokens=max(a.batch * 5, 2048), max_seqs=a.batch)
+                    max_len=1024 + 80, max_tokens=a.batch * 5, max_seqs=a.batch)
     truth = [list(np.random.default_rng(i).integers(0, s.vocab, size=64)) for i in range(a.batch)]
     eng = RolloutEngine(m, prompts, budget, k=4, drafters=(SyntheticDrafter(truth, trace, "draft-0.5b", 0),),
                         bonus_token=True, history=1)

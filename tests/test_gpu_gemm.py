@@ -103,3 +103,67 @@ def test_f32_gemm(M, N, K):
         S = torch.empty(M, N // 2, device="cuda")
         sr_gemm(A, W, S, EPI_SWIGLU)
         torch.testing.assert_close(S.double(), swiglu_ref(exp), rtol=1e-5, atol=1e-5)
+
+
+PAIR_CASES = [(1280, 1536, 1536, -112), (1280, 2048, 1536, -160), (300, 1000, 192, -112),
+              (77, 512, 8960, -128), (1280, 17920, 1536, -256), (513, 3000, 640, -96),
+              (256, 4096, 256, -224), (1000, 768, 896, -64), (1280, 1536, 8960, -192)]
+
+
+@pytest.mark.parametrize("M,N,K,bn", PAIR_CASES)
+def test_bf16_pair_kernel(M, N, K, bn):
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g)
+    exp = ref(A, W, bias)
+    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    sr_gemm(A, W, C, EPI_STORE, bias, bn)
+    torch.testing.assert_close(C.float(), exp, rtol=1e-2, atol=1e-2)
+    C32 = torch.empty(M, N, device="cuda")
+    sr_gemm(A, W, C32, EPI_F32, bias, bn)
+    torch.testing.assert_close(C32, exp, rtol=1e-4, atol=1e-3)
+    R = torch.randn(M, N, device="cuda", generator=g)
+    C = R.clone()
+    sr_gemm(A, W, C, EPI_RESID, None, bn)
+    torch.testing.assert_close(C, R + ref(A, W), rtol=1e-4, atol=1e-3)
+    if N % 32 == 0 and (-bn) % 32 == 0:
+        S = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+        sr_gemm(A, W, S, EPI_SWIGLU, None, bn)
+        torch.testing.assert_close(S.float(), swiglu_ref(ref(A, W)), rtol=1e-2, atol=1e-2)
+
+
+@pytest.mark.parametrize("bn", [-256, -112, 128, 256])
+def test_argmax_epilogue(bn):
+    from paper_2511_16193_b200 import _native
+
+    lib = _native.lib()
+    M, N, K = 300, 151936, 256
+    g = torch.Generator(device="cuda").manual_seed(11)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    width = -bn if bn < 0 else bn
+    tiles = (N + width - 1) // width
+    pv = torch.empty(M, tiles, device="cuda")
+    pi = torch.empty(M, tiles, device="cuda", dtype=torch.int32)
+    _native.check(lib.sr_gemm(1, M, N, K, A.data_ptr(), K, W.data_ptr(), K, pv.data_ptr(), tiles, 4, None, bn,
+                              pi.data_ptr(), _native.stream_handle()), "sr_gemm argmax")
+    torch.cuda.synchronize()
+    logits = torch.empty(M, N, device="cuda")
+    sr_gemm(A, W, logits, EPI_F32, None, bn)
+    best = pv.max(1)
+    idx = pi.gather(1, best.indices[:, None])[:, 0]
+    assert torch.equal(idx.long(), logits.argmax(1))
+    assert torch.equal(best.values, logits.max(1).values)
+
+
+def test_pair_batch_invariance():
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randn(1280, 1536, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(1536, 1536, device="cuda", generator=g) * 0.05).bfloat16()
+    big = torch.empty(1280, 1536, device="cuda")
+    sr_gemm(A, W, big, EPI_F32, None, -112)
+    for start in (0, 5, 256, 1275):
+        small = torch.empty(5, 1536, device="cuda")
+        sr_gemm(A[start:start + 5].contiguous(), W, small, EPI_F32, None, -112)
+        assert torch.equal(small, big[start:start + 5])
