@@ -68,12 +68,14 @@ def parse():
 # -- workload -------------------------------------------------------------------
 
 
-def workload(rank: int, batch: int, steps_total: int, vocab: int):
+def workload(rank: int, batch: int, steps_total: int, vocab: int, world: int = 1):
     from paper_2511_16193_b200 import scenarios
+    from paper_2511_16193_b200.dist import shard
     from paper_2511_16193_b200.streams import stream
     from paper_2511_16193_b200.workload import gen_trace
 
-    trace = gen_trace(scenarios.default_trace_spec(batch=batch * (rank + 1), seed=0))[rank * batch:]
+    # global batch of batch*world prompts, round-robin over ranks (sim.py:307-309)
+    trace = shard(gen_trace(scenarios.default_trace_spec(batch=batch * world, seed=0)), rank, world)
     prompts = [stream(0, r.id, "prompt").integers(0, vocab, size=r.prompt_len).astype(np.int32)
                for r in trace]
     # budget large enough that no request leaves the batch during the run
@@ -130,6 +132,17 @@ class ClockSampler:
 # -- our arm -------------------------------------------------------------------------
 
 
+def traffic_bytes():
+    f = ROOT / "profiles" / "r01" / "ncu_step_layer0.json"
+    try:
+        for d in json.loads(f.read_text()):
+            if "gemm" in d["kernel"] and ", 2>" in d["kernel"]:
+                return d["dram_read_bytes"] + d["dram_write_bytes"]
+    except Exception:
+        return None
+    return None
+
+
 def peaks():
     if PEAKS.exists():
         d = json.loads(PEAKS.read_text())
@@ -148,7 +161,7 @@ def run_ours(args, rank, world, dist):
     lib = _native.lib()
     s = shape(args.model, args.layers)
     steps_total = args.warmup + 2 * args.steps + 8
-    trace, prompts, budget = workload(rank, args.batch, steps_total, s.vocab)
+    trace, prompts, budget = workload(rank, args.batch, steps_total, s.vocab, world)
     max_len = max(len(p) for p in prompts) + budget[0] + K + 8
     w = init_weights(s, seed=0, device="cuda")
     B = len(prompts)
@@ -250,14 +263,11 @@ def run_ours(args, rank, world, dist):
     e2e_ms = e0.elapsed_time(e1)
     e2e_committed = int((eng.gen_len.sum() - gen1).item())
 
-    # ---- cross-rank reduction
-    t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device="cuda")
-    c = torch.tensor([committed, e2e_committed], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(c, op=dist.ReduceOp.SUM)
-    ms_max, e2e_max = float(t[0]), float(t[1])
-    tot_committed, tot_e2e = float(c[0]), float(c[1])
+    # ---- cross-rank reduction: max time, summed tokens
+    from paper_2511_16193_b200.dist import reduce_step_stats
+
+    (ms_max, e2e_max), (tot_committed, tot_e2e) = reduce_step_stats(
+        [ms, e2e_ms], [committed, e2e_committed], dist, device="cuda")
 
     # ---- roofline of the dominant kernel family: the verify GEMMs (tensor-bound)
     gemm_ms = sum(cat_ms[i] for i in range(5))
@@ -274,7 +284,7 @@ def run_ours(args, rank, world, dist):
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init N(0,0.02) weights; keyed-stream prompt tokens; reference trace lengths)",
         "config": {"workload": f"configs[1]: {args.model}-shaped target, batch {B}/GPU, k={K}, "
-                               "single n-gram drafter (min_n=1,max_n=3), greedy exact match, bonus token",
+                               f"single {args.drafter} drafter, greedy exact match, bonus token",
                    "model": args.model, "layers": s.layers, "batch_per_gpu": B, "global_batch": B * world,
                    "k": K, "verify_rows_per_step": rows, "prompt_len": "U[128,1024] (default_trace_spec)",
                    "parallelism": f"prompt-sharded x{world} (no data-path collective)",
@@ -292,7 +302,10 @@ def run_ours(args, rank, world, dist):
                      "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
                      "frac": (achieved / sustained) if achieved else None,
                      "peak_source": f"{src} bf16_tflops_sustained (kernels timed inside the step)",
-                     "traffic": None,
+                     "traffic": traffic_bytes(),
+                     "traffic_note": "DRAM read+write bytes per launch of the largest verify GEMM (gate_up "
+                                     "+SwiGLU) from profiles/r01/ncu_step_layer0.json (ncu --set full); "
+                                     "algorithmic = 55.0 MB weights + 3.9 MB activations + 2.3 MB output",
                      "algorithmic_flops_per_step": flops_step,
                      "gemm_ms_per_step": gemm_ms / args.steps,
                      "gemm_share_of_step": (gemm_ms / args.steps) / step_ms,
