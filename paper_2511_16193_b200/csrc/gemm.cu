@@ -377,10 +377,53 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint32_t acc_phase = 0;
     for (int tile = pair; tile < num_tiles; tile += npairs) {
       const int m_blk = tile % num_m, n_blk = tile / num_m;
-      sm100::mbar_wait(&tfull[acc], acc_phase);
-      sm100::tc_fence_after();
       const int row = m_blk * 2 * kBM + (int)rank * kBM + quad * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      if constexpr (EPI == kEpiResidualF32 && BN <= 128) {
+        // Residual epilogue: the warps are idle during the mainloop, so pull
+        // this row's residual slice into registers before the accumulator is
+        // ready; the add + store then never waits on a global load.
+        float res[BN];
+        float* xr = reinterpret_cast<float*>(C) + (int64_t)row * ldc + n_blk * BN;
+        const bool row_ok = row < M;
+        const bool vec = row_ok && n_blk * BN + BN <= N;
+#pragma unroll
+        for (int q = 0; q < BN / 4; ++q) {
+          float4 r4 = make_float4(0, 0, 0, 0);
+          if (vec) r4 = reinterpret_cast<const float4*>(xr)[q];
+          res[4 * q] = r4.x; res[4 * q + 1] = r4.y; res[4 * q + 2] = r4.z; res[4 * q + 3] = r4.w;
+        }
+        sm100::mbar_wait(&tfull[acc], acc_phase);
+        sm100::tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < BN / CW; ++c) {
+          uint32_t v[CW];
+          if constexpr (CW == 32) sm100::tmem_ld_32x32b_x32(taddr + c * CW, *reinterpret_cast<uint32_t(*)[32]>(v));
+          else sm100::tmem_ld_32x32b_x16(taddr + c * CW, v);
+          sm100::tmem_ld_wait();
+          const int col = n_blk * BN + c * CW;
+          if (vec) {
+#pragma unroll
+            for (int q = 0; q < CW / 4; ++q) {
+              float4 o4;
+              o4.x = res[c * CW + 4 * q] + __uint_as_float(v[4 * q]);
+              o4.y = res[c * CW + 4 * q + 1] + __uint_as_float(v[4 * q + 1]);
+              o4.z = res[c * CW + 4 * q + 2] + __uint_as_float(v[4 * q + 2]);
+              o4.w = res[c * CW + 4 * q + 3] + __uint_as_float(v[4 * q + 3]);
+              reinterpret_cast<float4*>(xr)[c * CW / 4 + q] = o4;
+            }
+          } else if (row_ok && col < N) {
+            epilogue_chunk<EPI, CW>(v, row, col, M, N, C, ldc, bias);
+          }
+        }
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive_cluster(leader_tempty + acc * 8);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        continue;
+      }
+      sm100::mbar_wait(&tfull[acc], acc_phase);
+      sm100::tc_fence_after();
       float best = -INFINITY;
       int best_idx = 0x7fffffff;
 #pragma unroll 1
@@ -519,7 +562,9 @@ int launch_pair(const GemmPlan& p, int M, cudaStream_t stream) {
 // Pair tile width minimizing waves x per-tile time, where a k-block costs
 // max(MMA: 2*BN clk, operand ingress: (16 KB + 64*BN B) / 62 B/clk per SM).
 int choose_pair_bn(int M, int N, int epi) {
-  static const int cands[] = {256, 224, 192, 160, 128, 112, 96, 64};
+  // multiples of 32 only: 16-column epilogue chunks and N % 32 != 0 MMAs
+  // measured slower on B200 (scripts/gemm_probe.py)
+  static const int cands[] = {256, 224, 192, 160, 128, 96, 64};
   const int pairs = num_sms() / 2;
   const int num_m = (M + 255) / 256;
   int best = 256;
