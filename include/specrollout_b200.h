@@ -40,6 +40,10 @@ const char* sr_last_error(void);
 /* Number of SMs of the current device (for grid sizing by callers). */
 int sr_device_sm_count(void);
 
+/* sizeof(sr_model_desc), sizeof(sr_forward_args), sizeof(sr_seq_info) into
+ * out[0..n) -- lets bindings verify their struct mirrors (no GPU needed). */
+int sr_abi_sizes(int64_t* out, int n);
+
 /* Kernels launched by this library since load (bench evidence). */
 long long sr_launch_count(void);
 
@@ -179,7 +183,8 @@ typedef struct sr_forward_args {
   int32_t num_tokens, num_seqs;
   int32_t max_q_len;        /* host upper bound of q_len over the sequences */
   int32_t max_key;          /* host upper bound of ctx_len + q_len - 1 */
-  int32_t output;           /* 0: argmax ids (int32 [rows]) ; 1: fp32 logits [rows, vocab] */
+  int32_t output;           /* 0: argmax ids (int32 [rows]); 1: fp32 logits [rows, vocab];
+                               2: keyed sample at `temperature` (int32 [rows]) */
   int32_t num_logit_rows;   /* rows of logit_rows (ignored when it is NULL) */
   const int32_t* token_ids; /* [num_tokens] */
   const int32_t* positions; /* [num_tokens] */
@@ -187,7 +192,18 @@ typedef struct sr_forward_args {
   const int32_t* logit_rows;/* optional token rows to project (e.g. last prompt token) */
   void* out;
   float* out_val;           /* optional max logit per row (argmax output) */
+  float temperature;        /* output 2: T > 0 */
+  uint32_t seed;            /* output 2: sampling stream seed */
 } sr_forward_args;
+
+/* Keyed Gumbel-max sampling of fp32 logit rows:
+ *   id = argmax_v logits[r, v] / T + G(seed, req[r], pos[r], v)
+ * with G from Philox4x32-10 keyed by (seed, request), counter (position, v/4).
+ * The draw is a pure function of (seed, request, position), so speculative and
+ * plain decoding sample identical tokens.  Same noise as the
+ * fused lm_head epilogue of sr_model_forward(output = 2). */
+int sr_sample_rows(const float* logits, int rows, int vocab, int ld, const int32_t* req, const int32_t* pos,
+                   uint32_t seed, float temperature, int32_t* ids, sr_stream_t stream);
 
 /* K2 alone: paged GQA attention of the verify rows described by seqs over
  * one layer of the KV cache (layouts as above; bf16 rows pre-swizzled in

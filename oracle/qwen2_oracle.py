@@ -22,7 +22,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from oracle import ngram_oracle
+from oracle import ngram_oracle, sampling_oracle
 
 
 class Qwen2Oracle:
@@ -105,23 +105,32 @@ class Qwen2Oracle:
             seq.append(tok)
         return out
 
-    def spec_decode(self, prompt, max_new: int, k: int, min_n: int = 1, max_n: int = 3,
-                    bonus: bool = False, max_model_len: int | None = None):
-        """n-gram speculative greedy decode with exact-match verification.
+    def _pick(self, logits_row, pos: int, sample):
+        """Greedy argmax, or the keyed sample (seed, request, temperature)."""
+        if sample is None:
+            return int(torch.argmax(logits_row))
+        seed, req, temp = sample
+        return sampling_oracle.sample(logits_row.float().numpy(), seed, req, pos, temp)
 
+    def spec_decode(self, prompt, max_new: int, k: int, min_n: int = 1, max_n: int = 3,
+                    bonus: bool = False, max_model_len: int | None = None, sample=None):
+        """n-gram speculative decode with exact-match verification.
+
+        ``sample`` = (seed, request row, temperature) switches the target token
+        to the keyed Gumbel-max sample at each generated position.
         Returns (output tokens, outcome rows [(proposed, accepted, committed, wasted)]).
         """
         seq = list(prompt)
         out, rows = [], []
         # first token comes from the prompt forward (prefill)
-        first = int(torch.argmax(self.logits(seq)[-1]))
+        first = self._pick(self.logits(seq)[-1], len(seq), sample)
         out.append(first)
         seq.append(first)
         while len(out) < max_new:
             remaining = max_new - len(out)
             d = ngram_oracle.propose(seq, min_n, max_n, k, max_model_len)[: min(k, remaining)]
             lg = self.logits(seq + d)
-            y = [int(torch.argmax(lg[len(seq) - 1 + j])) for j in range(len(d) + 1)]
+            y = [self._pick(lg[len(seq) - 1 + j], len(seq) + j, sample) for j in range(len(d) + 1)]
             a = 0
             while a < len(d) and d[a] == y[a]:
                 a += 1

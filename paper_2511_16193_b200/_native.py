@@ -23,6 +23,7 @@ SIGNATURES: dict[str, list] = {
     "sr_version": [],
     "sr_last_error": [],
     "sr_device_sm_count": [],
+    "sr_abi_sizes": [_vp, _i32],
     "sr_keyed_tokens": [_i32, _vp, _vp, _i32, _i64, _i32, _vp, _vp],
     "sr_keyed_uniforms": [_i32, _vp, _vp, _i32, _i32, _vp, _vp],
     "sr_verify_windows": [_i32, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _i32,
@@ -33,6 +34,7 @@ SIGNATURES: dict[str, list] = {
     "sr_paged_attention": [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _i32,
                            _vp, _i32, _vp, _i32, _i32, _vp, ctypes.c_uint64, _vp, _vp],
     "sr_set_attention_split": [_i32],
+    "sr_sample_rows": [_vp, _i32, _i32, _i32, _vp, _vp, ctypes.c_uint32, ctypes.c_float, _vp, _vp],
     "sr_model_workspace_bytes": [_vp],
     "sr_model_create": [_vp, _vp],
     "sr_model_destroy": [_vp],
@@ -52,6 +54,7 @@ _RESTYPES = {"sr_last_error": ctypes.c_char_p, "sr_model_workspace_bytes": ctype
 class SeqInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in
                 ("q_start", "q_len", "request", "ctx_len", "branch", "pad0", "pad1", "pad2")]
+    __slots__ = ()
 
 
 class ModelDesc(ctypes.Structure):
@@ -66,6 +69,7 @@ class ModelDesc(ctypes.Structure):
         (n, ctypes.c_void_p) for n in
         ("embed", "lm_head", "final_norm", "layer_weights", "rope_cos", "rope_sin", "kv_cache",
          "block_table", "window_kv", "workspace")] + [("workspace_bytes", ctypes.c_uint64)]
+    __slots__ = ()
 
 
 class ForwardArgs(ctypes.Structure):
@@ -74,7 +78,9 @@ class ForwardArgs(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in
                 ("num_tokens", "num_seqs", "max_q_len", "max_key", "output", "num_logit_rows")] + [
         (n, ctypes.c_void_p) for n in
-        ("token_ids", "positions", "seqs", "logit_rows", "out", "out_val")]
+        ("token_ids", "positions", "seqs", "logit_rows", "out", "out_val")] + [
+        ("temperature", ctypes.c_float), ("seed", ctypes.c_uint32)]
+    __slots__ = ()  # typos in field names raise instead of silently adding attributes
 
 _lib = None
 

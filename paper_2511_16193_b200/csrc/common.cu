@@ -28,6 +28,13 @@ long long sr_launch_count(void) { return sr::g_launches.load(); }
 
 const char* sr_last_error(void) { return sr::g_last_error; }
 
+int sr_abi_sizes(int64_t* out, int n) {
+  const int64_t sizes[3] = {(int64_t)sizeof(sr_model_desc), (int64_t)sizeof(sr_forward_args),
+                            (int64_t)sizeof(sr_seq_info)};
+  for (int i = 0; i < n && i < 3; ++i) out[i] = sizes[i];
+  return SR_OK;
+}
+
 int sr_device_sm_count(void) {
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;

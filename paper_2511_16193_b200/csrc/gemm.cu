@@ -21,6 +21,7 @@
 // batch, which makes speculative verify and plain decode bit-identical.
 #include "common.cuh"
 #include "gemm.cuh"
+#include "sampling.cuh"
 #include "sm100.cuh"
 
 #include <cudaTypedefs.h>
@@ -121,6 +122,35 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, int row, int c
   }
 }
 
+// Vocabulary argmax over W accumulator columns; with sampling on, each logit
+// is scaled by 1/T and perturbed by its keyed Gumbel noise first (keyed
+// Gumbel-max = exact sample of softmax(logits / T)).  Strict '>' in column
+// order keeps the lowest index on ties.
+template <int W>
+__device__ __forceinline__ void argmax_chunk(const uint32_t* v, int col, int N, int row, int M,
+                                             const SampleArgs& sa, float& best, int& best_idx) {
+  if (sa.inv_temp > 0.0f) {
+    if (row >= M) return;
+    const int rq = sa.req[row], ps = sa.pos[row];
+#pragma unroll
+    for (int i = 0; i < W; i += 4) {
+      float g[4];
+      gumbel4(sa.seed, rq, ps, (col + i) >> 2, g);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float f = __uint_as_float(v[i + t]) * sa.inv_temp + g[t];
+        if (col + i + t < N && f > best) { best = f; best_idx = col + i + t; }
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    const float f = __uint_as_float(v[i]);
+    if (col + i < N && f > best) { best = f; best_idx = col + i; }
+  }
+}
+
 template <int EPI>
 __device__ __forceinline__ void epilogue32(const uint32_t (&v)[32], int row, int col, int M, int N, void* C,
                                            int ldc, const float* bias) {
@@ -131,7 +161,7 @@ template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     int M, int N, int K, void* C, int ldc, const float* __restrict__ bias,
-                    int32_t* __restrict__ aux) {
+                    int32_t* __restrict__ aux, SampleArgs sa) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -232,12 +262,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         sm100::tmem_ld_wait();
         const int col = n_blk * BN + c * 32;
         if constexpr (EPI == kEpiArgmax) {
-          // strict '>' in column order keeps the lowest index on ties
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float f = __uint_as_float(v[i]);
-            if (col + i < N && f > best) { best = f; best_idx = col + i; }
-          }
+          argmax_chunk<32>(v, col, N, row, M, sa, best, best_idx);
         } else {
           if (col < N) epilogue32<EPI>(v, row, col, M, N, C, ldc, bias);
         }
@@ -284,7 +309,7 @@ template <int BN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  int M, int N, int K, void* C, int ldc, const float* __restrict__ bias,
-                 int32_t* __restrict__ aux) {
+                 int32_t* __restrict__ aux, SampleArgs sa) {
   using Cfg = PairCfg<BN>;
   constexpr int S = Cfg::kStages;
   constexpr int CW = Cfg::kChunk;
@@ -434,11 +459,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         sm100::tmem_ld_wait();
         const int col = n_blk * BN + c * CW;
         if constexpr (EPI == kEpiArgmax) {
-#pragma unroll
-          for (int i = 0; i < CW; ++i) {
-            const float f = __uint_as_float(v[i]);
-            if (col + i < N && f > best) { best = f; best_idx = col + i; }
-          }
+          argmax_chunk<CW>(v, col, N, row, M, sa, best, best_idx);
         } else {
           if (col < N) epilogue_chunk<EPI, CW>(v, row, col, M, N, C, ldc, bias);
         }
@@ -499,7 +520,7 @@ int launch_typed(const GemmPlan& p, int M, cudaStream_t stream) {
   }
   const int tiles = ((M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, kThreads, Cfg::kSmem, stream>>>(p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux);
+  kern<<<grid, kThreads, Cfg::kSmem, stream>>>(p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux, p.sample);
   return check_launch("gemm_tcgen05_kernel");
 }
 
@@ -527,7 +548,8 @@ int launch_pair_typed(const GemmPlan& p, int M, cudaStream_t stream) {
   }
   const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * ((p.N + BN - 1) / BN);
   const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-  kern<<<2 * pairs, kThreads, Cfg::kSmem, stream>>>(p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux);
+  kern<<<2 * pairs, kThreads, Cfg::kSmem, stream>>>(p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux,
+                                                    p.sample);
   return check_launch("gemm_pair_kernel");
 }
 
@@ -628,6 +650,7 @@ int gemm_bf16_plan(GemmPlan* p, int M, int N, int K, const __nv_bfloat16* A, int
   p->M = M; p->N = N; p->K = K; p->bn = bn; p->epi = epi; p->c = C; p->ldc = ldc; p->bias = bias;
   p->aux = aux;
   p->pair = pair;
+  p->sample = SampleArgs{nullptr, nullptr, 0u, 0.0f};
   const int mrows = M > 0 ? M : 1;
   int rc = make_tmap_bf16(&p->a, A, (uint64_t)K, (uint64_t)mrows, (uint64_t)lda * 2, kBK, kBM);
   if (rc) return rc;

@@ -4,6 +4,8 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 
+#include "sampling.cuh"
+
 namespace sr {
 
 enum GemmEpilogue : int {
@@ -28,6 +30,7 @@ struct GemmPlan {
   int ldc;
   const float* bias;
   int32_t* aux;
+  SampleArgs sample;  // argmax epilogue: keyed Gumbel sampling when inv_temp > 0
 };
 
 // Build a plan (tensor maps) once; launch many times (graph-capturable).

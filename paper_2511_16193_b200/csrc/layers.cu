@@ -1,6 +1,7 @@
 // K6 helpers of the verify forward; see layers.cuh.
 #include "common.cuh"
 #include "layers.cuh"
+#include "sampling.cuh"
 
 namespace sr {
 
@@ -241,7 +242,85 @@ __global__ void argmax_rows_kernel(const float* __restrict__ logits, int V, int 
   }
 }
 
+// Keyed Gumbel-max sample of fp32 logit rows (same noise as the fused
+// lm_head epilogue): one CTA per row.
+__global__ void sample_rows_kernel(const float* __restrict__ logits, int V, int ld,
+                                   const int32_t* __restrict__ req, const int32_t* __restrict__ pos,
+                                   uint32_t seed, float inv_temp, int32_t* __restrict__ ids,
+                                   float* __restrict__ vals) {
+  const int row = blockIdx.x;
+  const float* r = logits + (int64_t)row * ld;
+  const int rq = req[row], ps = pos[row];
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int b = threadIdx.x; b * 4 < V; b += blockDim.x) {
+    float g[4];
+    gumbel4(seed, rq, ps, b, g);
+    for (int t = 0; t < 4 && 4 * b + t < V; ++t) {
+      const float v = r[4 * b + t] * inv_temp + g[t];
+      if (better(v, 4 * b + t, bv, bi)) { bv = v; bi = 4 * b + t; }
+    }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float v = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int i = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (better(v, i, bv, bi)) { bv = v; bi = i; }
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { sv[w] = bv; si[w] = bi; }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    bv = lane < nw ? sv[lane] : -INFINITY;
+    bi = lane < nw ? si[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float v = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int i = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(v, i, bv, bi)) { bv = v; bi = i; }
+    }
+    if (lane == 0) {
+      ids[row] = bi;
+      if (vals) vals[row] = bv;
+    }
+  }
+}
+
+// Sampling key of each lm_head row: the request of the sequence holding the
+// token row (sequences sorted by q_start) and the position being generated.
+__global__ void row_keys_kernel(const SeqInfo* __restrict__ seqs, int S, const int32_t* __restrict__ positions,
+                                const int32_t* __restrict__ logit_rows, int R, int32_t* __restrict__ key_req,
+                                int32_t* __restrict__ key_pos) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= R) return;
+  const int t = logit_rows ? logit_rows[i] : i;
+  int lo = 0, hi = S - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (seqs[mid].q_start <= t) lo = mid; else hi = mid - 1;
+  }
+  key_req[i] = seqs[lo].request;
+  key_pos[i] = positions[t] + 1;
+}
+
 }  // namespace
+
+int sample_rows(const float* logits, int M, int V, int ld, const int32_t* req, const int32_t* pos, uint32_t seed,
+                float inv_temp, int32_t* ids, float* vals, cudaStream_t s) {
+  if (M == 0) return SR_OK;
+  sample_rows_kernel<<<M, 512, 0, s>>>(logits, V, ld, req, pos, seed, inv_temp, ids, vals);
+  return check_launch("sample_rows_kernel");
+}
+
+int row_keys(const SeqInfo* seqs, int S, const int32_t* positions, const int32_t* logit_rows, int R,
+             int32_t* key_req, int32_t* key_pos, cudaStream_t s) {
+  if (R == 0 || S == 0) return SR_OK;
+  row_keys_kernel<<<ceil_div(R, 256), 256, 0, s>>>(seqs, S, positions, logit_rows, R, key_req, key_pos);
+  return check_launch("row_keys_kernel");
+}
 
 template <typename T>
 int embed_rows(const T* table, const int32_t* ids, int M, int H, float* x, cudaStream_t s) {

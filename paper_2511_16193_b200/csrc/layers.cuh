@@ -65,6 +65,14 @@ int rope_scatter(const T* qkv, const int32_t* positions, const SeqInfo* seqs, in
 int argmax_reduce(const float* part_val, const int32_t* part_idx, int M, int tiles,
                   int32_t* out_ids, float* out_val, cudaStream_t s);
 
+// Keyed Gumbel-max sample of fp32 logit rows (sampling.cuh); req/pos per row.
+int sample_rows(const float* logits, int M, int V, int ld, const int32_t* req, const int32_t* pos, uint32_t seed,
+                float inv_temp, int32_t* ids, float* vals, cudaStream_t s);
+
+// (request, generated position) of each lm_head row, from sorted SeqInfo.
+int row_keys(const SeqInfo* seqs, int S, const int32_t* positions, const int32_t* logit_rows, int R,
+             int32_t* key_req, int32_t* key_pos, cudaStream_t s);
+
 // Full-row argmax over fp32 logits [M, V] (lowest index on ties).
 int argmax_rows(const float* logits, int M, int V, int ld, int32_t* out_ids, float* out_val,
                 cudaStream_t s);

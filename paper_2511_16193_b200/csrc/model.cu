@@ -125,6 +125,8 @@ struct Model {
   float* part_val;
   int32_t* part_idx;
   float* attn_part;
+  int32_t* key_req;    // sampling keys of the lm_head rows
+  int32_t* key_pos;
   // plans (bf16)
   std::vector<GemmPlan> p_qkv, p_o, p_gu, p_down;
   GemmPlan p_lm_argmax, p_lm_logits;
@@ -150,9 +152,12 @@ static size_t carve(const sr_model_desc& d, Model* m, char* base) {
   float* pv = c.take<float>((size_t)T * lm_tiles);
   int32_t* pi = c.take<int32_t>((size_t)T * lm_tiles);
   float* ap = c.take<float>(d.dtype == 1 ? pf : 0);
+  int32_t* kr = c.take<int32_t>((size_t)T);
+  int32_t* kp = c.take<int32_t>((size_t)T);
   if (m != nullptr) {
     m->x = x; m->h = h; m->qkv = qkv; m->q = q; m->attn = attn; m->act = act; m->h_sel = h_sel;
     m->logits = logits; m->part_val = pv; m->part_idx = pi; m->attn_part = ap;
+    m->key_req = kr; m->key_pos = kp;
     m->esize = esize; m->qkv_width = qkv_w; m->lm_tiles = lm_tiles;
     m->partial_floats = d.dtype == 1 ? pf : 0;
   }
@@ -263,11 +268,16 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
   SR_REQUIRE(a->output == 0 || (a->output == 1 && m->logits != nullptr && R <= d.logits_capacity) ||
                  a->output == 2,
              "logits output needs logits_capacity >= rows");
+  SR_REQUIRE(a->output != 2 || a->temperature > 0.0f, "sampling needs temperature > 0");
+
   if (M == 0) return SR_OK;
   const auto* seqs = reinterpret_cast<const sr::SeqInfo*>(a->seqs);
+  const sr::SampleArgs sample{m->key_req, m->key_pos, a->seed,
+                              a->output == 2 ? 1.0f / a->temperature : 0.0f};
   const int H = d.hidden, I = d.intermediate, nqd = d.q_heads * d.head_dim;
   int rc;
 #define SR_TRY(x) do { rc = (x); if (rc) return rc; } while (0)
+  if (a->output == 2) SR_TRY(sr::row_keys(seqs, S, a->positions, a->logit_rows, R, m->key_req, m->key_pos, st));
   if (d.dtype == 1) {
     using bf = __nv_bfloat16;
     SR_TRY(sr::embed_rows<bf>((const bf*)d.embed, a->token_ids, M, H, m->x, st));
@@ -319,6 +329,7 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
                                       cudaMemcpyDeviceToDevice, st));
     } else {
       m->prof.begin(sr::kProfLmHead, st);
+      m->p_lm_argmax.sample = sample;
       SR_TRY(sr::gemm_bf16_launch(m->p_lm_argmax, st, R));
       m->prof.end(st);
       m->prof.begin(sr::kProfOther, st);
@@ -356,7 +367,10 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
                "fp32 path needs logits_capacity >= rows for argmax");
     SR_TRY(sr::gemm_f32(R, d.vocab, H, (const float*)m->h_sel, H, (const float*)d.lm_head, H, logits, d.vocab,
                         sr::kEpiStoreF32, nullptr, st));
-    if (a->output != 1) SR_TRY(sr::argmax_rows(logits, R, d.vocab, d.vocab, (int32_t*)a->out, a->out_val, st));
+    if (a->output == 0) SR_TRY(sr::argmax_rows(logits, R, d.vocab, d.vocab, (int32_t*)a->out, a->out_val, st));
+    if (a->output == 2)
+      SR_TRY(sr::sample_rows(logits, R, d.vocab, d.vocab, m->key_req, m->key_pos, a->seed, sample.inv_temp,
+                             (int32_t*)a->out, a->out_val, st));
   }
 #undef SR_TRY
   return SR_OK;
@@ -383,6 +397,16 @@ int sr_model_profile(void* handle, int enable, float* ms_out, int32_t* count_out
   P.next = 0;
   P.on = enable != 0;
   return SR_OK;
+}
+
+int sr_sample_rows(const float* logits, int rows, int vocab, int ld, const int32_t* req, const int32_t* pos,
+                   uint32_t seed, float temperature, int32_t* ids, sr_stream_t stream) {
+  SR_REQUIRE(rows >= 0 && vocab > 0 && ld >= vocab, "bad logits shape");
+  SR_REQUIRE(temperature > 0.0f, "temperature must be > 0");
+  if (rows == 0) return SR_OK;
+  SR_REQUIRE(logits && req && pos && ids, "null pointer");
+  return sr::sample_rows(logits, rows, vocab, ld, req, pos, seed, 1.0f / temperature, ids, nullptr,
+                         (cudaStream_t)stream);
 }
 
 int sr_kv_commit(void* handle, int num_requests, int num_drafters, const void* seqs, const int32_t* outcome,

@@ -75,7 +75,8 @@ class RolloutEngine:
     """Batch state (token buffer, lengths, budgets) + per-step device work."""
 
     def __init__(self, target: DeviceModel, prompts: list[np.ndarray], max_new: list[int], *, k: int = 4,
-                 drafters: tuple = (NgramDrafter(),), bonus_token: bool = False, history: int = 0):
+                 drafters: tuple = (NgramDrafter(),), bonus_token: bool = False, history: int = 0,
+                 temperature: float = 0.0, seed: int = 0):
         if not prompts:
             raise ConfigError("empty batch")
         if len(prompts) != len(max_new):
@@ -88,6 +89,10 @@ class RolloutEngine:
         self.N = len(self.drafters)
         self.B = len(prompts)
         self.bonus = 1 if bonus_token else 0
+        # T = 0: greedy; T > 0: keyed Gumbel-max sampling (exact match still
+        # verifies because the target's draw is keyed by (seed, request, position))
+        self.temperature, self.seed = float(temperature), int(seed)
+        self._out_mode = 2 if self.temperature > 0 else 0
         if self.N > 1 and target.branches < self.B * (self.N - 1):
             raise ConfigError("target model needs max_branches >= B*(N-1) for Best-of-N")
         if self.B * self.N > target.max_seqs or self.B * self.N * (k + 1) > target.max_tokens:
@@ -149,7 +154,8 @@ class RolloutEngine:
             lr = torch.tensor(last, dtype=torch.int32, device=self.dev)
             out = torch.empty(len(rows), dtype=torch.int32, device=self.dev)
             m.forward(ids, pos, seqs, num_seqs=len(rows), max_q_len=max_q, max_key=max_q - 1,
-                      out=out, logit_rows=lr)
+                      out=out, logit_rows=lr, output=self._out_mode, temperature=self.temperature,
+                      seed=self.seed)
             for j, r in enumerate(rows):
                 b = r[2]
                 self.tokens[b, self.prompt_lens[b]] = out[j]
@@ -181,7 +187,8 @@ class RolloutEngine:
             self.token_ids.data_ptr(), self.positions.data_ptr(), self.seqs.data_ptr(), st),
             "sr_build_verify_batch")
         self.m.forward(self.token_ids, self.positions, self.seqs, num_seqs=self.B * self.N,
-                       max_q_len=self.k + 1, max_key=self.max_key, out=self.target_ids)
+                       max_q_len=self.k + 1, max_key=self.max_key, out=self.target_ids,
+                       output=self._out_mode, temperature=self.temperature, seed=self.seed)
         out = self.history[slot]
         _native.check(lib.sr_accept_commit(
             self.B, self.N, self.seqs.data_ptr(), self.token_ids.data_ptr(), self.target_ids.data_ptr(),

@@ -204,8 +204,10 @@ class DeviceModel:
                 pass
 
     def forward(self, token_ids, positions, seqs, *, num_seqs: int, max_q_len: int, max_key: int,
-                out, output: int = 0, logit_rows=None, out_val=None, stream=None) -> None:
-        """Enqueue one forward (``output`` 0 = argmax ids, 1 = fp32 logits)."""
+                out, output: int = 0, logit_rows=None, out_val=None, stream=None,
+                temperature: float = 0.0, seed: int = 0) -> None:
+        """Enqueue one forward (``output`` 0 = argmax ids, 1 = fp32 logits,
+        2 = keyed Gumbel-max sample at ``temperature``)."""
         a = _native.ForwardArgs()
         a.num_tokens = token_ids.numel()
         a.num_seqs = num_seqs
@@ -215,6 +217,7 @@ class DeviceModel:
         a.logit_rows = logit_rows.data_ptr() if logit_rows is not None else None
         a.out = out.data_ptr()
         a.out_val = out_val.data_ptr() if out_val is not None else None
+        a.temperature, a.seed = float(temperature), int(seed) & 0xFFFFFFFF
         _native.check(self.lib.sr_model_forward(self.handle, ctypes.byref(a),
                                                 _native.stream_handle(stream)), "sr_model_forward")
 

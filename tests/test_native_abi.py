@@ -48,3 +48,15 @@ def test_config_errors_need_no_gpu():
     assert b"min_n" in lib.sr_last_error()
     assert lib.sr_verify_windows(-1, None, 0, 1, 1, None, None, None, None, 0,
                                  None, None, None, None) == 2
+
+
+def test_struct_mirrors_match_c_layout():
+    import ctypes
+
+    from paper_2511_16193_b200 import _native
+
+    lib = _native.load()
+    out = (ctypes.c_int64 * 3)()
+    assert lib.sr_abi_sizes(out, 3) == 0
+    assert list(out) == [ctypes.sizeof(_native.ModelDesc), ctypes.sizeof(_native.ForwardArgs),
+                         ctypes.sizeof(_native.SeqInfo)]
