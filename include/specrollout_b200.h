@@ -265,6 +265,19 @@ int sr_synthetic_draft(int num_requests, int k, const int32_t* truth, int64_t tr
                        const double* accept_p, const int32_t* gen_len, int vocab, int32_t* drafts,
                        int32_t* ndraft, sr_stream_t stream);
 
+/* K5 small-model drafter batches (drafting methods `draft-0.5b`/`draft-1.5b`,
+ * scenarios.py:25-29, priced per token at sim.py:883-892).  Rows [b*(k+2),
+ * +k+2) belong to request b.  step 0: catch-up of the committed tokens the
+ * drafter has not cached, [dkv_len, seq_len) (advances dkv_len), logits at
+ * the last one; step j in [1, k): decode the previous draft; step k: file the
+ * last output and write ndraft.  prev_out [B] is the previous forward's
+ * output and becomes draft (step-1).  drafts [B, k], ndraft [B]. */
+int sr_draft_model_batch(int num_requests, int k, int step, const int32_t* tokens, int64_t tok_stride,
+                         const int32_t* seq_len, const int32_t* gen_len, const int32_t* max_new,
+                         int32_t* dkv_len, const int32_t* prev_out, int32_t* drafts, int32_t* ndraft,
+                         int32_t* token_ids, int32_t* positions, void* seqs, int32_t* logit_rows,
+                         sr_stream_t stream);
+
 /* Next verify batch from device state: for drafter n of request b, rows
  * [(b*N+n)*(k+1), +nd+1) = last committed token then the drafts.  drafts
  * [N, B, k] / ndraft [N, B] are drafter-major (each drafter kernel writes its

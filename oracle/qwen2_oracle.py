@@ -122,10 +122,8 @@ class Qwen2Oracle:
         """
         seq = list(prompt)
         out, rows = [], []
-        # first token comes from the prompt forward (prefill)
-        first = self._pick(self.logits(seq)[-1], len(seq), sample)
-        out.append(first)
-        seq.append(first)
+        # every generated token comes out of a window (the first window
+        # starts from the last prompt token), as in sim.py:834-928
         while len(out) < max_new:
             remaining = max_new - len(out)
             d = ngram_oracle.propose(seq, min_n, max_n, k, max_model_len)[: min(k, remaining)]

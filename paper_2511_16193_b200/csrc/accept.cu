@@ -169,6 +169,56 @@ __global__ void synthetic_draft_kernel(int B, int k, const int32_t* __restrict__
   ndraft[b] = nd;
 }
 
+// Draft-model batches (K5).  step 0 = catch-up: the committed tokens the
+// drafter has not cached yet, [dkv_len, seq_len), with logits taken at the
+// last one; step j >= 1 = one decode step on the previous draft token.
+// The output of step j-1 (prev_out [B]) is filed as draft j-1.
+__global__ void draft_batch_kernel(int B, int k, int step, const int32_t* __restrict__ tokens, int64_t tok_stride,
+                                   const int32_t* __restrict__ seq_len, const int32_t* __restrict__ gen_len,
+                                   const int32_t* __restrict__ max_new, int32_t* __restrict__ dkv_len,
+                                   const int32_t* __restrict__ prev_out, int32_t* __restrict__ drafts,
+                                   int32_t* __restrict__ ndraft, int32_t* __restrict__ token_ids,
+                                   int32_t* __restrict__ positions, SeqInfo* __restrict__ seqs,
+                                   int32_t* __restrict__ logit_rows) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int rows = k + 2;
+  const int L = seq_len[b];
+  const int want = max(0, min(k, max_new[b] - gen_len[b]));
+  if (step >= 1 && step - 1 < k) drafts[(int64_t)b * k + step - 1] = (step - 1 < want) ? prev_out[b] : -1;
+  if (step == k) {  // collect only
+    ndraft[b] = want;
+    return;
+  }
+  SeqInfo sq;
+  sq.q_start = b * rows;
+  sq.request = b;
+  sq.branch = -1;
+  sq.pad0 = sq.pad1 = sq.pad2 = 0;
+  if (step == 0) {
+    const int d0 = dkv_len[b];
+    const int q = want > 0 ? min(L - d0, rows) : 0;
+    const int first = L - q;  // clamp: never more than `rows` tokens of catch-up
+    sq.q_len = q;
+    sq.ctx_len = first;
+    for (int j = 0; j < rows; ++j) {
+      const int p = first + j;
+      token_ids[b * rows + j] = (j < q) ? tokens[(int64_t)b * tok_stride + p] : 0;
+      positions[b * rows + j] = (j < q) ? p : 0;
+    }
+    logit_rows[b] = b * rows + max(q - 1, 0);
+    if (q > 0) dkv_len[b] = L;
+  } else {
+    const int p = L - 1 + step;
+    sq.q_len = step < want ? 1 : 0;
+    sq.ctx_len = p;
+    token_ids[b * rows] = prev_out[b];
+    positions[b * rows] = p;
+    logit_rows[b] = b * rows;
+  }
+  seqs[b] = sq;
+}
+
 }  // namespace
 
 int kv_commit(int B, int N, const SeqInfo* seqs, const int32_t* outcome, const int32_t* bon,
@@ -211,6 +261,22 @@ extern "C" int sr_synthetic_draft(int num_requests, int k, const int32_t* truth,
       num_requests, k, truth, truth_stride, truth_len, uniforms, u_stride, accept_p, gen_len, vocab, drafts,
       ndraft);
   return sr::check_launch("synthetic_draft_kernel");
+}
+
+extern "C" int sr_draft_model_batch(int num_requests, int k, int step, const int32_t* tokens, int64_t tok_stride,
+                                    const int32_t* seq_len, const int32_t* gen_len, const int32_t* max_new,
+                                    int32_t* dkv_len, const int32_t* prev_out, int32_t* drafts, int32_t* ndraft,
+                                    int32_t* token_ids, int32_t* positions, void* seqs, int32_t* logit_rows,
+                                    sr_stream_t stream) {
+  SR_REQUIRE(num_requests >= 0 && k >= 1 && step >= 0 && step <= k, "bad draft step");
+  if (num_requests == 0) return SR_OK;
+  SR_REQUIRE(tokens && seq_len && gen_len && max_new && dkv_len && drafts && ndraft && token_ids && positions &&
+                 seqs && logit_rows && (step == 0 || prev_out),
+             "null pointer");
+  sr::draft_batch_kernel<<<sr::ceil_div(num_requests, 128), 128, 0, (cudaStream_t)stream>>>(
+      num_requests, k, step, tokens, tok_stride, seq_len, gen_len, max_new, dkv_len, prev_out, drafts, ndraft,
+      token_ids, positions, reinterpret_cast<sr::SeqInfo*>(seqs), logit_rows);
+  return sr::check_launch("draft_batch_kernel");
 }
 
 extern "C" int sr_build_verify_batch(int num_requests, int num_drafters, int k, const int32_t* tokens,

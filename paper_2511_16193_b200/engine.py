@@ -71,6 +71,73 @@ class SyntheticDrafter:
         self.method = method
 
 
+class ModelDrafter:
+    """Small-model drafter (K5; reference methods ``draft-0.5b``/``draft-1.5b``,
+    ``scenarios.py:25-29``): k greedy decode steps of its own decoder per
+    window, with its own paged KV cache.  Each window first catches the
+    drafter's cache up on the tokens committed since the previous window
+    (``sr_draft_model_batch`` step 0), then decodes k-1 more tokens."""
+
+    name = "model"
+
+    def __init__(self, model: DeviceModel, name: str = "draft-0.5b"):
+        self.m = model
+        self.name = name
+        self.eng = None
+
+    def attach(self, eng: "RolloutEngine") -> None:
+        B, k, dev = eng.B, eng.k, eng.dev
+        if self.m.max_tokens < B * (k + 2) or self.m.max_seqs < B or self.m.max_len < eng.max_key + 2:
+            raise ConfigError("drafter model capacity too small for the batch")
+        self.eng = eng
+        self.dkv_len = torch.tensor([L - 1 for L in eng.prompt_lens], dtype=torch.int32, device=dev)
+        self.token_ids = torch.zeros(B * (k + 2), dtype=torch.int32, device=dev)
+        self.positions = torch.zeros(B * (k + 2), dtype=torch.int32, device=dev)
+        self.seqs = torch.zeros((B, 8), dtype=torch.int32, device=dev)
+        self.logit_rows = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.out = torch.zeros(B, dtype=torch.int32, device=dev)
+        prefill_model(self.m, eng.tokens, [L - 1 for L in eng.prompt_lens])
+
+    def enqueue(self, drafts, ndraft) -> None:
+        e, lib, st = self.eng, self.eng.lib, _native.stream_handle()
+        for step in range(e.k + 1):
+            _native.check(lib.sr_draft_model_batch(
+                e.B, e.k, step, e.tokens.data_ptr(), e.stride, e.seq_len.data_ptr(), e.gen_len.data_ptr(),
+                e.max_new.data_ptr(), self.dkv_len.data_ptr(), self.out.data_ptr(), drafts.data_ptr(),
+                ndraft.data_ptr(), self.token_ids.data_ptr(), self.positions.data_ptr(), self.seqs.data_ptr(),
+                self.logit_rows.data_ptr(), st), "sr_draft_model_batch")
+            if step < e.k:
+                self.m.forward(self.token_ids, self.positions, self.seqs, num_seqs=e.B,
+                               max_q_len=e.k + 2, max_key=e.max_key, out=self.out,
+                               logit_rows=self.logit_rows)
+
+
+def prefill_model(m: DeviceModel, tokens, lens) -> None:
+    """Chunked prompt forward writing KV for positions [0, lens[b]) of every
+    request b into ``m``'s paged cache (the logits are not needed)."""
+    dev = tokens.device
+    order = [b for b in range(len(lens)) if lens[b] > 0]
+    i = 0
+    while i < len(order):
+        rows, tok_rows, pos_rows = [], [], []
+        start, max_q = 0, 0
+        while i < len(order):
+            b = order[i]
+            L = lens[b]
+            if rows and (start + L > m.max_tokens or len(rows) + 1 > m.max_prefill_seqs(max(max_q, L))):
+                break
+            rows.append((start, L, b, 0, -1))
+            tok_rows.append(tokens[b, :L])
+            pos_rows.append(torch.arange(L, dtype=torch.int32, device=dev))
+            start += L
+            max_q = max(max_q, L)
+            i += 1
+        lr = torch.tensor([r[0] + r[1] - 1 for r in rows], dtype=torch.int32, device=dev)
+        out = torch.empty(len(rows), dtype=torch.int32, device=dev)
+        m.forward(torch.cat(tok_rows), torch.cat(pos_rows), seq_table(rows, dev), num_seqs=len(rows),
+                  max_q_len=max_q, max_key=max_q - 1, out=out, logit_rows=lr)
+
+
 class RolloutEngine:
     """Batch state (token buffer, lengths, budgets) + per-step device work."""
 
@@ -128,39 +195,15 @@ class RolloutEngine:
     # -- prefill -------------------------------------------------------------
 
     def prefill(self) -> None:
-        """Prompt forward (KV straight into the paged cache) + first token."""
-        m = self.m
-        order = list(range(self.B))
-        i = 0
-        while i < len(order):
-            rows, tok_rows, pos_rows, last = [], [], [], []
-            start = 0
-            max_q = 0
-            while i < len(order):
-                b = order[i]
-                L = self.prompt_lens[b]
-                if rows and (start + L > m.max_tokens or len(rows) + 1 > m.max_prefill_seqs(max(max_q, L))):
-                    break
-                rows.append((start, L, b, 0, -1))
-                tok_rows.append(self.tokens[b, :L])
-                pos_rows.append(torch.arange(L, dtype=torch.int32, device=self.dev))
-                last.append(start + L - 1)
-                start += L
-                max_q = max(max_q, L)
-                i += 1
-            ids = torch.cat(tok_rows)
-            pos = torch.cat(pos_rows)
-            seqs = seq_table(rows, self.dev)
-            lr = torch.tensor(last, dtype=torch.int32, device=self.dev)
-            out = torch.empty(len(rows), dtype=torch.int32, device=self.dev)
-            m.forward(ids, pos, seqs, num_seqs=len(rows), max_q_len=max_q, max_key=max_q - 1,
-                      out=out, logit_rows=lr, output=self._out_mode, temperature=self.temperature,
-                      seed=self.seed)
-            for j, r in enumerate(rows):
-                b = r[2]
-                self.tokens[b, self.prompt_lens[b]] = out[j]
-        self.seq_len += 1
-        self.gen_len += 1
+        """Cache the KV of every prompt token but the last.  The last prompt
+        token is the "last committed token" the first window starts from, so
+        generated position 0 comes out of the first verify window -- the
+        reference's round structure, where every output token is produced by
+        a window (``sim.py:834-928``).  Model drafters prefill their caches."""
+        prefill_model(self.m, self.tokens, [L - 1 for L in self.prompt_lens])
+        for d in self.drafters:
+            if isinstance(d, ModelDrafter):
+                d.attach(self)
 
     # -- one speculation window ------------------------------------------------
 
@@ -169,6 +212,9 @@ class RolloutEngine:
         drafts_ptr, nd_ptr = None, None
         if self.k > 0:
             for n, d in enumerate(self.drafters):
+                if isinstance(d, ModelDrafter):
+                    d.enqueue(self.drafts[n], self.ndraft[n])
+                    continue
                 if isinstance(d, SyntheticDrafter):
                     _native.check(lib.sr_synthetic_draft(
                         self.B, self.k, d.truth.data_ptr(), d.stride, d.truth_len.data_ptr(),

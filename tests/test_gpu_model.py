@@ -255,7 +255,7 @@ def test_synthetic_drafter_follows_reference_accept_law():
     for b, r in enumerate(reqs):
         u = rollout_oracle.accept_uniforms(0, r.id, method, max_new[b] + 8)
         p = r.latent_accept[method]
-        g = 1
+        g = 0
         for step in range(steps):
             n, a, c, _ = rows[step, b]
             if n == 0 and c == 0:
@@ -266,3 +266,70 @@ def test_synthetic_drafter_follows_reference_accept_law():
             assert a == exp_a, (b, step, g)
             g += c
         assert g == max_new[b]
+
+
+def test_model_drafter_exactness_and_self_drafting():
+    """K5 small-model drafter: a different drafter keeps outputs identical to
+    plain decode; a drafter that *is* the target is accepted every time."""
+    from paper_2511_16193_b200.engine import ModelDrafter, RolloutEngine
+    from paper_2511_16193_b200.model import DeviceModel, init_weights, shape
+
+    B, k = 4, 4
+    s, w, m = make("tiny", "bf16", B=B)
+    prompts = prompts_for(s.vocab, B, 14)
+    max_new = [40, 21, 33, 9]
+    plain, _ = run_engine(m, prompts, max_new, k=0)
+
+    def drafter(seed):
+        d = DeviceModel(s, init_weights(s, seed=seed), dtype="bf16", max_requests=B, max_len=512,
+                        max_tokens=512, max_seqs=B * 3)
+        return ModelDrafter(d)
+
+    other = RolloutEngine(m, prompts, max_new, k=k, drafters=(drafter(7),), history=256)
+    other.prefill()
+    other.run()
+    assert other.outputs() == plain.outputs()
+
+    selfd = RolloutEngine(m, prompts, max_new, k=k, drafters=(drafter(0),), history=256)
+    selfd.prefill()
+    steps = selfd.run()
+    assert selfd.outputs() == plain.outputs()
+    rows = selfd.outcome_rows(steps).reshape(-1, 4)
+    live = rows[rows[:, 0] > 0]
+    assert len(live) and (live[:, 1] == live[:, 0]).all()   # every draft accepted
+
+
+def test_engine_outcomes_match_reference_coupled_golden():
+    """Model-mode rollout (real tiny target, reference-acceptance drafter,
+    w = k = 4, bonus off) reproduces the reference simulator's per-request
+    VerificationOutcome stream (proposed, accepted, committed, wasted) of the
+    config-1 golden run (tests/golden/sim_runs.json, c1-coupled-ngram-w4)."""
+    from conftest import golden
+    from paper_2511_16193_b200 import scenarios
+    from paper_2511_16193_b200.engine import RolloutEngine, SyntheticDrafter
+    from paper_2511_16193_b200.model import DeviceModel, init_weights, shape
+    from paper_2511_16193_b200.streams import stream
+    from paper_2511_16193_b200.workload import gen_trace
+
+    rec = next(r for r in golden("sim_runs.json") if r["name"] == "c1-coupled-ngram-w4")
+    trace = gen_trace(scenarios.default_trace_spec(batch=8, seed=0))
+    s = shape("tiny")
+    prompts = [stream(0, r.id, "prompt").integers(0, s.vocab, size=r.prompt_len).astype(np.int32) for r in trace]
+    lens = [r.true_len for r in trace]
+    max_len = max(len(p) + L for p, L in zip(prompts, lens)) + 16
+    m = DeviceModel(s, init_weights(s, seed=0), dtype="bf16", max_requests=8, max_len=max_len,
+                    max_tokens=2048, max_seqs=24)
+    plain = RolloutEngine(m, prompts, lens, k=0, history=1)
+    plain.prefill()
+    plain.run()
+    truth = plain.outputs()
+    eng = RolloutEngine(m, prompts, lens, k=4, drafters=(SyntheticDrafter(truth, trace, "ngram", 0),),
+                        bonus_token=False, history=max(lens) + 1)
+    eng.prefill()
+    steps = eng.run()
+    assert eng.outputs() == truth
+    rows = eng.outcome_rows(steps)
+    for b, r in enumerate(trace):
+        got = [tuple(int(x) for x in row) for row in rows[:, b, :] if row[0] or row[2]]
+        exp = [tuple(o[5:9]) for o in rec["outcomes"] if o[0] == r.id]
+        assert got == exp, f"request {r.id}"
