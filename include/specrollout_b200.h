@@ -281,7 +281,8 @@ int sr_draft_model_batch(int num_requests, int k, int step, const int32_t* token
 /* Next verify batch from device state: for drafter n of request b, rows
  * [(b*N+n)*(k+1), +nd+1) = last committed token then the drafts.  drafts
  * [N, B, k] / ndraft [N, B] are drafter-major (each drafter kernel writes its
- * own [B, k] block); both NULL = plain decode. */
+ * own [B, k] block); both NULL = plain decode; ndraft < 0 = the request has
+ * no window this round (decoupled gap round, sim.py:1076-1080). */
 int sr_build_verify_batch(int num_requests, int num_drafters, int k, const int32_t* tokens,
                           int64_t tok_stride, const int32_t* seq_len, const int32_t* gen_len,
                           const int32_t* max_new, const int32_t* drafts, const int32_t* ndraft,

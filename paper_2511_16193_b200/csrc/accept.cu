@@ -119,13 +119,15 @@ __global__ void build_verify_kernel(int B, int N, int k, const int32_t* __restri
   const int remaining = max_new[b] - gen_len[b];
   const int L = seq_len[b];
   int nd = 0;
-  if (remaining > 0) {
+  bool active = remaining > 0;
+  if (active) {
     nd = drafts != nullptr ? ndraft[n * B + b] : 0;
+    active = nd >= 0;  // ndraft < 0: no window this round (decoupled gap round)
     nd = max(0, min(nd, min(k, remaining)));
   }
   SeqInfo sq;
   sq.q_start = s * (k + 1);
-  sq.q_len = remaining > 0 ? nd + 1 : 0;
+  sq.q_len = active ? nd + 1 : 0;
   sq.request = b;
   sq.ctx_len = L - 1;
   sq.branch = n == 0 ? -1 : b * (N - 1) + (n - 1);

@@ -51,7 +51,8 @@ class SyntheticDrafter:
 
     name = "synthetic"
 
-    def __init__(self, truth: list[list[int]], requests, method: str, seed: int, device="cuda"):
+    def __init__(self, truth: list[list[int]], requests, method: str, seed: int, device="cuda",
+                 vocab: int = 0):
         from .verify import CHUNK, entropy_words, keyed_fill
 
         B = len(truth)
@@ -69,6 +70,7 @@ class SyntheticDrafter:
         self.p = torch.tensor([r.latent_accept[method] for r in requests], dtype=torch.float64,
                               device=device)
         self.method = method
+        self.vocab = vocab
 
 
 class ModelDrafter:
@@ -219,7 +221,7 @@ class RolloutEngine:
                     _native.check(lib.sr_synthetic_draft(
                         self.B, self.k, d.truth.data_ptr(), d.stride, d.truth_len.data_ptr(),
                         d.uniforms.data_ptr(), d.stride, d.p.data_ptr(), self.gen_len.data_ptr(),
-                        self.m.s.vocab, self.drafts[n].data_ptr(), self.ndraft[n].data_ptr(), st),
+                        d.vocab or self.m.s.vocab, self.drafts[n].data_ptr(), self.ndraft[n].data_ptr(), st),
                         "sr_synthetic_draft")
                     continue
                 _native.check(lib.sr_ngram_propose(

@@ -1,0 +1,100 @@
+"""Decoupled speculation across GPUs (configs[3] shape): ranks [0, D) draft,
+the rest verify; per round one NCCL P2P exchange per (drafter, verifier).
+
+    torchrun --nproc-per-node 2 scripts/decoupled_ranks.py --drafters 1 --check
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+from paper_2511_16193_b200 import scenarios  # noqa: E402
+from paper_2511_16193_b200.decoupled import pairing, run_ranks  # noqa: E402
+from paper_2511_16193_b200.dist import shard  # noqa: E402
+from paper_2511_16193_b200.engine import RolloutEngine, SyntheticDrafter  # noqa: E402
+from paper_2511_16193_b200.model import DeviceModel, init_weights, shape  # noqa: E402
+from paper_2511_16193_b200.streams import stream  # noqa: E402
+from paper_2511_16193_b200.workload import gen_trace  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--drafters", type=int, default=1)
+    ap.add_argument("--batch", type=int, default=64, help="prompts per verifier")
+    ap.add_argument("--model", default="tiny")
+    ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--k", type=int, default=4)
+    ap.add_argument("--method", default="draft-0.5b")
+    ap.add_argument("--cap", type=int, default=300, help="max generated tokens per request")
+    ap.add_argument("--check", action="store_true", help="compare outputs with plain decoding")
+    a = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    dist.init_process_group("nccl")
+    s = shape(a.model, a.layers)
+    nv = world - a.drafters
+    trace_all = gen_trace(scenarios.default_trace_spec(batch=a.batch * nv, seed=0))
+    shards, traces = {}, {}
+    for i, v in enumerate(range(a.drafters, world)):
+        tr = shard(trace_all, i, nv)
+        prompts = [stream(0, r.id, "prompt").integers(0, s.vocab, size=r.prompt_len).astype(np.int32) for r in tr]
+        shards[v] = (prompts, [min(r.true_len, a.cap) for r in tr])
+        traces[v] = tr
+    truth = {}
+    model = None
+    if rank >= a.drafters:
+        prompts, lens = shards[rank]
+        model = DeviceModel(s, init_weights(s, seed=0, device="cuda"), dtype="bf16", max_requests=len(prompts),
+                            max_len=max(len(p) + L for p, L in zip(prompts, lens)) + 2 * a.k + 16,
+                            max_tokens=max(2048, len(prompts) * (a.k + 1)), max_seqs=len(prompts))
+        plain = RolloutEngine(model, prompts, lens, k=0, history=1)
+        plain.prefill()
+        plain.run()
+        t = plain.outputs()
+        width = max(lens)
+        mat = torch.full((len(t), width), 0, dtype=torch.int32, device="cuda")
+        for b, row in enumerate(t):
+            mat[b, : len(row)] = torch.tensor(row, dtype=torch.int32)
+        truth[rank] = t
+        dist.send(mat, pairing(world, a.drafters)[rank])
+    else:
+        for v, d in pairing(world, a.drafters).items():
+            if d == rank:
+                lens = shards[v][1]
+                mat = torch.empty((len(lens), max(lens)), dtype=torch.int32, device="cuda")
+                dist.recv(mat, v)
+                truth[v] = [mat[b, :L].tolist() for b, L in enumerate(lens)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    outs, rows, rounds = run_ranks(
+        dist, rank, world, a.drafters, shards, a.k,
+        make_drafter=lambda v: SyntheticDrafter(truth[v], traces[v], a.method, 0, vocab=s.vocab),
+        make_model=lambda: model)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    res = {"rank": rank, "rounds": rounds, "seconds": dt}
+    if rank >= a.drafters:
+        committed = int(sum(len(o) for o in outs))
+        res.update(committed=committed, tokens_per_s=committed / dt,
+                   mean_accepted=float(rows[:, :, 1][rows[:, :, 0] > 0].mean()))
+        if a.check:
+            res["outputs_equal_plain"] = outs == truth[rank]
+    print(json.dumps(res), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -333,3 +333,36 @@ def test_engine_outcomes_match_reference_coupled_golden():
         got = [tuple(int(x) for x in row) for row in rows[:, b, :] if row[0] or row[2]]
         exp = [tuple(o[5:9]) for o in rec["outcomes"] if o[0] == r.id]
         assert got == exp, f"request {r.id}"
+
+
+def test_decoupled_outcomes_match_reference_golden():
+    """Depth-2 decoupled rollout (drafter and verifier roles; successors die
+    with their rejected predecessor) reproduces the reference simulator's
+    decoupled outcome stream, including depth-2 waste
+    (tests/golden/sim_runs.json, c1-decoupled-ngram-w4, sim.py:1051-1092)."""
+    from conftest import golden
+    from paper_2511_16193_b200 import scenarios
+    from paper_2511_16193_b200.decoupled import run_local
+    from paper_2511_16193_b200.engine import RolloutEngine, SyntheticDrafter
+    from paper_2511_16193_b200.model import DeviceModel, init_weights, shape
+    from paper_2511_16193_b200.streams import stream
+    from paper_2511_16193_b200.workload import gen_trace
+
+    rec = next(r for r in golden("sim_runs.json") if r["name"] == "c1-decoupled-ngram-w4")
+    trace = gen_trace(scenarios.default_trace_spec(batch=8, seed=0))
+    s = shape("tiny")
+    prompts = [stream(0, r.id, "prompt").integers(0, s.vocab, size=r.prompt_len).astype(np.int32) for r in trace]
+    lens = [r.true_len for r in trace]
+    max_len = max(len(p) + L for p, L in zip(prompts, lens)) + 16
+    m = DeviceModel(s, init_weights(s, seed=0), dtype="bf16", max_requests=8, max_len=max_len,
+                    max_tokens=2048, max_seqs=24)
+    plain = RolloutEngine(m, prompts, lens, k=0, history=1)
+    plain.prefill()
+    plain.run()
+    truth = plain.outputs()
+    outs, rows = run_local(m, prompts, lens, 4, SyntheticDrafter(truth, trace, "ngram", 0))
+    assert outs == truth
+    for b, r in enumerate(trace):
+        got = [tuple(int(x) for x in row) for row in rows[:, b, :] if row[0] or row[2]]
+        exp = [tuple(o[5:9]) for o in rec["outcomes"] if o[0] == r.id]
+        assert got == exp, f"request {r.id}"
