@@ -24,6 +24,8 @@
 
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 namespace sr {
 
 namespace {
@@ -78,6 +80,9 @@ struct AttnArgs {
   int qblocks, splits;
   int split_tiles;     // tiles per KV split (fixed per model: batch invariance)
   __nv_bfloat16* out;  // [M, nq, HD]
+  int* order;          // work items, longest first (attn_plan_kernel)
+  int* counters;       // [0] items in order, [1] work-claim counter
+  int n_slots;         // S*nkv * qblocks * splits
 };
 
 int g_split_tiles = 32;  // 2048-key splits
@@ -102,20 +107,35 @@ attn_bf16_kernel(AttnArgs A) {
   uint8_t* sKV = sQ + kRows * HD * 2;              // [stages][K tile, V tile]
 
   const int nkv = A.kv.kv_heads;
-  const int sp = blockIdx.x, qb = blockIdx.y;
-  const int s = blockIdx.z / nkv, h = blockIdx.z % nkv;
-  const SeqInfo sq = A.seqs[s];
   const int G = A.G;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // K/V ring: stage = [K tile | V tile]; full[stage] completes when both land.
+  // Stage/parity follow a CTA-global tile counter so the ring runs across items.
+  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ int s_item;
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) sm100::mbar_init(&full[i], 1);
+    sm100::fence_barrier_init();
+  }
+  uint32_t gi = 0;
+  for (;;) {
+  __syncthreads();  // previous item fully consumed (smem reusable)
+  if (tid == 0) s_item = atomicAdd(&A.counters[1], 1);
+  __syncthreads();
+  if (s_item >= A.counters[0]) break;
+  const int packed = A.order[s_item];
+  const int sp = packed % A.splits;
+  const int qb = (packed / A.splits) % A.qblocks;
+  const int z = packed / (A.splits * A.qblocks);
+  const int s = z / nkv, h = z % nkv;
+  const SeqInfo sq = A.seqs[s];
   const int rows_total = sq.q_len * G;
   const int r0 = qb * kRows;
-  if (r0 >= rows_total) return;
   const int rows = min(kRows, rows_total - r0);
   const int max_key = block_max_key(sq, r0, rows, G);
   const int ntiles = max_key / kKT + 1;
   const int t_begin = sp * A.split_tiles, t_end = min(ntiles, t_begin + A.split_tiles);
-  if (t_begin >= t_end) return;
   const int mtv = (rows + 15) / 16;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   const __nv_bfloat16* cache = reinterpret_cast<const __nv_bfloat16*>(A.kv.cache) +
                                (int64_t)A.layer * A.kv.cache_layer_elems();
@@ -134,14 +154,6 @@ attn_bf16_kernel(AttnArgs A) {
       *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
     }
   }
-
-  // K/V ring: stage = [K tile | V tile]; full[stage] completes when both land.
-  __shared__ __align__(8) uint64_t full[kStages];
-  if (tid == 0) {
-    for (int i = 0; i < kStages; ++i) sm100::mbar_init(&full[i], 1);
-    sm100::fence_barrier_init();
-  }
-  __syncthreads();
 
   // Called by all threads (uniform control flow).
   auto load_tile = [&](int t, int stage) {
@@ -208,17 +220,17 @@ attn_bf16_kernel(AttnArgs A) {
     qpos[hi] = r < rows ? sq.ctx_len + (r0 + r) / G : -1;  // -1: padding row, all masked
   }
   const int min_qpos = sq.ctx_len + r0 / G;  // first query row of the block
-  load_tile(t_begin, 0);
-  load_tile(t_begin + 1, 1);
+  load_tile(t_begin, gi % kStages);
+  load_tile(t_begin + 1, (gi + 1) % kStages);
   cp_async_commit();
   cp_async_wait<0>();  // Q block
   const uint32_t q_base = (uint32_t)__cvta_generic_to_shared(sQ);
   for (int t = t_begin; t < t_end; ++t) {
-    const int i = t - t_begin;
-    const int stage = i % kStages;
-    sm100::mbar_wait(&full[stage], (uint32_t)((i / kStages) & 1));
+    const uint32_t g = gi + (uint32_t)(t - t_begin);
+    const int stage = g % kStages;
+    sm100::mbar_wait(&full[stage], (g / kStages) & 1u);
     __syncthreads();  // tile t (incl. plain smem stores) visible; tile t-1's slot is free
-    load_tile(t + 2, (i + 2) % kStages);
+    load_tile(t + 2, (g + 2) % kStages);
     const uint32_t k_base = (uint32_t)__cvta_generic_to_shared(sKV + stage * 2 * kTileBytes);
     const uint32_t v_base = k_base + kTileBytes;
     const int key0 = t * kKT + kw * 16;
@@ -335,7 +347,7 @@ attn_bf16_kernel(AttnArgs A) {
     }
   }
   __syncthreads();
-  const int64_t pidx = ((int64_t)blockIdx.z * A.qblocks + qb) * A.splits + sp;
+  const int64_t pidx = ((int64_t)z * A.qblocks + qb) * A.splits + sp;
   float* po = A.part_o + pidx * kRows * HD;
   float* pml = A.part_ml + pidx * kRows * 2;
   // A block whose keys fit one split finishes here: out = O / l is exactly
@@ -375,6 +387,46 @@ attn_bf16_kernel(AttnArgs A) {
       pml[r * 2] = M;
       pml[r * 2 + 1] = l;
     }
+  }
+  gi += (uint32_t)(t_end - t_begin);
+  }  // item loop
+}
+
+// Work list of the persistent attention kernel: every non-empty (sequence x
+// kv head, query block, split) item, ordered by decreasing tile count
+// (counting sort), so the 2-per-SM persistent CTAs claim the longest items
+// first (LPT).  Processing order does not change any item's arithmetic.
+__global__ void __launch_bounds__(1024) attn_plan_kernel(AttnArgs A) {
+  __shared__ int hist[1025];
+  __shared__ int base[1025];
+  const int T = A.split_tiles;
+  for (int i = threadIdx.x; i <= T; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const int nkv = A.kv.kv_heads;
+  auto tiles_of = [&](int packed) {
+    const int sp = packed % A.splits;
+    const int qb = (packed / A.splits) % A.qblocks;
+    const int z = packed / (A.splits * A.qblocks);
+    const SeqInfo sq = A.seqs[z / nkv];
+    const int rows_total = sq.q_len * A.G;
+    const int r0 = qb * kRows;
+    if (r0 >= rows_total) return 0;
+    const int rows = min(kRows, rows_total - r0);
+    const int ntiles = block_max_key(sq, r0, rows, A.G) / kKT + 1;
+    return max(0, min(ntiles, sp * T + T) - sp * T);
+  };
+  for (int i = threadIdx.x; i < A.n_slots; i += blockDim.x) atomicAdd(&hist[tiles_of(i)], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int t = T; t >= 1; --t) { base[t] = acc; acc += hist[t]; }
+    A.counters[0] = acc;
+    A.counters[1] = 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < A.n_slots; i += blockDim.x) {
+    const int t = tiles_of(i);
+    if (t > 0) A.order[atomicAdd(&base[t], 1)] = i;
   }
 }
 
@@ -472,7 +524,8 @@ size_t attention_partial_floats(int num_seqs, int kv_heads, int qblocks, int spl
 size_t attention_workspace_floats(int max_seqs, int max_tokens, int G, int kv_heads, int max_key, int hd) {
   const int qblocks = max_seqs + (max_tokens * G + kRows - 1) / kRows;
   const int splits = ceil_div(max_key / kKT + 1, 4);  // bound for any split size >= 4 tiles
-  return attention_partial_floats(1, kv_heads, qblocks, splits, hd);
+  const size_t slots = (size_t)qblocks * kv_heads * splits;
+  return attention_partial_floats(1, kv_heads, qblocks, splits, hd) + (slots + 2 + 63) / 64 * 64;
 }
 
 int attention_bf16(const __nv_bfloat16* q, const SeqInfo* seqs, int num_seqs, int max_q_len, int max_key,
@@ -488,12 +541,24 @@ int attention_bf16(const __nv_bfloat16* q, const SeqInfo* seqs, int num_seqs, in
   a.qblocks = ceil_div(max_q_len * G, kRows);
   a.split_tiles = g_split_tiles;
   a.splits = ceil_div(max_key / kKT + 1, a.split_tiles);
-  const size_t need = attention_partial_floats(num_seqs, kv.kv_heads, a.qblocks, a.splits, hd);
+  a.n_slots = num_seqs * kv.kv_heads * a.qblocks * a.splits;
+  // partial workspace = [item list (n_slots + 2 ints, 256 B aligned) | O | (m, l)]
+  const size_t list_floats = ((size_t)a.n_slots + 2 + 63) / 64 * 64;
+  const size_t need = list_floats + attention_partial_floats(num_seqs, kv.kv_heads, a.qblocks, a.splits, hd);
   SR_REQUIRE(need <= partial_floats, "attention partial workspace too small");
-  a.part_o = partials;
-  a.part_ml = partials + (size_t)num_seqs * kv.kv_heads * a.qblocks * a.splits * kRows * hd;
-  const dim3 grid(a.splits, a.qblocks, num_seqs * kv.kv_heads);
+  a.counters = reinterpret_cast<int*>(partials);
+  a.order = a.counters + 2;
+  a.part_o = partials + list_floats;
+  a.part_ml = a.part_o + (size_t)num_seqs * kv.kv_heads * a.qblocks * a.splits * kRows * hd;
   if (phase == 0) {
+    attn_plan_kernel<<<1, 1024, 0, stream>>>(a);
+    int rc = check_launch("attn_plan_kernel");
+    if (rc) return rc;
+    // persistent: two CTAs per SM (smem/register limited), longest items first
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = std::min(a.n_slots, 2 * (sms > 0 ? sms : 148));
     if (hd == 128) {
       static bool set = false;
       if (!set) {
