@@ -111,7 +111,11 @@ int sr_ngram_propose(int batch, const int32_t* tokens, int64_t stride, const int
  * K1 building block: C = A[M,K] . W[N,K]^T with a fused epilogue (the
  * projections of the target model's verification forward; no reference
  * counterpart -- the reference has no model).
- *   dtype 1: bf16 A/W on tcgen05 tensor cores (TMA + TMEM), bn = 128|256|0
+ *   dtype 1: bf16 A/W on tcgen05 tensor cores (TMA + TMEM).  bn selects the
+ *            tile: 128|256 one CTA per 128-row tile; -w a CTA pair
+ *            (cta_group::2) per 256 x w tile, w a multiple of 16 in [64, 256];
+ *            -(1024 + w) two such pairs per cluster sharing A by TMA
+ *            multicast; 0 chooses from (M, N, K)
  *   dtype 0: fp32 A/W on CUDA cores (parity path), bn ignored
  * epilogue 0: C = acc + bias (bf16; f32 when dtype 0)
  *          1: C(f32) += acc                      (residual stream)

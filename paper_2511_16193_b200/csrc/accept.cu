@@ -27,6 +27,7 @@ __global__ void accept_commit_kernel(int B, int N, const SeqInfo* __restrict__ s
                                      int32_t* __restrict__ gen_len, const int32_t* __restrict__ max_new,
                                      int bonus, int32_t* __restrict__ outcome,
                                      int32_t* __restrict__ bon) {
+  grid_dep_sync();
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= B) return;
@@ -83,6 +84,7 @@ __global__ void accept_commit_kernel(int B, int N, const SeqInfo* __restrict__ s
 template <typename T>
 __global__ void kv_commit_kernel(int N, const SeqInfo* __restrict__ seqs, const int32_t* __restrict__ outcome,
                                  const int32_t* __restrict__ bon, KvLayout kv) {
+  grid_dep_sync();
   const int b = blockIdx.x, layer = blockIdx.y;
   const int w = bon[b];
   if (w < 0) return;
@@ -113,6 +115,7 @@ __global__ void build_verify_kernel(int B, int N, int k, const int32_t* __restri
                                     const int32_t* __restrict__ max_new, const int32_t* __restrict__ drafts,
                                     const int32_t* __restrict__ ndraft, int32_t* __restrict__ token_ids,
                                     int32_t* __restrict__ positions, SeqInfo* __restrict__ seqs) {
+  grid_dep_sync();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= B * N) return;
   const int b = s / N, n = s % N;
@@ -154,6 +157,7 @@ __global__ void synthetic_draft_kernel(int B, int k, const int32_t* __restrict__
                                        int64_t u_stride, const double* __restrict__ p,
                                        const int32_t* __restrict__ gen_len, int vocab,
                                        int32_t* __restrict__ drafts, int32_t* __restrict__ ndraft) {
+  grid_dep_sync();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const int g0 = gen_len[b];
@@ -182,6 +186,7 @@ __global__ void draft_batch_kernel(int B, int k, int step, const int32_t* __rest
                                    int32_t* __restrict__ ndraft, int32_t* __restrict__ token_ids,
                                    int32_t* __restrict__ positions, SeqInfo* __restrict__ seqs,
                                    int32_t* __restrict__ logit_rows) {
+  grid_dep_sync();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const int rows = k + 2;
@@ -228,9 +233,9 @@ int kv_commit(int B, int N, const SeqInfo* seqs, const int32_t* outcome, const i
   if (B == 0 || N <= 1) return SR_OK;
   dim3 grid(B, kv.layers);
   if (dtype == 1)
-    kv_commit_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(N, seqs, outcome, bon, kv);
+    sr::launch_k(kv_commit_kernel<__nv_bfloat16>, grid, 256, 0, s, N, seqs, outcome, bon, kv);
   else
-    kv_commit_kernel<float><<<grid, 256, 0, s>>>(N, seqs, outcome, bon, kv);
+    sr::launch_k(kv_commit_kernel<float>, grid, 256, 0, s, N, seqs, outcome, bon, kv);
   return check_launch("kv_commit_kernel");
 }
 
@@ -246,7 +251,7 @@ extern "C" int sr_accept_commit(int num_requests, int num_drafters, const void* 
   SR_REQUIRE(num_drafters >= 1 && num_drafters <= 32, "num_drafters out of [1, 32]");
   SR_REQUIRE(seqs && token_ids && target && tokens && seq_len && gen_len && max_new && outcome && bon,
              "null pointer");
-  sr::accept_commit_kernel<<<sr::ceil_div(num_requests, 8), 256, 0, (cudaStream_t)stream>>>(
+  sr::launch_k(sr::accept_commit_kernel, sr::ceil_div(num_requests, 8), 256, 0, (cudaStream_t)stream, 
       num_requests, num_drafters, reinterpret_cast<const sr::SeqInfo*>(seqs), token_ids, target, tokens,
       tok_stride, seq_len, gen_len, max_new, bonus_token, outcome, bon);
   return sr::check_launch("accept_commit_kernel");
@@ -259,7 +264,7 @@ extern "C" int sr_synthetic_draft(int num_requests, int k, const int32_t* truth,
   SR_REQUIRE(num_requests >= 0 && k >= 1 && vocab >= 2, "bad synthetic draft shape");
   if (num_requests == 0) return SR_OK;
   SR_REQUIRE(truth && truth_len && uniforms && accept_p && gen_len && drafts && ndraft, "null pointer");
-  sr::synthetic_draft_kernel<<<sr::ceil_div(num_requests, 128), 128, 0, (cudaStream_t)stream>>>(
+  sr::launch_k(sr::synthetic_draft_kernel, sr::ceil_div(num_requests, 128), 128, 0, (cudaStream_t)stream, 
       num_requests, k, truth, truth_stride, truth_len, uniforms, u_stride, accept_p, gen_len, vocab, drafts,
       ndraft);
   return sr::check_launch("synthetic_draft_kernel");
@@ -275,7 +280,7 @@ extern "C" int sr_draft_model_batch(int num_requests, int k, int step, const int
   SR_REQUIRE(tokens && seq_len && gen_len && max_new && dkv_len && drafts && ndraft && token_ids && positions &&
                  seqs && logit_rows && (step == 0 || prev_out),
              "null pointer");
-  sr::draft_batch_kernel<<<sr::ceil_div(num_requests, 128), 128, 0, (cudaStream_t)stream>>>(
+  sr::launch_k(sr::draft_batch_kernel, sr::ceil_div(num_requests, 128), 128, 0, (cudaStream_t)stream, 
       num_requests, k, step, tokens, tok_stride, seq_len, gen_len, max_new, dkv_len, prev_out, drafts, ndraft,
       token_ids, positions, reinterpret_cast<sr::SeqInfo*>(seqs), logit_rows);
   return sr::check_launch("draft_batch_kernel");
@@ -291,7 +296,7 @@ extern "C" int sr_build_verify_batch(int num_requests, int num_drafters, int k, 
   SR_REQUIRE(tokens && seq_len && gen_len && max_new && token_ids && positions && seqs, "null pointer");
   SR_REQUIRE(drafts == nullptr || ndraft != nullptr, "drafts without ndraft");
   const int S = num_requests * num_drafters;
-  sr::build_verify_kernel<<<sr::ceil_div(S, 128), 128, 0, (cudaStream_t)stream>>>(
+  sr::launch_k(sr::build_verify_kernel, sr::ceil_div(S, 128), 128, 0, (cudaStream_t)stream, 
       num_requests, num_drafters, k, tokens, tok_stride, seq_len, gen_len, max_new, drafts, ndraft,
       token_ids, positions, reinterpret_cast<sr::SeqInfo*>(seqs));
   return sr::check_launch("build_verify_kernel");

@@ -99,6 +99,7 @@ __device__ __forceinline__ int block_max_key(const SeqInfo& sq, int r0, int rows
 template <int HD>
 __global__ void __launch_bounds__(kAttnThreads, 2)
 attn_bf16_kernel(AttnArgs A) {
+  grid_dep_sync();
   constexpr int CH = HD / 8;       // 16-byte chunks per row
   constexpr int NO = HD / 8;       // n8 tiles of O per m-tile
   constexpr uint32_t kTileBytes = kKT * HD * 2;
@@ -397,6 +398,7 @@ attn_bf16_kernel(AttnArgs A) {
 // (counting sort), so the 2-per-SM persistent CTAs claim the longest items
 // first (LPT).  Processing order does not change any item's arithmetic.
 __global__ void __launch_bounds__(1024) attn_plan_kernel(AttnArgs A) {
+  grid_dep_sync();
   __shared__ int hist[1025];
   __shared__ int base[1025];
   const int T = A.split_tiles;
@@ -435,6 +437,7 @@ __global__ void __launch_bounds__(1024) attn_plan_kernel(AttnArgs A) {
 template <int HD>
 __global__ void __launch_bounds__(256)
 attn_combine_kernel(AttnArgs A) {
+  grid_dep_sync();
   const int nkv = A.kv.kv_heads;
   const int qb = blockIdx.y, z = blockIdx.z;
   const int s = z / nkv, h = z % nkv;
@@ -467,6 +470,7 @@ attn_combine_kernel(AttnArgs A) {
 // order with an fp32 online softmax (no splits).
 __global__ void attn_f32_kernel(const float* __restrict__ q, const SeqInfo* __restrict__ seqs, KvLayout kv,
                                 int layer, int nq, int G, float scale, float* __restrict__ out) {
+  grid_dep_sync();
   const SeqInfo sq = seqs[blockIdx.y];
   const int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -551,7 +555,7 @@ int attention_bf16(const __nv_bfloat16* q, const SeqInfo* seqs, int num_seqs, in
   a.part_o = partials + list_floats;
   a.part_ml = a.part_o + (size_t)num_seqs * kv.kv_heads * a.qblocks * a.splits * kRows * hd;
   if (phase == 0) {
-    attn_plan_kernel<<<1, 1024, 0, stream>>>(a);
+    sr::launch_k(attn_plan_kernel, 1, 1024, 0, stream, a);
     int rc = check_launch("attn_plan_kernel");
     if (rc) return rc;
     // persistent: two CTAs per SM (smem/register limited), longest items first
@@ -566,7 +570,7 @@ int attention_bf16(const __nv_bfloat16* q, const SeqInfo* seqs, int num_seqs, in
                                            (int)attn_smem<128>()));
         set = true;
       }
-      attn_bf16_kernel<128><<<grid, kAttnThreads, attn_smem<128>(), stream>>>(a);
+      sr::launch_k(attn_bf16_kernel<128>, grid, kAttnThreads, attn_smem<128>(), stream, a);
     } else {
       static bool set = false;
       if (!set) {
@@ -574,14 +578,14 @@ int attention_bf16(const __nv_bfloat16* q, const SeqInfo* seqs, int num_seqs, in
                                            (int)attn_smem<64>()));
         set = true;
       }
-      attn_bf16_kernel<64><<<grid, kAttnThreads, attn_smem<64>(), stream>>>(a);
+      sr::launch_k(attn_bf16_kernel<64>, grid, kAttnThreads, attn_smem<64>(), stream, a);
     }
     return check_launch("attn_bf16_kernel");
   }
   if (a.splits <= 1) return SR_OK;  // every block finished in the main kernel
   const dim3 cgrid(ceil_div(kRows * hd, 256), a.qblocks, num_seqs * kv.kv_heads);
-  if (hd == 128) attn_combine_kernel<128><<<cgrid, 256, 0, stream>>>(a);
-  else attn_combine_kernel<64><<<cgrid, 256, 0, stream>>>(a);
+  if (hd == 128) sr::launch_k(attn_combine_kernel<128>, cgrid, 256, 0, stream, a);
+  else sr::launch_k(attn_combine_kernel<64>, cgrid, 256, 0, stream, a);
   return check_launch("attn_combine_kernel");
 }
 
@@ -591,7 +595,7 @@ int attention_f32(const float* q, const SeqInfo* seqs, int num_seqs, int max_q_l
   SR_REQUIRE(kv.head_dim <= 128, "fp32 attention supports head_dim <= 128");
   const int G = nq / kv.kv_heads;
   dim3 grid(ceil_div(max_q_len * nq, 8), num_seqs);
-  attn_f32_kernel<<<grid, 256, 0, stream>>>(q, seqs, kv, layer, nq, G, 1.0f / sqrtf((float)kv.head_dim), out);
+  sr::launch_k(attn_f32_kernel, grid, 256, 0, stream, q, seqs, kv, layer, nq, G, 1.0f / sqrtf((float)kv.head_dim), out);
   return check_launch("attn_f32_kernel");
 }
 

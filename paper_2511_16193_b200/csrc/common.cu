@@ -2,12 +2,19 @@
 #include "common.cuh"
 
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 
 namespace sr {
 
 static thread_local char g_last_error[1024] = {0};
 static std::atomic<long long> g_launches{0};
+
+static bool pdl_from_env() {
+  const char* v = getenv("SR_PDL");
+  return !(v && v[0] == '0');
+}
+bool g_pdl = pdl_from_env();
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdarg>
+#include <utility>
 
 #include "../../include/specrollout_b200.h"
 
@@ -31,6 +32,37 @@ inline int check_launch(const char* kernel) {
 }
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// Programmatic dependent launch.  Every kernel is launched with
+// programmatic stream serialization and begins (after any prologue that
+// touches no predecessor output) with grid_dep_sync(): wait for the previous
+// grid in the stream to complete and flush, then allow the next grid to be
+// scheduled.  The next kernel's CTA launch and prologue thus overlap this
+// kernel's body and tail instead of following its last CTA (within a CUDA
+// graph as well as eagerly).  Every kernel waits before any global access,
+// so ordering is transitive along the stream.  SR_PDL=0 disables it.
+extern bool g_pdl;
+
+__device__ __forceinline__ void grid_dep_sync() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);  // error surfaces in check_launch
+}
 
 }  // namespace sr
 

@@ -25,6 +25,7 @@
 #include "sm100.cuh"
 
 #include <cudaTypedefs.h>
+#include <cstdlib>
 
 namespace sr {
 
@@ -197,26 +198,30 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  grid_dep_sync();  // prologue above touched no predecessor output
 
   if (warp == 0) {
-    if (lane == 0) {
+    {
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int m_blk = tile % num_m, n_blk = tile / num_m;
         for (int kb = 0; kb < num_kb; ++kb) {
           sm100::mbar_wait(&empty[stage], phase ^ 1);
-          sm100::mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
-          sm100::tma_load_2d(sA + stage * Cfg::kABytes, &tmA, &full[stage], kb * kBK, m_blk * kBM,
-                             sm100::kEvictLast);
-          sm100::tma_load_2d(sB + stage * Cfg::kBBytes, &tmB, &full[stage], kb * kBK, n_blk * BN,
-                             sm100::kEvictNormal);
+          if (sm100::elect_one()) {
+            sm100::mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+            sm100::tma_load_2d(sA + stage * Cfg::kABytes, &tmA, &full[stage], kb * kBK, m_blk * kBM,
+                               sm100::kEvictLast);
+            sm100::tma_load_2d(sB + stage * Cfg::kBBytes, &tmB, &full[stage], kb * kBK, n_blk * BN,
+                               sm100::kEvictNormal);
+          }
+          __syncwarp();
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
       constexpr uint32_t idesc = sm100::umma_idesc_bf16(kBM, BN);
       int stage = 0;
       uint32_t phase = 0;
@@ -231,15 +236,19 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           sm100::tc_fence_after();
           const uint32_t a0 = sm100::smem_u32(sA + stage * Cfg::kABytes);
           const uint32_t b0 = sm100::smem_u32(sB + stage * Cfg::kBBytes);
+          if (sm100::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            sm100::umma_bf16(d, sm100::umma_desc_sw128(a0 + k * 32), sm100::umma_desc_sw128(b0 + k * 32),
-                             idesc, (kb | k) != 0);
+            for (int k = 0; k < kBK / 16; ++k) {
+              sm100::umma_bf16(d, sm100::umma_desc_sw128(a0 + k * 32), sm100::umma_desc_sw128(b0 + k * 32),
+                               idesc, (kb | k) != 0);
+            }
+            sm100::umma_commit(&empty[stage]);
           }
-          sm100::umma_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
-        sm100::umma_commit(&tfull[acc]);
+        if (sm100::elect_one()) sm100::umma_commit(&tfull[acc]);
+        __syncwarp();
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -292,25 +301,44 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 // leader issues tcgen05.mma.cta_group::2 (M=256) reading both CTAs' shared
 // memory, and each CTA's TMEM holds its 128 accumulator rows.  Per SM this
 // halves the weight bytes per MAC, the bound of the 1-CTA kernel.
+//
+// KC = k chunks (64 wide, one 128-byte swizzle atom per row) per pipeline
+// stage.  With KC = 2 each operand is staged by ONE 3D TMA instruction
+// (chunk as the outer box dimension) per 128 k: measured on B200, a stage
+// costs ~280 clk of TMA issue + barrier turnaround regardless of size up to
+// ~32 KB, plus ~100 clk per extra instruction (scripts/micro/tma_rate.cu),
+// so 64-k stages with two instructions (~400 clk) starve a 256 x 128 MMA
+// (256 clk) while 128-k stages (~450 clk vs 512 clk of MMA) do not.
 
-template <int BN>
+
+template <int BN, int KC = 1>
 struct PairCfg {
   static constexpr int kBNH = BN / 2;
-  static constexpr uint32_t kABytes = kBM * kBK * 2;
-  static constexpr uint32_t kBBytes = kBNH * kBK * 2;
+  static constexpr uint32_t kAChunk = kBM * kBK * 2;   // 128 rows x 128 B
+  static constexpr uint32_t kBChunk = kBNH * kBK * 2;
+  static constexpr uint32_t kABytes = KC * kAChunk;
+  static constexpr uint32_t kBBytes = KC * kBChunk;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (196608 / kStageBytes) < 8 ? (196608 / kStageBytes) : 8;
+  static constexpr int kStages = (212992 / kStageBytes) < 8 ? (212992 / kStageBytes) : 8;
   static constexpr uint32_t kTmemCols = 2 * BN <= 256 ? 256 : 512;
   static constexpr int kChunk = BN % 32 == 0 ? 32 : 16;
   static constexpr size_t kSmem = 1024 + (size_t)kStages * kStageBytes + 256;
 };
 
-template <int BN, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// MC = 2: a cluster of two pairs computes two horizontally adjacent tiles
+// (n blocks 2j, 2j+1) of the same 256 rows.  Both pairs need the same
+// activation rows, so each CTA loads half of its 128-row A block and
+// multicasts it to itself and its counterpart in the other pair: A's L2->SM
+// traffic halves, the bound of the small-N verify GEMMs (o, down, qkv).  A
+// stage is reusable only when both pairs' MMAs have drained it, so the
+// leaders' commits are multicast to all four CTAs' empty barriers (count 2).
+template <int BN, int EPI, int MC, int KC>
+__global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  int M, int N, int K, void* C, int ldc, const float* __restrict__ bias,
                  int32_t* __restrict__ aux, SampleArgs sa) {
-  using Cfg = PairCfg<BN>;
+  static_assert(MC == 1 || KC == 1 || KC == MC, "A multicast splits rows (KC 1) or k chunks (KC == MC)");
+  using Cfg = PairCfg<BN, KC>;
   constexpr int S = Cfg::kStages;
   constexpr int CW = Cfg::kChunk;
   extern __shared__ uint8_t smem_raw[];
@@ -324,18 +352,21 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = sm100::cluster_ctarank();
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const uint32_t crank = sm100::cluster_ctarank();
+  const uint32_t rank = crank & 1;        // position inside the pair
+  const uint32_t q = crank >> 1;          // pair inside the cluster
+  const uint32_t lead = crank & ~1u;      // this pair's MMA-issuing CTA
+  const int pair = blockIdx.x / (2 * MC), npairs = gridDim.x / (2 * MC);
   const int num_m = (M + 2 * kBM - 1) / (2 * kBM), num_n = (N + BN - 1) / BN;
-  const int num_tiles = num_m * num_n;
-  const int num_kb = (K + kBK - 1) / kBK;
+  const int num_tiles = num_m * ((num_n + MC - 1) / MC);
+  const int num_kb = (K + KC * kBK - 1) / (KC * kBK);
 
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch_desc(&tmA);
     sm100::tma_prefetch_desc(&tmB);
     for (int s = 0; s < S; ++s) {
       sm100::mbar_init(&full[s], 1);
-      sm100::mbar_init(&empty[s], 1);
+      sm100::mbar_init(&empty[s], MC);  // one commit per pair reading this CTA's loads
     }
     for (int a = 0; a < 2; ++a) {
       sm100::mbar_init(&tfull[a], 1);
@@ -348,28 +379,50 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   sm100::cluster_sync();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  grid_dep_sync();  // prologue above touched no predecessor output
 
   if (warp == 0) {
-    if (lane == 0) {
+    {
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = pair; tile < num_tiles; tile += npairs) {
-        const int m_blk = tile % num_m, n_blk = tile / num_m;
+        const int m_blk = tile % num_m, n_blk = (tile / num_m) * MC + (int)q;
         const int arow = m_blk * 2 * kBM + (int)rank * kBM;
         const int brow = n_blk * BN + (int)rank * Cfg::kBNH;
         for (int kb = 0; kb < num_kb; ++kb) {
           sm100::mbar_wait(&empty[stage], phase ^ 1);
+          if (sm100::elect_one()) {
           if (rank == 0) sm100::mbar_arrive_expect_tx(&full[stage], 2 * Cfg::kStageBytes);
-          sm100::tma_load_2d_pair(sA + stage * Cfg::kABytes, &tmA, &full[stage], kb * kBK, arow,
-                                  sm100::kEvictLast);
-          sm100::tma_load_2d_pair(sB + stage * Cfg::kBBytes, &tmB, &full[stage], kb * kBK, brow,
-                                  sm100::kEvictNormal);
+          if constexpr (MC > 1 && KC == MC) {
+            // chunk q of this stage's A for both pairs (same rows, same layout)
+            sm100::tma_load_2d_pair_mc(sA + stage * Cfg::kABytes + q * Cfg::kAChunk, &tmA, &full[stage],
+                                       (kb * KC + (int)q) * kBK, arow,
+                                       (uint16_t)((1u << crank) | (1u << (crank ^ 2u))), sm100::kEvictLast);
+          } else if constexpr (KC > 1) {
+            sm100::tma_load_3d_pair(sA + stage * Cfg::kABytes, &tmA, &full[stage], 0, arow, kb * KC,
+                                    sm100::kEvictLast);
+          } else if constexpr (MC == 1) {
+            sm100::tma_load_2d_pair(sA + stage * Cfg::kABytes, &tmA, &full[stage], kb * kBK, arow,
+                                    sm100::kEvictLast);
+          } else {
+            sm100::tma_load_2d_pair_mc(sA + stage * Cfg::kABytes + q * (Cfg::kABytes / 2), &tmA,
+                                       &full[stage], kb * kBK, arow + (int)q * (kBM / 2),
+                                       (uint16_t)((1u << crank) | (1u << (crank ^ 2u))), sm100::kEvictLast);
+          }
+          if constexpr (KC > 1)
+            sm100::tma_load_3d_pair(sB + stage * Cfg::kBBytes, &tmB, &full[stage], 0, brow, kb * KC,
+                                    sm100::kEvictNormal);
+          else
+            sm100::tma_load_2d_pair(sB + stage * Cfg::kBBytes, &tmB, &full[stage], kb * kBK, brow,
+                                    sm100::kEvictNormal);
+          }
+          __syncwarp();
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (rank == 0 && lane == 0) {
+    if (rank == 0) {
       constexpr uint32_t idesc = sm100::umma_idesc_bf16(2 * kBM, BN);
       int stage = 0;
       uint32_t phase = 0;
@@ -384,24 +437,29 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           sm100::tc_fence_after();
           const uint32_t a0 = sm100::smem_u32(sA + stage * Cfg::kABytes);
           const uint32_t b0 = sm100::smem_u32(sB + stage * Cfg::kBBytes);
+          if (sm100::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            sm100::umma_bf16_pair(d, sm100::umma_desc_sw128(a0 + k * 32), sm100::umma_desc_sw128(b0 + k * 32),
-                                  idesc, (kb | k) != 0);
-          sm100::umma_commit_pair(&empty[stage], 0x3);
+            for (int k = 0; k < KC * kBK / 16; ++k)
+              sm100::umma_bf16_pair(d, sm100::umma_desc_sw128(a0 + (k >> 2) * Cfg::kAChunk + (k & 3) * 32),
+                                    sm100::umma_desc_sw128(b0 + (k >> 2) * Cfg::kBChunk + (k & 3) * 32),
+                                    idesc, (kb | k) != 0);
+            sm100::umma_commit_pair(&empty[stage], MC == 1 ? 0x3 : 0xF);
+          }
+          __syncwarp();
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
-        sm100::umma_commit_pair(&tfull[acc], 0x3);
+        if (sm100::elect_one()) sm100::umma_commit_pair(&tfull[acc], (uint16_t)(0x3u << lead));
+        __syncwarp();
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else {
     const int quad = warp & 3;
-    const uint32_t leader_tempty = sm100::mapa_shared(sm100::smem_u32(tempty), 0);
+    const uint32_t leader_tempty = sm100::mapa_shared(sm100::smem_u32(tempty), lead);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = pair; tile < num_tiles; tile += npairs) {
-      const int m_blk = tile % num_m, n_blk = tile / num_m;
+      const int m_blk = tile % num_m, n_blk = (tile / num_m) * MC + (int)q;
       const int row = m_blk * 2 * kBM + (int)rank * kBM + quad * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
       if constexpr (EPI == kEpiResidualF32 && BN <= 128) {
@@ -465,7 +523,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
       }
       if constexpr (EPI == kEpiArgmax) {
-        if (row < M) {
+        if (row < M && n_blk < num_n) {
           const int tiles_n = (N + BN - 1) / BN;
           reinterpret_cast<float*>(C)[(int64_t)row * tiles_n + n_blk] = best;
           aux[(int64_t)row * tiles_n + n_blk] = best_idx;
@@ -498,6 +556,10 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 }
 
 int g_num_sms = 0;
+int g_pair_kc = [] {
+  const char* v = getenv("SR_GEMM_KC");
+  return (v && v[0] == '1') ? 1 : 2;
+}();
 
 int num_sms() {
   if (g_num_sms == 0) {
@@ -520,7 +582,7 @@ int launch_typed(const GemmPlan& p, int M, cudaStream_t stream) {
   }
   const int tiles = ((M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, kThreads, Cfg::kSmem, stream>>>(p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux, p.sample);
+  sr::launch_k(kern, grid, kThreads, Cfg::kSmem, stream, p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux, p.sample);
   return check_launch("gemm_tcgen05_kernel");
 }
 
@@ -537,20 +599,29 @@ int launch_bn(const GemmPlan& p, int M, cudaStream_t stream) {
 }
 
 
-template <int BN, int EPI>
-int launch_pair_typed(const GemmPlan& p, int M, cudaStream_t stream) {
-  using Cfg = PairCfg<BN>;
-  auto kern = gemm_pair_kernel<BN, EPI>;
+template <int BN, int EPI, int MC, int KC>
+int launch_pair_mc(const GemmPlan& p, int M, cudaStream_t stream) {
+  using Cfg = PairCfg<BN, KC>;
+  auto kern = gemm_pair_kernel<BN, EPI, MC, KC>;
   static bool attr_set = false;
   if (!attr_set) {
     SR_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
     attr_set = true;
   }
-  const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * ((p.N + BN - 1) / BN);
-  const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-  kern<<<2 * pairs, kThreads, Cfg::kSmem, stream>>>(p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux,
+  const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * (((p.N + BN - 1) / BN + MC - 1) / MC);
+  const int slots = num_sms() / (2 * MC);
+  const int clusters = tiles < slots ? tiles : slots;
+  sr::launch_k(kern, 2 * MC * clusters, kThreads, Cfg::kSmem, stream, p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux,
                                                     p.sample);
   return check_launch("gemm_pair_kernel");
+}
+
+template <int BN, int EPI>
+int launch_pair_typed(const GemmPlan& p, int M, cudaStream_t stream) {
+  if (p.mc == 2) {
+    return p.kc == 2 ? launch_pair_mc<BN, EPI, 2, 2>(p, M, stream) : launch_pair_mc<BN, EPI, 2, 1>(p, M, stream);
+  }
+  return p.kc == 2 ? launch_pair_mc<BN, EPI, 1, 2>(p, M, stream) : launch_pair_mc<BN, EPI, 1, 1>(p, M, stream);
 }
 
 template <int BN>
@@ -581,25 +652,32 @@ int launch_pair(const GemmPlan& p, int M, cudaStream_t stream) {
   return config_error("unsupported pair tile width (64|96|112|128|160|192|224|256)");
 }
 
-// Pair tile width minimizing waves x per-tile time, where a k-block costs
-// max(MMA: 2*BN clk, operand ingress: (16 KB + 64*BN B) / 62 B/clk per SM).
-int choose_pair_bn(int M, int N, int epi) {
-  // multiples of 32 only: 16-column epilogue chunks and N % 32 != 0 MMAs
-  // measured slower on B200 (scripts/gemm_probe.py)
+// Pair tile (width, pairs per cluster).  Measured on B200 (scripts/
+// gemm_probe.py) the pair kernel is MMA-bound once operands are staged 128 k
+// per TMA instruction: a 64-k block of a 256 x BN tile costs ~1.64 ns * BN,
+// plus ~1.5 us per tile of fill/drain.  Minimize waves x per-tile time over
+// widths that are multiples of 32 (16-column epilogue chunks measured
+// slower).  Two pairs per cluster multicasting A save ~3% when the grid is a
+// single wave with an even tile count per row block, and lose badly
+// (cluster-of-4 residency) over several waves.
+void choose_pair_tile(int M, int N, int K, int epi, int* bn_out, int* mc_out) {
   static const int cands[] = {256, 224, 192, 160, 128, 96, 64};
-  const int pairs = num_sms() / 2;
   const int num_m = (M + 255) / 256;
+  const int kb = (K + 63) / 64;
+  const int pairs = num_sms() / 2;
   int best = 256;
   double best_t = 1e30;
   for (int bn : cands) {
     if (epi == kEpiSwiGLU && bn % 32 != 0) continue;
     const int tiles = num_m * ((N + bn - 1) / bn);
     const int waves = (tiles + pairs - 1) / pairs;
-    const double kb = fmax(2.0 * bn, (16384.0 + 64.0 * bn) / 62.0);
-    const double t = waves * kb;
+    const double t = waves * ((double)kb * bn + 900.0);
     if (t < best_t * 0.999) { best_t = t; best = bn; }
   }
-  return best;
+  const int num_n = (N + best - 1) / best;
+  const int clusters = num_m * (num_n / 2);
+  *bn_out = best;
+  *mc_out = (num_n % 2 == 0 && clusters <= num_sms() / 4) ? 2 : 1;
 }
 }  // namespace
 
@@ -625,6 +703,31 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t 
   return SR_OK;
 }
 
+// [rows, K] bf16 viewed as (64-element k chunk, row, chunk index): a box of
+// (64, box_rows, box_chunks) lands as box_chunks swizzled [box_rows x 128 B]
+// blocks back to back -- the K-major SW128 layout UMMA reads per 16-k step.
+int make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t K, uint64_t rows, uint64_t row_bytes,
+                      uint32_t box_rows, uint32_t box_chunks) {
+  auto enc = tmap_encoder();
+  if (enc == nullptr) {
+    set_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
+    return SR_ERR_RUNTIME;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)kBK, rows, K / kBK};
+  cuuint64_t strides[2] = {row_bytes, (cuuint64_t)kBK * 2};
+  cuuint32_t box[3] = {(cuuint32_t)kBK, box_rows, box_chunks};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (3d) failed (%d): K=%llu rows=%llu", (int)r, (unsigned long long)K,
+              (unsigned long long)rows);
+    return SR_ERR_CONFIG;
+  }
+  return SR_OK;
+}
+
 int gemm_bf16_plan(GemmPlan* p, int M, int N, int K, const __nv_bfloat16* A, int lda,
                    const __nv_bfloat16* W, int ldw, void* C, int ldc, int epi,
                    const float* bias, int bn, int32_t* aux) {
@@ -635,12 +738,15 @@ int gemm_bf16_plan(GemmPlan* p, int M, int N, int K, const __nv_bfloat16* A, int
   SR_REQUIRE(((uintptr_t)A & 15) == 0 && ((uintptr_t)W & 15) == 0 && ((uintptr_t)C & 15) == 0,
              "A, W, C must be 16-byte aligned");
   bool pair;
+  int mc = 1;
   if (bn == 0) {
     pair = M >= 256;
-    bn = pair ? choose_pair_bn(M, N, epi) : (N >= 4096 ? 256 : 128);
+    if (pair) choose_pair_tile(M, N, K, epi, &bn, &mc);
+    else bn = N >= 4096 ? 256 : 128;
   } else if (bn < 0) {
     pair = true;
     bn = -bn;
+    if (bn > 1024) { mc = 2; bn -= 1024; }
   } else {
     pair = false;
     SR_REQUIRE(bn == 128 || bn == 256, "single-CTA bn must be 128 or 256");
@@ -650,9 +756,18 @@ int gemm_bf16_plan(GemmPlan* p, int M, int N, int K, const __nv_bfloat16* A, int
   p->M = M; p->N = N; p->K = K; p->bn = bn; p->epi = epi; p->c = C; p->ldc = ldc; p->bias = bias;
   p->aux = aux;
   p->pair = pair;
+  p->mc = mc;
+  p->kc = (pair && K % kBK == 0 && g_pair_kc == 2) ? 2 : 1;
   p->sample = SampleArgs{nullptr, nullptr, 0u, 0.0f};
   const int mrows = M > 0 ? M : 1;
-  int rc = make_tmap_bf16(&p->a, A, (uint64_t)K, (uint64_t)mrows, (uint64_t)lda * 2, kBK, kBM);
+  if (p->kc > 1) {
+    int rc = mc == 2 ? make_tmap_bf16(&p->a, A, (uint64_t)K, (uint64_t)mrows, (uint64_t)lda * 2, kBK, kBM)
+                     : make_tmap_bf16_3d(&p->a, A, (uint64_t)K, (uint64_t)mrows, (uint64_t)lda * 2, kBM, p->kc);
+    if (rc) return rc;
+    return make_tmap_bf16_3d(&p->b, W, (uint64_t)K, (uint64_t)N, (uint64_t)ldw * 2, bn / 2, p->kc);
+  }
+  int rc = make_tmap_bf16(&p->a, A, (uint64_t)K, (uint64_t)mrows, (uint64_t)lda * 2, kBK,
+                          mc == 2 ? kBM / 2 : kBM);
   if (rc) return rc;
   return make_tmap_bf16(&p->b, W, (uint64_t)K, (uint64_t)N, (uint64_t)ldw * 2, kBK, pair ? bn / 2 : bn);
 }
@@ -679,6 +794,7 @@ __global__ void __launch_bounds__(256)
 gemm_f32_kernel(int M, int N, int K, const float* __restrict__ A, int lda,
                 const float* __restrict__ W, int ldw, float* __restrict__ C, int ldc,
                 const float* __restrict__ bias) {
+  grid_dep_sync();
   __shared__ float sa[kFK][kFT + 4];
   __shared__ float sw[kFK][kFT + 4];
   const int m0 = blockIdx.y * kFT, n0 = blockIdx.x * kFT;
@@ -739,13 +855,13 @@ int gemm_f32(int M, int N, int K, const float* A, int lda, const float* W, int l
   switch (epi) {
     case kEpiStoreBf16:
     case kEpiStoreF32:
-      gemm_f32_kernel<kEpiStoreF32><<<grid, 256, 0, stream>>>(M, N, K, A, lda, W, ldw, c, ldc, bias);
+      sr::launch_k(gemm_f32_kernel<kEpiStoreF32>, grid, 256, 0, stream, M, N, K, A, lda, W, ldw, c, ldc, bias);
       break;
     case kEpiResidualF32:
-      gemm_f32_kernel<kEpiResidualF32><<<grid, 256, 0, stream>>>(M, N, K, A, lda, W, ldw, c, ldc, bias);
+      sr::launch_k(gemm_f32_kernel<kEpiResidualF32>, grid, 256, 0, stream, M, N, K, A, lda, W, ldw, c, ldc, bias);
       break;
     case kEpiSwiGLU:
-      gemm_f32_kernel<kEpiSwiGLU><<<grid, 256, 0, stream>>>(M, N, K, A, lda, W, ldw, c, ldc, bias);
+      sr::launch_k(gemm_f32_kernel<kEpiSwiGLU>, grid, 256, 0, stream, M, N, K, A, lda, W, ldw, c, ldc, bias);
       break;
     default:
       return config_error("unknown epilogue");

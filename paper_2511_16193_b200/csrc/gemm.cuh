@@ -26,6 +26,8 @@ struct GemmPlan {
   CUtensorMap a, b;
   int M, N, K, bn, epi;
   bool pair;          // CTA-pair (cta_group::2, 256-row tiles) kernel
+  int mc;             // pairs per cluster sharing (multicasting) A: 1 | 2
+  int kc;             // 64-wide k chunks per pipeline stage (pair kernel): 1 | 2
   void* c;
   int ldc;
   const float* bias;
@@ -35,7 +37,8 @@ struct GemmPlan {
 
 // Build a plan (tensor maps) once; launch many times (graph-capturable).
 // bn > 0: single-CTA kernel with that tile width (128 | 256); bn < 0: CTA-pair
-// kernel with width -bn (multiple of 16, <= 256); bn == 0: choose from
+// kernel with width -bn (multiple of 16, <= 256), or width -bn - 1024 with
+// two pairs per cluster multicasting A (bn < -1024); bn == 0: choose from
 // (M, N, K) -- M is the plan's capacity, so the choice (and hence the
 // accumulation order) never depends on how many rows a launch carries.
 int gemm_bf16_plan(GemmPlan* plan, int M, int N, int K, const __nv_bfloat16* A, int lda,

@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(kStreamsPerBlock)
 keyed_fill_kernel(int num_streams, const uint32_t* __restrict__ words,
                   const int32_t* __restrict__ num_words, int max_words,
                   uint32_t rng, int per_stream, T* __restrict__ out) {
+  grid_dep_sync();
   const int s = blockIdx.x * kStreamsPerBlock + threadIdx.x;
   Pcg64 g;
   if (s < num_streams) {
@@ -61,7 +62,7 @@ int sr_keyed_tokens(int num_streams, const uint32_t* words, const int32_t* num_w
   if (num_streams == 0 || per_stream == 0) return SR_OK;
   SR_REQUIRE(words && num_words && out, "null pointer");
   dim3 grid(sr::ceil_div(num_streams, sr::kStreamsPerBlock));
-  sr::keyed_fill_kernel<int32_t, false><<<grid, sr::kStreamsPerBlock, 0, (cudaStream_t)stream>>>(
+  sr::launch_k(sr::keyed_fill_kernel<int32_t, false>, grid, sr::kStreamsPerBlock, 0, (cudaStream_t)stream, 
       num_streams, words, num_words, max_words, (uint32_t)(high - 1), per_stream, out);
   return sr::check_launch("keyed_fill_kernel<tokens>");
 }
@@ -73,7 +74,7 @@ int sr_keyed_uniforms(int num_streams, const uint32_t* words, const int32_t* num
   if (num_streams == 0 || per_stream == 0) return SR_OK;
   SR_REQUIRE(words && num_words && out, "null pointer");
   dim3 grid(sr::ceil_div(num_streams, sr::kStreamsPerBlock));
-  sr::keyed_fill_kernel<double, true><<<grid, sr::kStreamsPerBlock, 0, (cudaStream_t)stream>>>(
+  sr::launch_k(sr::keyed_fill_kernel<double, true>, grid, sr::kStreamsPerBlock, 0, (cudaStream_t)stream, 
       num_streams, words, num_words, max_words, 0u, per_stream, out);
   return sr::check_launch("keyed_fill_kernel<uniforms>");
 }

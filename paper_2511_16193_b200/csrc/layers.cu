@@ -17,6 +17,7 @@ template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float
 template <typename T>
 __global__ void embed_kernel(const T* __restrict__ table, const int32_t* __restrict__ ids, int H,
                              float* __restrict__ x) {
+  grid_dep_sync();
   const int row = blockIdx.x;
   const T* src = table + (int64_t)ids[row] * H;
   float* dst = x + (int64_t)row * H;
@@ -30,6 +31,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ w, int M, int H, float eps,
                T* __restrict__ out) {
+  grid_dep_sync();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -81,6 +83,7 @@ __global__ void rope_scatter_kernel(const T* __restrict__ qkv, const int32_t* __
                                     const SeqInfo* __restrict__ seqs, const float* __restrict__ cos_t,
                                     const float* __restrict__ sin_t, int nq, int layer, KvLayout kv,
                                     T* __restrict__ q_out) {
+  grid_dep_sync();
   const SeqInfo sq = seqs[blockIdx.y];
   const int j = blockIdx.x;
   if (j >= sq.q_len) return;
@@ -182,6 +185,7 @@ __device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
 __global__ void argmax_reduce_kernel(const float* __restrict__ pv, const int32_t* __restrict__ pi,
                                      int M, int tiles, int32_t* __restrict__ ids,
                                      float* __restrict__ vals) {
+  grid_dep_sync();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -206,6 +210,7 @@ __global__ void argmax_reduce_kernel(const float* __restrict__ pv, const int32_t
 
 __global__ void argmax_rows_kernel(const float* __restrict__ logits, int V, int ld,
                                    int32_t* __restrict__ ids, float* __restrict__ vals) {
+  grid_dep_sync();
   const int row = blockIdx.x;
   const float* r = logits + (int64_t)row * ld;
   float bv = -INFINITY;
@@ -248,6 +253,7 @@ __global__ void sample_rows_kernel(const float* __restrict__ logits, int V, int 
                                    const int32_t* __restrict__ req, const int32_t* __restrict__ pos,
                                    uint32_t seed, float inv_temp, int32_t* __restrict__ ids,
                                    float* __restrict__ vals) {
+  grid_dep_sync();
   const int row = blockIdx.x;
   const float* r = logits + (int64_t)row * ld;
   const int rq = req[row], ps = pos[row];
@@ -294,6 +300,7 @@ __global__ void sample_rows_kernel(const float* __restrict__ logits, int V, int 
 __global__ void row_keys_kernel(const SeqInfo* __restrict__ seqs, int S, const int32_t* __restrict__ positions,
                                 const int32_t* __restrict__ logit_rows, int R, int32_t* __restrict__ key_req,
                                 int32_t* __restrict__ key_pos) {
+  grid_dep_sync();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= R) return;
   const int t = logit_rows ? logit_rows[i] : i;
@@ -311,28 +318,28 @@ __global__ void row_keys_kernel(const SeqInfo* __restrict__ seqs, int S, const i
 int sample_rows(const float* logits, int M, int V, int ld, const int32_t* req, const int32_t* pos, uint32_t seed,
                 float inv_temp, int32_t* ids, float* vals, cudaStream_t s) {
   if (M == 0) return SR_OK;
-  sample_rows_kernel<<<M, 512, 0, s>>>(logits, V, ld, req, pos, seed, inv_temp, ids, vals);
+  sr::launch_k(sample_rows_kernel, M, 512, 0, s, logits, V, ld, req, pos, seed, inv_temp, ids, vals);
   return check_launch("sample_rows_kernel");
 }
 
 int row_keys(const SeqInfo* seqs, int S, const int32_t* positions, const int32_t* logit_rows, int R,
              int32_t* key_req, int32_t* key_pos, cudaStream_t s) {
   if (R == 0 || S == 0) return SR_OK;
-  row_keys_kernel<<<ceil_div(R, 256), 256, 0, s>>>(seqs, S, positions, logit_rows, R, key_req, key_pos);
+  sr::launch_k(row_keys_kernel, ceil_div(R, 256), 256, 0, s, seqs, S, positions, logit_rows, R, key_req, key_pos);
   return check_launch("row_keys_kernel");
 }
 
 template <typename T>
 int embed_rows(const T* table, const int32_t* ids, int M, int H, float* x, cudaStream_t s) {
   if (M == 0) return SR_OK;
-  embed_kernel<T><<<M, 256, 0, s>>>(table, ids, H, x);
+  sr::launch_k(embed_kernel<T>, M, 256, 0, s, table, ids, H, x);
   return check_launch("embed_kernel");
 }
 
 template <typename T>
 int rmsnorm_rows(const float* x, const float* w, int M, int H, float eps, T* out, cudaStream_t s) {
   if (M == 0) return SR_OK;
-  rmsnorm_kernel<T><<<ceil_div(M, 8), 256, 0, s>>>(x, w, M, H, eps, out);
+  sr::launch_k(rmsnorm_kernel<T>, ceil_div(M, 8), 256, 0, s, x, w, M, H, eps, out);
   return check_launch("rmsnorm_kernel");
 }
 
@@ -342,20 +349,20 @@ int rope_scatter(const T* qkv, const int32_t* positions, const SeqInfo* seqs, in
                  const KvLayout& kv, T* q_out, cudaStream_t s) {
   if (num_seqs == 0 || max_q_len == 0) return SR_OK;
   dim3 grid(max_q_len, num_seqs);
-  rope_scatter_kernel<T><<<grid, 128, 0, s>>>(qkv, positions, seqs, cos_t, sin_t, nq, layer, kv, q_out);
+  sr::launch_k(rope_scatter_kernel<T>, grid, 128, 0, s, qkv, positions, seqs, cos_t, sin_t, nq, layer, kv, q_out);
   return check_launch("rope_scatter_kernel");
 }
 
 int argmax_reduce(const float* pv, const int32_t* pi, int M, int tiles, int32_t* ids, float* vals,
                   cudaStream_t s) {
   if (M == 0) return SR_OK;
-  argmax_reduce_kernel<<<ceil_div(M, 8), 256, 0, s>>>(pv, pi, M, tiles, ids, vals);
+  sr::launch_k(argmax_reduce_kernel, ceil_div(M, 8), 256, 0, s, pv, pi, M, tiles, ids, vals);
   return check_launch("argmax_reduce_kernel");
 }
 
 int argmax_rows(const float* logits, int M, int V, int ld, int32_t* ids, float* vals, cudaStream_t s) {
   if (M == 0) return SR_OK;
-  argmax_rows_kernel<<<M, 512, 0, s>>>(logits, V, ld, ids, vals);
+  sr::launch_k(argmax_rows_kernel, M, 512, 0, s, logits, V, ld, ids, vals);
   return check_launch("argmax_rows_kernel");
 }
 

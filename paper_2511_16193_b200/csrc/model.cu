@@ -43,6 +43,7 @@ constexpr int kLmBn = 64;  // smallest lm_head tile width: sizes the argmax part
 
 __global__ void gather_rows_kernel(const void* __restrict__ src, const int32_t* __restrict__ rows, int H,
                                    int esize, void* __restrict__ dst) {
+  grid_dep_sync();
   const int r = blockIdx.x;
   const char* s = reinterpret_cast<const char*>(src) + (int64_t)rows[r] * H * esize;
   char* d = reinterpret_cast<char*>(dst) + (int64_t)r * H * esize;
@@ -317,7 +318,7 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
     }
     SR_TRY(sr::rmsnorm_rows<bf>(m->x, d.final_norm, M, H, d.rms_eps, (bf*)m->h, st));
     if (a->logit_rows) {
-      sr::gather_rows_kernel<<<R, 256, 0, st>>>(m->h, a->logit_rows, H, 2, m->h_sel);
+      sr::launch_k(sr::gather_rows_kernel, R, 256, 0, st, m->h, a->logit_rows, H, 2, m->h_sel);
       SR_TRY(sr::check_launch("gather_rows_kernel"));
     } else {
       SR_CHECK_CUDA(cudaMemcpyAsync(m->h_sel, m->h, (size_t)M * H * 2, cudaMemcpyDeviceToDevice, st));
@@ -357,7 +358,7 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
     }
     SR_TRY(sr::rmsnorm_rows<float>(m->x, d.final_norm, M, H, d.rms_eps, (float*)m->h, st));
     if (a->logit_rows) {
-      sr::gather_rows_kernel<<<R, 256, 0, st>>>(m->h, a->logit_rows, H, 4, m->h_sel);
+      sr::launch_k(sr::gather_rows_kernel, R, 256, 0, st, m->h, a->logit_rows, H, 4, m->h_sel);
       SR_TRY(sr::check_launch("gather_rows_kernel"));
     } else {
       SR_CHECK_CUDA(cudaMemcpyAsync(m->h_sel, m->h, (size_t)M * H * 4, cudaMemcpyDeviceToDevice, st));

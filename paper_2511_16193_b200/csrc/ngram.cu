@@ -38,6 +38,7 @@ ngram_kernel(const int32_t* __restrict__ tokens, int64_t stride, const int32_t* 
              int min_n, int max_n, int k, int32_t* __restrict__ out_draft,
              int32_t* __restrict__ out_nd, unsigned long long* __restrict__ keys,
              unsigned int* __restrict__ arrivals) {
+  grid_dep_sync();
   const int b = blockIdx.y;
   const int len = lens[b];
   const int32_t* ctx = tokens + (int64_t)b * stride;
@@ -135,7 +136,7 @@ extern "C" int sr_ngram_propose(int batch, const int32_t* tokens, int64_t stride
   dim3 grid(tiles < 8 ? tiles : 8, batch);
   auto* keys = reinterpret_cast<unsigned long long*>(scratch);
   auto* arrivals = reinterpret_cast<unsigned int*>(scratch + batch);
-  sr::ngram_kernel<<<grid, sr::kNgramThreads, 0, (cudaStream_t)stream>>>(
+  sr::launch_k(sr::ngram_kernel, grid, sr::kNgramThreads, 0, (cudaStream_t)stream, 
       tokens, stride, lens, min_n, max_n, k, out_draft, out_ndraft, keys, arrivals);
   return sr::check_launch("ngram_kernel");
 }

@@ -11,6 +11,20 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// One lane of a converged warp (elect.sync).  Issuing TMA / tcgen05 from an
+// elected lane of a converged warp keeps descriptors in uniform registers;
+// issuing from a `lane == 0` branch makes the compiler wrap every
+// UTMALDG / UTCHMMA in an ELECT + R2UR.BROADCAST loop (~50 clk each).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---- mbarrier ---------------------------------------------------------------
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -32,10 +46,10 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
       "selp.b32 %0, 1, 0, P1;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(phase), "r"(0x989680u)
+      : "r"(smem_u32(bar)), "r"(phase)
       : "memory");
   return ok != 0;
 }
@@ -228,6 +242,31 @@ __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const void* des
       "cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(crd0), "r"(crd1),
       "l"(cache_hint)
+      : "memory");
+}
+
+// 3D tiled pair load (crd0 = element within the 64-wide k chunk, crd1 =
+// row, crd2 = k chunk): one instruction stages several swizzled k chunks.
+__device__ __forceinline__ void tma_load_3d_pair(void* smem_dst, const void* desc, uint64_t* bar,
+                                                 int crd0, int crd1, int crd2, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::"
+      "cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(crd0), "r"(crd1),
+      "r"(crd2), "l"(cache_hint)
+      : "memory");
+}
+
+// Pair load multicast to the CTAs in cta_mask (same smem offset in each);
+// every destination signals the barrier of its own pair leader.
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* smem_dst, const void* desc, uint64_t* bar,
+                                                    int crd0, int crd1, uint16_t cta_mask,
+                                                    uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".cta_group::2.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(crd0), "r"(crd1),
+      "h"(cta_mask), "l"(cache_hint)
       : "memory");
 }
 

@@ -18,6 +18,7 @@ verify_windows_kernel(int W, const int32_t* __restrict__ win, int method, int M,
                       const double* __restrict__ accept_p, const int32_t* __restrict__ true_len,
                       int bonus, int32_t* __restrict__ seq, int32_t* __restrict__ high,
                       int32_t* __restrict__ out) {
+  grid_dep_sync();
   const int lane = threadIdx.x & 31;
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= W) return;
@@ -102,7 +103,7 @@ extern "C" int sr_verify_windows(int num_windows, const int32_t* win, int method
              "null pointer");
   const int warps_per_block = 8;
   dim3 grid(sr::ceil_div(num_windows, warps_per_block));
-  sr::verify_windows_kernel<<<grid, warps_per_block * 32, 0, (cudaStream_t)stream>>>(
+  sr::launch_k(sr::verify_windows_kernel, grid, warps_per_block * 32, 0, (cudaStream_t)stream, 
       num_windows, win, method, num_methods, row_stride, truth, uniforms, accept_p, true_len,
       bonus_token, seq, high, out);
   return sr::check_launch("verify_windows_kernel");

@@ -107,7 +107,15 @@ def test_f32_gemm(M, N, K):
 
 PAIR_CASES = [(1280, 1536, 1536, -112), (1280, 2048, 1536, -160), (300, 1000, 192, -112),
               (77, 512, 8960, -128), (1280, 17920, 1536, -256), (513, 3000, 640, -96),
-              (256, 4096, 256, -224), (1000, 768, 896, -64), (1280, 1536, 8960, -192)]
+              (256, 4096, 256, -224), (1000, 768, 896, -64), (1280, 1536, 8960, -192),
+              # two pairs per cluster, A multicast (-(1024 + width)); odd tile counts included
+              (1280, 1536, 8960, -1152), (1280, 2048, 1536, -1184), (300, 1000, 192, -1136),
+              (77, 512, 8960, -1152), (1280, 17920, 1536, -1280), (1000, 768, 896, -1088)]
+
+
+def tile_width(bn):
+    w = -bn if bn < 0 else bn
+    return w - 1024 if w > 1024 else w
 
 
 @pytest.mark.parametrize("M,N,K,bn", PAIR_CASES)
@@ -127,13 +135,13 @@ def test_bf16_pair_kernel(M, N, K, bn):
     C = R.clone()
     sr_gemm(A, W, C, EPI_RESID, None, bn)
     torch.testing.assert_close(C, R + ref(A, W), rtol=1e-4, atol=1e-3)
-    if N % 32 == 0 and (-bn) % 32 == 0:
+    if N % 32 == 0 and tile_width(bn) % 32 == 0:
         S = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
         sr_gemm(A, W, S, EPI_SWIGLU, None, bn)
         torch.testing.assert_close(S.float(), swiglu_ref(ref(A, W)), rtol=1e-2, atol=1e-2)
 
 
-@pytest.mark.parametrize("bn", [-256, -112, 128, 256])
+@pytest.mark.parametrize("bn", [-256, -112, 128, 256, -1280, -1136])
 def test_argmax_epilogue(bn):
     from paper_2511_16193_b200 import _native
 
@@ -142,7 +150,7 @@ def test_argmax_epilogue(bn):
     g = torch.Generator(device="cuda").manual_seed(11)
     A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
     W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
-    width = -bn if bn < 0 else bn
+    width = tile_width(bn)
     tiles = (N + width - 1) // width
     pv = torch.empty(M, tiles, device="cuda")
     pi = torch.empty(M, tiles, device="cuda", dtype=torch.int32)
@@ -157,13 +165,18 @@ def test_argmax_epilogue(bn):
     assert torch.equal(best.values, logits.max(1).values)
 
 
-def test_pair_batch_invariance():
+@pytest.mark.parametrize("bn", [-112, -1152])
+def test_pair_batch_invariance(bn):
     g = torch.Generator(device="cuda").manual_seed(5)
     A = torch.randn(1280, 1536, device="cuda", generator=g).bfloat16()
     W = (torch.randn(1536, 1536, device="cuda", generator=g) * 0.05).bfloat16()
     big = torch.empty(1280, 1536, device="cuda")
-    sr_gemm(A, W, big, EPI_F32, None, -112)
+    sr_gemm(A, W, big, EPI_F32, None, bn)
     for start in (0, 5, 256, 1275):
         small = torch.empty(5, 1536, device="cuda")
-        sr_gemm(A[start:start + 5].contiguous(), W, small, EPI_F32, None, -112)
+        sr_gemm(A[start:start + 5].contiguous(), W, small, EPI_F32, None, bn)
         assert torch.equal(small, big[start:start + 5])
+    # the multicast cluster computes exactly what the single pair computes
+    other = torch.empty(1280, 1536, device="cuda")
+    sr_gemm(A, W, other, EPI_F32, None, -128 if bn == -1152 else -1136)
+    assert torch.equal(other, big)
