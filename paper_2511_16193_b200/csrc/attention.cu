@@ -32,6 +32,7 @@ namespace {
 
 constexpr int kKT = 64;          // keys per tile (= page size)
 constexpr int kRows = 32;        // query rows per CTA
+constexpr int kMaxLayers = 128;  // per-layer work-claim counters
 constexpr int kStages = 3;       // cp.async ring depth
 constexpr int kAttnThreads = 256;  // 8 warps: (m-tile, 16-key slice) pairs
 
@@ -63,6 +64,14 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+// 2^x on the SFU (ex2.approx.ftz: ~2 ulp, -inf -> +0).  Used for every
+// softmax exponent of the bf16 path, so verify and decode stay bit-identical.
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // [rows][HD] bf16 tile, 16-byte chunks XOR-swizzled by (row & 7).
 template <int HD>
 __device__ __forceinline__ uint32_t swz(int row, int chunk) {
@@ -81,7 +90,7 @@ struct AttnArgs {
   int split_tiles;     // tiles per KV split (fixed per model: batch invariance)
   __nv_bfloat16* out;  // [M, nq, HD]
   int* order;          // work items, longest first (attn_plan_kernel)
-  int* counters;       // [0] items in order, [1] work-claim counter
+  int* counters;       // [0] items in order, [1 + layer] work-claim counter of a layer
   int n_slots;         // S*nkv * qblocks * splits
 };
 
@@ -121,7 +130,7 @@ attn_bf16_kernel(AttnArgs A) {
   uint32_t gi = 0;
   for (;;) {
   __syncthreads();  // previous item fully consumed (smem reusable)
-  if (tid == 0) s_item = atomicAdd(&A.counters[1], 1);
+  if (tid == 0) s_item = atomicAdd(&A.counters[1 + A.layer], 1);
   __syncthreads();
   if (s_item >= A.counters[0]) break;
   const int packed = A.order[s_item];
@@ -281,7 +290,7 @@ attn_bf16_kernel(AttnArgs A) {
         alpha[hi] = 1.0f;
         if (mx[hi] != -INFINITY && (m_old == -INFINITY || (mx[hi] - m_old) * A.scale_log2 > 8.0f)) {
           m_ref = mx[hi];
-          alpha[hi] = m_old == -INFINITY ? 0.0f : exp2f((m_old - m_ref) * A.scale_log2);
+          alpha[hi] = m_old == -INFINITY ? 0.0f : fast_exp2((m_old - m_ref) * A.scale_log2);
           rescale = true;
         }
         m_run[hi] = m_ref;
@@ -292,7 +301,7 @@ attn_bf16_kernel(AttnArgs A) {
         for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            p[nt * 2 + c] = exp2f(fmaf(sacc[nt][hi * 2 + c], A.scale_log2, neg));
+            p[nt * 2 + c] = fast_exp2(fmaf(sacc[nt][hi * 2 + c], A.scale_log2, neg));
             rs += p[nt * 2 + c];
           }
         l_run[hi] = l_run[hi] * alpha[hi] + rs;
@@ -354,7 +363,9 @@ attn_bf16_kernel(AttnArgs A) {
   // A block whose keys fit one split finishes here: out = O / l is exactly
   // what the combine computes for a single split (weight exp2(0) = 1).
   const bool single = ntiles <= A.split_tiles;
-  float* sW = sML + 4 * kRows * 2;  // [kRows][4] warp weights, [kRows] M, [kRows] l
+  // per row: warp weights, M, l, 1/l and the output row (token * nq + head)
+  float* sW = sML + 4 * kRows * 2;  // [kRows][4] weights, [kRows] M, [kRows] l, [kRows] 1/l
+  int* sOutRow = reinterpret_cast<int*>(sW + 7 * kRows);
   if (tid < rows) {
     const int r = tid;
     float M = -INFINITY;
@@ -364,29 +375,48 @@ attn_bf16_kernel(AttnArgs A) {
     float l = 0.0f;
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      const float wt = exp2f(sML[(w * kRows + r) * 2] - Mu);
+      const float wt = fast_exp2(sML[(w * kRows + r) * 2] - Mu);
       sW[r * 4 + w] = wt;
       l += wt * sML[(w * kRows + r) * 2 + 1];
     }
     sW[4 * kRows + r] = M;
     sW[5 * kRows + r] = l;
+    sW[6 * kRows + r] = 1.0f / l;
+    const int gr = r0 + r, j = gr / G, g = gr % G;
+    sOutRow[r] = (sq.q_start + j) * A.nq + h * G + g;
   }
   __syncthreads();
-  for (int e = tid; e < rows * HD; e += kAttnThreads) {
-    const int r = e / HD, d = e % HD;
-    float acc = 0.0f;
+  // 8 consecutive head-dim elements per thread: 16-byte stores
+  for (int e = tid; e < rows * (HD / 8); e += kAttnThreads) {
+    const int r = e / (HD / 8), d0 = (e % (HD / 8)) * 8;
+    float acc[8];
 #pragma unroll
-    for (int w = 0; w < 4; ++w) acc += sW[r * 4 + w] * sO[(w * kRows + r) * OP + d];
-    const float M = sW[4 * kRows + r], l = sW[5 * kRows + r];
+    for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float wt = sW[r * 4 + w];
+      const float4 a = *reinterpret_cast<const float4*>(&sO[(w * kRows + r) * OP + d0]);
+      const float4 b = *reinterpret_cast<const float4*>(&sO[(w * kRows + r) * OP + d0 + 4]);
+      acc[0] += wt * a.x; acc[1] += wt * a.y; acc[2] += wt * a.z; acc[3] += wt * a.w;
+      acc[4] += wt * b.x; acc[5] += wt * b.y; acc[6] += wt * b.z; acc[7] += wt * b.w;
+    }
     if (single) {
-      const int gr = r0 + r, j = gr / G, g = gr % G;
-      A.out[((int64_t)(sq.q_start + j) * A.nq + h * G + g) * HD + d] = __float2bfloat16_rn(acc / l);
+      const float inv = sW[6 * kRows + r];
+      uint4 pk;
+      uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        __nv_bfloat162 v2 = __floats2bfloat162_rn(acc[2 * i] * inv, acc[2 * i + 1] * inv);
+        pw[i] = *reinterpret_cast<uint32_t*>(&v2);
+      }
+      *reinterpret_cast<uint4*>(A.out + (int64_t)sOutRow[r] * HD + d0) = pk;
       continue;
     }
-    po[r * HD + d] = acc;
-    if (d == 0) {
-      pml[r * 2] = M;
-      pml[r * 2 + 1] = l;
+    *reinterpret_cast<float4*>(&po[r * HD + d0]) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    *reinterpret_cast<float4*>(&po[r * HD + d0 + 4]) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    if (d0 == 0) {
+      pml[r * 2] = sW[4 * kRows + r];
+      pml[r * 2 + 1] = sW[5 * kRows + r];
     }
   }
   gi += (uint32_t)(t_end - t_begin);
@@ -396,7 +426,9 @@ attn_bf16_kernel(AttnArgs A) {
 // Work list of the persistent attention kernel: every non-empty (sequence x
 // kv head, query block, split) item, ordered by decreasing tile count
 // (counting sort), so the 2-per-SM persistent CTAs claim the longest items
-// first (LPT).  Processing order does not change any item's arithmetic.
+// first (LPT).  Processing order does not change any item's arithmetic.  The
+// list depends only on the sequence table, so a forward builds it once (layer
+// 0) and every layer claims from its own zeroed counter.
 __global__ void __launch_bounds__(1024) attn_plan_kernel(AttnArgs A) {
   grid_dep_sync();
   __shared__ int hist[1025];
@@ -423,8 +455,8 @@ __global__ void __launch_bounds__(1024) attn_plan_kernel(AttnArgs A) {
     int acc = 0;
     for (int t = T; t >= 1; --t) { base[t] = acc; acc += hist[t]; }
     A.counters[0] = acc;
-    A.counters[1] = 0;
   }
+  for (int i = threadIdx.x; i < kMaxLayers; i += blockDim.x) A.counters[1 + i] = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < A.n_slots; i += blockDim.x) {
     const int t = tiles_of(i);
@@ -458,12 +490,13 @@ attn_combine_kernel(AttnArgs A) {
   for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, A.part_ml[((base + sp) * kRows + r) * 2]);
   float den = 0.0f, num = 0.0f;
   for (int sp = 0; sp < nsplit; ++sp) {
-    const float w = exp2f(A.part_ml[((base + sp) * kRows + r) * 2] - M);
+    const float w = fast_exp2(A.part_ml[((base + sp) * kRows + r) * 2] - M);
     den += w * A.part_ml[((base + sp) * kRows + r) * 2 + 1];
     num += w * A.part_o[((base + sp) * kRows + r) * HD + d];
   }
   const int gr = r0 + r, j = gr / G, g = gr % G;
-  A.out[((int64_t)(sq.q_start + j) * A.nq + h * G + g) * HD + d] = __float2bfloat16_rn(num / den);
+  const float inv = 1.0f / den;  // same form as the single-split path of attn_bf16_kernel
+  A.out[((int64_t)(sq.q_start + j) * A.nq + h * G + g) * HD + d] = __float2bfloat16_rn(num * inv);
 }
 
 // fp32 parity attention: one warp per (token, q head), keys in position
@@ -513,7 +546,7 @@ __global__ void attn_f32_kernel(const float* __restrict__ q, const SeqInfo* __re
 template <int HD>
 size_t attn_smem() {
   const size_t ring = (size_t)kStages * 2 * kKT * HD * 2;
-  const size_t merge = (size_t)4 * kRows * (HD + 8 + 2) * 4 + (size_t)6 * kRows * 4;
+  const size_t merge = (size_t)4 * kRows * (HD + 8 + 2) * 4 + (size_t)8 * kRows * 4;
   return (size_t)kRows * HD * 2 + (ring > merge ? ring : merge);
 }
 
@@ -529,16 +562,17 @@ size_t attention_workspace_floats(int max_seqs, int max_tokens, int G, int kv_he
   const int qblocks = max_seqs + (max_tokens * G + kRows - 1) / kRows;
   const int splits = ceil_div(max_key / kKT + 1, 4);  // bound for any split size >= 4 tiles
   const size_t slots = (size_t)qblocks * kv_heads * splits;
-  return attention_partial_floats(1, kv_heads, qblocks, splits, hd) + (slots + 2 + 63) / 64 * 64;
+  return attention_partial_floats(1, kv_heads, qblocks, splits, hd) + (slots + 1 + kMaxLayers + 63) / 64 * 64;
 }
 
 int attention_bf16(const __nv_bfloat16* q, const SeqInfo* seqs, int num_seqs, int max_q_len, int max_key,
                    const KvLayout& kv, int layer, int nq, float* partials, size_t partial_floats,
-                   __nv_bfloat16* out, cudaStream_t stream, int phase) {
+                   __nv_bfloat16* out, cudaStream_t stream, int phase, bool plan) {
   if (num_seqs == 0) return SR_OK;
   const int hd = kv.head_dim, G = nq / kv.kv_heads;
   SR_REQUIRE(hd == 64 || hd == 128, "bf16 attention supports head_dim 64 or 128");
   SR_REQUIRE(kv.page == kKT, "paged cache page size must be 64 tokens");
+  SR_REQUIRE(layer >= 0 && layer < kMaxLayers, "attention supports at most 128 layers");
   AttnArgs a;
   a.q = q; a.seqs = seqs; a.kv = kv; a.layer = layer; a.nq = nq; a.G = G; a.out = out;
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
@@ -546,18 +580,20 @@ int attention_bf16(const __nv_bfloat16* q, const SeqInfo* seqs, int num_seqs, in
   a.split_tiles = g_split_tiles;
   a.splits = ceil_div(max_key / kKT + 1, a.split_tiles);
   a.n_slots = num_seqs * kv.kv_heads * a.qblocks * a.splits;
-  // partial workspace = [item list (n_slots + 2 ints, 256 B aligned) | O | (m, l)]
-  const size_t list_floats = ((size_t)a.n_slots + 2 + 63) / 64 * 64;
+  // partial workspace = [counters (1 + kMaxLayers) + item list (n_slots), 256 B aligned | O | (m, l)]
+  const size_t list_floats = ((size_t)a.n_slots + 1 + kMaxLayers + 63) / 64 * 64;
   const size_t need = list_floats + attention_partial_floats(num_seqs, kv.kv_heads, a.qblocks, a.splits, hd);
   SR_REQUIRE(need <= partial_floats, "attention partial workspace too small");
   a.counters = reinterpret_cast<int*>(partials);
-  a.order = a.counters + 2;
+  a.order = a.counters + 1 + kMaxLayers;
   a.part_o = partials + list_floats;
   a.part_ml = a.part_o + (size_t)num_seqs * kv.kv_heads * a.qblocks * a.splits * kRows * hd;
   if (phase == 0) {
-    sr::launch_k(attn_plan_kernel, 1, 1024, 0, stream, a);
-    int rc = check_launch("attn_plan_kernel");
-    if (rc) return rc;
+    if (plan) {
+      sr::launch_k(attn_plan_kernel, 1, 1024, 0, stream, a);
+      int rc = check_launch("attn_plan_kernel");
+      if (rc) return rc;
+    }
     // persistent: two CTAs per SM (smem/register limited), longest items first
     int sms = 0, dev = 0;
     cudaGetDevice(&dev);
@@ -630,10 +666,10 @@ extern "C" int sr_paged_attention(int dtype, const void* q, const void* seqs, in
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == 1) {
     int rc = sr::attention_bf16(reinterpret_cast<const __nv_bfloat16*>(q), sq, num_seqs, max_q_len, max_key, kv,
-                                layer, q_heads, partials, partial_floats, reinterpret_cast<__nv_bfloat16*>(out), st, 0);
+                                layer, q_heads, partials, partial_floats, reinterpret_cast<__nv_bfloat16*>(out), st, 0, true);
     if (rc) return rc;
     return sr::attention_bf16(reinterpret_cast<const __nv_bfloat16*>(q), sq, num_seqs, max_q_len, max_key, kv,
-                              layer, q_heads, partials, partial_floats, reinterpret_cast<__nv_bfloat16*>(out), st, 1);
+                              layer, q_heads, partials, partial_floats, reinterpret_cast<__nv_bfloat16*>(out), st, 1, true);
   }
   SR_REQUIRE(dtype == 0, "dtype must be 0 or 1");
   return sr::attention_f32(reinterpret_cast<const float*>(q), sq, num_seqs, max_q_len, kv, layer, q_heads,

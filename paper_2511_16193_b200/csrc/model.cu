@@ -30,7 +30,7 @@ namespace sr {
 size_t attention_workspace_floats(int max_seqs, int max_tokens, int G, int kv_heads, int max_key, int hd);
 int attention_bf16(const __nv_bfloat16* q, const SeqInfo* seqs, int num_seqs, int max_q_len, int max_key,
                    const KvLayout& kv, int layer, int nq, float* partials, size_t partial_floats,
-                   __nv_bfloat16* out, cudaStream_t stream, int phase);
+                   __nv_bfloat16* out, cudaStream_t stream, int phase, bool plan);
 int attention_f32(const float* q, const SeqInfo* seqs, int num_seqs, int max_q_len, const KvLayout& kv,
                   int layer, int nq, float* out, cudaStream_t stream);
 int kv_commit(int B, int N, const SeqInfo* seqs, const int32_t* outcome, const int32_t* bon,
@@ -297,11 +297,11 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
       P.end(st);
       P.begin(sr::kProfAttn, st);
       SR_TRY(sr::attention_bf16((const bf*)m->q, seqs, S, a->max_q_len, a->max_key, m->kv, l, d.q_heads,
-                                m->attn_part, m->partial_floats, (bf*)m->attn, st, 0));
+                                m->attn_part, m->partial_floats, (bf*)m->attn, st, 0, l == 0));
       P.end(st);
       P.begin(sr::kProfCombine, st);
       SR_TRY(sr::attention_bf16((const bf*)m->q, seqs, S, a->max_q_len, a->max_key, m->kv, l, d.q_heads,
-                                m->attn_part, m->partial_floats, (bf*)m->attn, st, 1));
+                                m->attn_part, m->partial_floats, (bf*)m->attn, st, 1, false));
       P.end(st);
       P.begin(sr::kProfO, st);
       SR_TRY(sr::gemm_bf16_launch(m->p_o[l], st, M));
