@@ -6,7 +6,9 @@ its "target token" is a keyed random integer (sim.py:313-320) -- so logits
 parity is UNPINNED by the reference; this oracle is cross-checked against
 transformers' Qwen2ForCausalLM in tests/test_oracle_model.py instead.
 
-Arithmetic (both modes): residual stream fp32; RMSNorm y = x*rsqrt(mean(x^2)+eps)*w;
+Arithmetic (both modes): residual stream fp32; RMSNorm y = x*rsqrt(mean(x^2)+eps)*w
+(bf16 mode: the GPU fuses the norm into the GEMMs, norm(x) W = r * (bf16(x*w) W),
+so the rounding point is bf16(x*w) and r scales the fp32 accumulator);
 RoPE on the NeoX halves with the shared float64->float32 cos/sin tables;
 softmax in fp32.  In "bf16" mode values are rounded to bf16 exactly where the
 GPU stores bf16: normed activations, qkv after bias, rotated q/k, softmax
@@ -56,6 +58,13 @@ class Qwen2Oracle:
         var = (x * x).mean(-1, keepdim=True)
         return self._r(x * torch.rsqrt(var + self.s.rms_eps) * w)
 
+    def _normed_proj(self, x, w, W):
+        """norm(x, w) @ W.T with the GPU's rounding points (gemm.cuh NormArgs)."""
+        if not self.bf16:
+            return self._norm(x, w) @ W.t()
+        r = torch.rsqrt((x * x).mean(-1, keepdim=True) + self.s.rms_eps)
+        return r * (self._r(x * w) @ W.t())
+
     def _rope(self, x, pos):
         half = self.s.head_dim // 2
         c, s = self.cos[pos][:, None, :], self.sin[pos][:, None, :]
@@ -73,8 +82,7 @@ class Qwen2Oracle:
         G = nq // nkv
         mask = torch.triu(torch.ones(T, T, dtype=torch.bool), 1)
         for L in self.layers:
-            h = self._norm(x, L["ln1"])
-            qkv = self._r(h @ L["wqkv"].t() + L["bqkv"])
+            qkv = self._r(self._normed_proj(x, L["ln1"], L["wqkv"]) + L["bqkv"])
             q = qkv[:, : nq * hd].view(T, nq, hd)
             k = qkv[:, nq * hd: (nq + nkv) * hd].view(T, nkv, hd)
             v = qkv[:, (nq + nkv) * hd:].view(T, nkv, hd)
@@ -88,12 +96,11 @@ class Qwen2Oracle:
             l = p.sum(-1, keepdim=True)
             o = torch.einsum("hqk,khd->qhd", self._r(p), v) / l.permute(1, 0, 2)
             x = x + self._r(o.reshape(T, nq * hd)) @ L["wo"].t()
-            h = self._norm(x, L["ln2"])
-            g, u = h @ L["wg"].t(), h @ L["wu"].t()
+            g = self._normed_proj(x, L["ln2"], L["wg"])
+            u = self._normed_proj(x, L["ln2"], L["wu"])
             act = self._r(g / (1.0 + torch.exp(-g)) * u)
             x = x + act @ L["wd"].t()
-        h = self._norm(x, self.final_norm)
-        return h @ self.lm_head.t()
+        return self._normed_proj(x, self.final_norm, self.lm_head)
 
     def greedy(self, prompt, max_new: int) -> list[int]:
         """Plain greedy decode (lowest index on ties)."""
@@ -174,8 +181,7 @@ class CachedRollout:
         G = nq // nkv
         mask = torch.ones(T, start + T, dtype=torch.bool).triu(start + 1)
         for li, L in enumerate(o.layers):
-            h = o._norm(x, L["ln1"])
-            qkv = o._r(h @ L["wqkv"].t() + L["bqkv"])
+            qkv = o._r(o._normed_proj(x, L["ln1"], L["wqkv"]) + L["bqkv"])
             q = o._rope(qkv[:, : nq * hd].view(T, nq, hd), pos)
             k = o._rope(qkv[:, nq * hd: (nq + nkv) * hd].view(T, nkv, hd), pos)
             v = qkv[:, (nq + nkv) * hd:].view(T, nkv, hd)
@@ -189,10 +195,10 @@ class CachedRollout:
             l = p.sum(-1, keepdim=True)
             att = torch.einsum("hqk,khd->qhd", o._r(p), vv) / l.permute(1, 0, 2)
             x = x + o._r(att.reshape(T, nq * hd)) @ L["wo"].t()
-            h = o._norm(x, L["ln2"])
-            g, u = h @ L["wg"].t(), h @ L["wu"].t()
+            g = o._normed_proj(x, L["ln2"], L["wg"])
+            u = o._normed_proj(x, L["ln2"], L["wu"])
             x = x + o._r(g / (1.0 + torch.exp(-g)) * u) @ L["wd"].t()
-        return o._norm(x, o.final_norm) @ o.lm_head.t()
+        return o._normed_proj(x, o.final_norm, o.lm_head)
 
     def prefill(self, prompts) -> list[list[int]]:
         seqs = []

@@ -56,7 +56,7 @@ __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g));
 // Epilogue for W (16 or 32) consecutive accumulator columns [col, col+W) of one row.
 template <int EPI, int W = 32>
 __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, int row, int col, int M, int N, void* C,
-                                               int ldc, const float* bias) {
+                                               int ldc, const float* bias, const NormArgs& na, float& ss) {
   if (row >= M) return;
   if constexpr (EPI == kEpiArgmax) return;  // handled in the tile loop
   float f[W];
@@ -104,6 +104,37 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, int row, int c
       }
     } else {
       for (int i = 0; i < W && col + i < N; ++i) out[i] += f[i];
+    }
+  } else if constexpr (EPI == kEpiResidualNorm) {
+    float* out = reinterpret_cast<float*>(C) + (int64_t)row * ldc + col;
+    __nv_bfloat16* hr = na.h_out + (int64_t)row * na.ld_h + col;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < W / 8; ++q) {
+        float4 a = reinterpret_cast<float4*>(out)[2 * q];
+        float4 b = reinterpret_cast<float4*>(out)[2 * q + 1];
+        a.x += f[8 * q]; a.y += f[8 * q + 1]; a.z += f[8 * q + 2]; a.w += f[8 * q + 3];
+        b.x += f[8 * q + 4]; b.y += f[8 * q + 5]; b.z += f[8 * q + 6]; b.w += f[8 * q + 7];
+        reinterpret_cast<float4*>(out)[2 * q] = a;
+        reinterpret_cast<float4*>(out)[2 * q + 1] = b;
+        ss = fmaf(a.x, a.x, ss); ss = fmaf(a.y, a.y, ss); ss = fmaf(a.z, a.z, ss); ss = fmaf(a.w, a.w, ss);
+        ss = fmaf(b.x, b.x, ss); ss = fmaf(b.y, b.y, ss); ss = fmaf(b.z, b.z, ss); ss = fmaf(b.w, b.w, ss);
+        const float4 wa = reinterpret_cast<const float4*>(na.w + col)[2 * q];
+        const float4 wb = reinterpret_cast<const float4*>(na.w + col)[2 * q + 1];
+        uint4 hv;
+        hv.x = pack_bf16(a.x * wa.x, a.y * wa.y);
+        hv.y = pack_bf16(a.z * wa.z, a.w * wa.w);
+        hv.z = pack_bf16(b.x * wb.x, b.y * wb.y);
+        hv.w = pack_bf16(b.z * wb.z, b.w * wb.w);
+        reinterpret_cast<uint4*>(hr)[q] = hv;
+      }
+    } else {
+      for (int i = 0; i < W && col + i < N; ++i) {
+        const float xn = out[i] + f[i];
+        out[i] = xn;
+        ss = fmaf(xn, xn, ss);
+        hr[i] = __float2bfloat16_rn(xn * na.w[col + i]);
+      }
     }
   } else if constexpr (EPI == kEpiSwiGLU) {
     static_assert(EPI != kEpiSwiGLU || W == 32, "SwiGLU pairs 16 gate + 16 up columns");
@@ -154,15 +185,31 @@ __device__ __forceinline__ void argmax_chunk(const uint32_t* v, int col, int N, 
 
 template <int EPI>
 __device__ __forceinline__ void epilogue32(const uint32_t (&v)[32], int row, int col, int M, int N, void* C,
-                                           int ldc, const float* bias) {
-  epilogue_chunk<EPI, 32>(v, row, col, M, N, C, ldc, bias);
+                                           int ldc, const float* bias, const NormArgs& na, float& ss) {
+  epilogue_chunk<EPI, 32>(v, row, col, M, N, C, ldc, bias, na, ss);
+}
+
+// Consumer side of the fused RMSNorm: r = rsqrt(sum of the row's partials
+// (tile order) / H + eps), the same expression rmsnorm_kernel evaluates.
+__device__ __forceinline__ float norm_row_scale(const NormArgs& na, int row, int M) {
+  if (na.ssq_in == nullptr || row >= M) return 1.0f;
+  const float* p = na.ssq_in + (int64_t)row * na.parts_in;
+  float s = 0.0f;
+  for (int t = 0; t < na.parts_in; ++t) s += p[t];
+  return rsqrtf(s / na.hdim + na.eps);
+}
+
+template <int W>
+__device__ __forceinline__ void scale_chunk(uint32_t* v, float r) {
+#pragma unroll
+  for (int i = 0; i < W; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * r);
 }
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     int M, int N, int K, void* C, int ldc, const float* __restrict__ bias,
-                    int32_t* __restrict__ aux, SampleArgs sa) {
+                    int32_t* __restrict__ aux, SampleArgs sa, NormArgs na) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -264,16 +311,19 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
       float best = -INFINITY;
       int best_idx = 0x7fffffff;
+      float ss = 0.0f;
+      const float rs = norm_row_scale(na, row, M);
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t v[32];
         sm100::tmem_ld_32x32b_x32(taddr + c * 32, v);
         sm100::tmem_ld_wait();
+        if (na.ssq_in != nullptr) scale_chunk<32>(v, rs);
         const int col = n_blk * BN + c * 32;
         if constexpr (EPI == kEpiArgmax) {
           argmax_chunk<32>(v, col, N, row, M, sa, best, best_idx);
         } else {
-          if (col < N) epilogue32<EPI>(v, row, col, M, N, C, ldc, bias);
+          if (col < N) epilogue32<EPI>(v, row, col, M, N, C, ldc, bias, na, ss);
         }
       }
       if constexpr (EPI == kEpiArgmax) {
@@ -282,6 +332,9 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           reinterpret_cast<float*>(C)[(int64_t)row * tiles_n + n_blk] = best;
           aux[(int64_t)row * tiles_n + n_blk] = best_idx;
         }
+      }
+      if constexpr (EPI == kEpiResidualNorm) {
+        if (row < M) na.ssq_out[(int64_t)row * num_n + n_blk] = ss;
       }
       sm100::tc_fence_before();
       sm100::mbar_arrive(&tempty[acc]);
@@ -336,7 +389,7 @@ template <int BN, int EPI, int MC, int KC>
 __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  int M, int N, int K, void* C, int ldc, const float* __restrict__ bias,
-                 int32_t* __restrict__ aux, SampleArgs sa) {
+                 int32_t* __restrict__ aux, SampleArgs sa, NormArgs na) {
   static_assert(MC == 1 || KC == 1 || KC == MC, "A multicast splits rows (KC 1) or k chunks (KC == MC)");
   using Cfg = PairCfg<BN, KC>;
   constexpr int S = Cfg::kStages;
@@ -462,7 +515,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       const int m_blk = tile % num_m, n_blk = (tile / num_m) * MC + (int)q;
       const int row = m_blk * 2 * kBM + (int)rank * kBM + quad * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
-      if constexpr (EPI == kEpiResidualF32 && BN <= 128) {
+      if constexpr ((EPI == kEpiResidualF32 || EPI == kEpiResidualNorm) && BN <= 128) {
         // Residual epilogue: the warps are idle during the mainloop, so pull
         // this row's residual slice into registers before the accumulator is
         // ready; the add + store then never waits on a global load.
@@ -478,6 +531,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
         sm100::mbar_wait(&tfull[acc], acc_phase);
         sm100::tc_fence_after();
+        float ss = 0.0f;
 #pragma unroll
         for (int c = 0; c < BN / CW; ++c) {
           uint32_t v[CW];
@@ -487,17 +541,31 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           const int col = n_blk * BN + c * CW;
           if (vec) {
 #pragma unroll
-            for (int q = 0; q < CW / 4; ++q) {
-              float4 o4;
-              o4.x = res[c * CW + 4 * q] + __uint_as_float(v[4 * q]);
-              o4.y = res[c * CW + 4 * q + 1] + __uint_as_float(v[4 * q + 1]);
-              o4.z = res[c * CW + 4 * q + 2] + __uint_as_float(v[4 * q + 2]);
-              o4.w = res[c * CW + 4 * q + 3] + __uint_as_float(v[4 * q + 3]);
-              reinterpret_cast<float4*>(xr)[c * CW / 4 + q] = o4;
+            for (int q = 0; q < CW / 8; ++q) {
+              float xn[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) xn[i] = res[c * CW + 8 * q + i] + __uint_as_float(v[8 * q + i]);
+              reinterpret_cast<float4*>(xr)[c * CW / 4 + 2 * q] = make_float4(xn[0], xn[1], xn[2], xn[3]);
+              reinterpret_cast<float4*>(xr)[c * CW / 4 + 2 * q + 1] = make_float4(xn[4], xn[5], xn[6], xn[7]);
+              if constexpr (EPI == kEpiResidualNorm) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) ss = fmaf(xn[i], xn[i], ss);
+                const float4 wa = reinterpret_cast<const float4*>(na.w + col)[2 * q];
+                const float4 wb = reinterpret_cast<const float4*>(na.w + col)[2 * q + 1];
+                uint4 hv;
+                hv.x = pack_bf16(xn[0] * wa.x, xn[1] * wa.y);
+                hv.y = pack_bf16(xn[2] * wa.z, xn[3] * wa.w);
+                hv.z = pack_bf16(xn[4] * wb.x, xn[5] * wb.y);
+                hv.w = pack_bf16(xn[6] * wb.z, xn[7] * wb.w);
+                reinterpret_cast<uint4*>(na.h_out + (int64_t)row * na.ld_h + col)[q] = hv;
+              }
             }
           } else if (row_ok && col < N) {
-            epilogue_chunk<EPI, CW>(v, row, col, M, N, C, ldc, bias);
+            epilogue_chunk<EPI, CW>(v, row, col, M, N, C, ldc, bias, na, ss);
           }
+        }
+        if constexpr (EPI == kEpiResidualNorm) {
+          if (row_ok && n_blk < num_n) na.ssq_out[(int64_t)row * num_n + n_blk] = ss;
         }
         sm100::tc_fence_before();
         __syncwarp();
@@ -505,22 +573,28 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         continue;
       }
+      const float rs = norm_row_scale(na, row, M);
       sm100::mbar_wait(&tfull[acc], acc_phase);
       sm100::tc_fence_after();
       float best = -INFINITY;
       int best_idx = 0x7fffffff;
+      float ss = 0.0f;
 #pragma unroll 1
       for (int c = 0; c < BN / CW; ++c) {
         uint32_t v[CW];
         if constexpr (CW == 32) sm100::tmem_ld_32x32b_x32(taddr + c * CW, *reinterpret_cast<uint32_t(*)[32]>(v));
         else sm100::tmem_ld_32x32b_x16(taddr + c * CW, v);
         sm100::tmem_ld_wait();
+        if (na.ssq_in != nullptr) scale_chunk<CW>(v, rs);
         const int col = n_blk * BN + c * CW;
         if constexpr (EPI == kEpiArgmax) {
           argmax_chunk<CW>(v, col, N, row, M, sa, best, best_idx);
         } else {
-          if (col < N) epilogue_chunk<EPI, CW>(v, row, col, M, N, C, ldc, bias);
+          if (col < N) epilogue_chunk<EPI, CW>(v, row, col, M, N, C, ldc, bias, na, ss);
         }
+      }
+      if constexpr (EPI == kEpiResidualNorm) {
+        if (row < M && n_blk < num_n) na.ssq_out[(int64_t)row * num_n + n_blk] = ss;
       }
       if constexpr (EPI == kEpiArgmax) {
         if (row < M && n_blk < num_n) {
@@ -582,7 +656,8 @@ int launch_typed(const GemmPlan& p, int M, cudaStream_t stream) {
   }
   const int tiles = ((M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  sr::launch_k(kern, grid, kThreads, Cfg::kSmem, stream, p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux, p.sample);
+  sr::launch_k(kern, grid, kThreads, Cfg::kSmem, stream, p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux, p.sample,
+               p.norm);
   return check_launch("gemm_tcgen05_kernel");
 }
 
@@ -591,6 +666,7 @@ int launch_bn(const GemmPlan& p, int M, cudaStream_t stream) {
   switch (p.epi) {
     case kEpiStoreBf16: return launch_typed<BN, kEpiStoreBf16>(p, M, stream);
     case kEpiResidualF32: return launch_typed<BN, kEpiResidualF32>(p, M, stream);
+    case kEpiResidualNorm: return launch_typed<BN, kEpiResidualNorm>(p, M, stream);
     case kEpiSwiGLU: return launch_typed<BN, kEpiSwiGLU>(p, M, stream);
     case kEpiStoreF32: return launch_typed<BN, kEpiStoreF32>(p, M, stream);
     case kEpiArgmax: return launch_typed<BN, kEpiArgmax>(p, M, stream);
@@ -612,7 +688,7 @@ int launch_pair_mc(const GemmPlan& p, int M, cudaStream_t stream) {
   const int slots = num_sms() / (2 * MC);
   const int clusters = tiles < slots ? tiles : slots;
   sr::launch_k(kern, 2 * MC * clusters, kThreads, Cfg::kSmem, stream, p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux,
-                                                    p.sample);
+               p.sample, p.norm);
   return check_launch("gemm_pair_kernel");
 }
 
@@ -629,6 +705,7 @@ int launch_pair_bn(const GemmPlan& p, int M, cudaStream_t stream) {
   switch (p.epi) {
     case kEpiStoreBf16: return launch_pair_typed<BN, kEpiStoreBf16>(p, M, stream);
     case kEpiResidualF32: return launch_pair_typed<BN, kEpiResidualF32>(p, M, stream);
+    case kEpiResidualNorm: return launch_pair_typed<BN, kEpiResidualNorm>(p, M, stream);
     case kEpiStoreF32: return launch_pair_typed<BN, kEpiStoreF32>(p, M, stream);
     case kEpiArgmax: return launch_pair_typed<BN, kEpiArgmax>(p, M, stream);
     case kEpiSwiGLU:
@@ -774,6 +851,9 @@ int gemm_bf16_plan(GemmPlan* p, int M, int N, int K, const __nv_bfloat16* A, int
 
 int gemm_bf16_launch(const GemmPlan& p, cudaStream_t stream, int m_override) {
   const int M = m_override >= 0 ? m_override : p.M;
+  SR_REQUIRE(p.epi != kEpiResidualNorm ||
+                 (p.norm.h_out != nullptr && p.norm.w != nullptr && p.norm.ssq_out != nullptr && p.N % 8 == 0),
+             "residual+norm epilogue needs NormArgs (h_out, w, ssq_out) and N % 8 == 0");
   if (M == 0) return SR_OK;
   if (p.pair) return launch_pair(p, M, stream);
   return p.bn == 256 ? launch_bn<256>(p, M, stream) : launch_bn<128>(p, M, stream);
@@ -874,6 +954,8 @@ int gemm_f32(int M, int N, int K, const float* A, int lda, const float* W, int l
 extern "C" int sr_gemm(int dtype, int M, int N, int K, const void* A, int lda, const void* W,
                        int ldw, void* C, int ldc, int epilogue, const float* bias, int bn,
                        int32_t* aux, sr_stream_t stream) {
+  SR_REQUIRE(epilogue >= 0 && epilogue <= sr::kEpiArgmax,
+             "epilogue must be 0..4 (the fused-norm epilogue is internal to sr_model_forward)");
   if (dtype == 1) {
     sr::GemmPlan plan;
     int rc = sr::gemm_bf16_plan(&plan, M, N, K, reinterpret_cast<const __nv_bfloat16*>(A), lda,

@@ -16,6 +16,24 @@ enum GemmEpilogue : int {
   kEpiStoreF32 = 3,     // C f32 = acc (+ bias)     (logits)
   kEpiArgmax = 4,       // per (row, N tile): max value -> C f32 [M, tiles],
                         //   its lowest column index -> aux [M, tiles]
+  kEpiResidualNorm = 5, // C f32 += acc, then RMSNorm producer side (NormArgs):
+                        //   h[row, col] = bf16(C * w[col]), ssq[row, n tile] = sum C^2
+};
+
+// Fused RMSNorm.  norm(x) W = r (x o w) W with r = rsqrt(mean(x^2) + eps) per
+// row, so the residual GEMM that produces x (kEpiResidualNorm) writes
+// bf16(x o w) as the next GEMM's A operand plus per-N-tile partial sums of
+// x^2, and the consuming GEMM scales each accumulator row by r (summing the
+// partials in tile order) before its bias / SwiGLU / argmax.  No separate
+// normalization pass touches the residual stream.
+struct NormArgs {
+  const float* ssq_in = nullptr;  // consumer: [M, parts_in] (nullptr: no row scaling)
+  int parts_in = 0;
+  float hdim = 0.0f, eps = 0.0f;
+  __nv_bfloat16* h_out = nullptr;  // producer (kEpiResidualNorm): [M, ld_h]
+  const float* w = nullptr;        // norm weights [N]
+  float* ssq_out = nullptr;        // [M, N tiles of this GEMM]
+  int ld_h = 0;
 };
 
 // Host: encode a 2D bf16 tensor map (inner dim contiguous) with 128B swizzle.
@@ -33,6 +51,7 @@ struct GemmPlan {
   const float* bias;
   int32_t* aux;
   SampleArgs sample;  // argmax epilogue: keyed Gumbel sampling when inv_temp > 0
+  NormArgs norm;      // fused RMSNorm (consumer scaling / producer outputs)
 };
 
 // Build a plan (tensor maps) once; launch many times (graph-capturable).

@@ -329,6 +329,36 @@ int row_keys(const SeqInfo* seqs, int S, const int32_t* positions, const int32_t
   return check_launch("row_keys_kernel");
 }
 
+// Producer side of the fused RMSNorm for rows that do not come out of a
+// residual GEMM (the embedding): h = bf16(x o w), ssq[row] = {sum x^2, 0, ...}
+// over `parts` slots, the layout the consuming GEMM sums (gemm.cuh NormArgs).
+__global__ void __launch_bounds__(256)
+norm_prep_kernel(const float* __restrict__ x, const float* __restrict__ w, int M, int H, int parts,
+                 __nv_bfloat16* __restrict__ h, float* __restrict__ ssq) {
+  grid_dep_sync();
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float* xr = x + (int64_t)row * H;
+  __nv_bfloat16* hr = h + (int64_t)row * H;
+  float ss = 0.0f;
+  for (int i = lane; i < H; i += 32) {
+    const float v = xr[i];
+    ss = fmaf(v, v, ss);
+    hr[i] = __float2bfloat16_rn(v * w[i]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  for (int t = lane; t < parts; t += 32) ssq[(int64_t)row * parts + t] = t == 0 ? ss : 0.0f;
+}
+
+int norm_prep_rows(const float* x, const float* w, int M, int H, int parts, __nv_bfloat16* h, float* ssq,
+                   cudaStream_t s) {
+  if (M == 0) return SR_OK;
+  sr::launch_k(norm_prep_kernel, ceil_div(M, 8), 256, 0, s, x, w, M, H, parts, h, ssq);
+  return check_launch("norm_prep_kernel");
+}
+
 template <typename T>
 int embed_rows(const T* table, const int32_t* ids, int M, int H, float* x, cudaStream_t s) {
   if (M == 0) return SR_OK;

@@ -128,9 +128,13 @@ struct Model {
   float* attn_part;
   int32_t* key_req;    // sampling keys of the lm_head rows
   int32_t* key_pos;
-  // plans (bf16)
+  float* ssq;          // fused RMSNorm partial sums of x^2 [T, parts] (bf16 path)
+  float* ssq_sel;      // the same for the gathered lm_head rows
+  int prep_parts;      // slots the embedding-side norm prep writes (= qkv[0]'s consumer count)
+  int lm_parts;        // partial slots behind the lm_head rows (last down's N tiles)
+  // plans (bf16); *_sel read the gathered rows (h_sel, ssq_sel)
   std::vector<GemmPlan> p_qkv, p_o, p_gu, p_down;
-  GemmPlan p_lm_argmax, p_lm_logits;
+  GemmPlan p_lm_argmax, p_lm_logits, p_lm_argmax_sel, p_lm_logits_sel;
 };
 
 static size_t carve(const sr_model_desc& d, Model* m, char* base) {
@@ -155,10 +159,14 @@ static size_t carve(const sr_model_desc& d, Model* m, char* base) {
   float* ap = c.take<float>(d.dtype == 1 ? pf : 0);
   int32_t* kr = c.take<int32_t>((size_t)T);
   int32_t* kp = c.take<int32_t>((size_t)T);
+  const int max_parts = (H + 63) / 64;  // residual GEMM N tiles (tile width >= 64)
+  float* ssq = c.take<float>(d.dtype == 1 ? (size_t)T * max_parts : 0);
+  float* ssq_sel = c.take<float>(d.dtype == 1 ? (size_t)T * max_parts : 0);
   if (m != nullptr) {
     m->x = x; m->h = h; m->qkv = qkv; m->q = q; m->attn = attn; m->act = act; m->h_sel = h_sel;
     m->logits = logits; m->part_val = pv; m->part_idx = pi; m->attn_part = ap;
     m->key_req = kr; m->key_pos = kp;
+    m->ssq = ssq; m->ssq_sel = ssq_sel;
     m->esize = esize; m->qkv_width = qkv_w; m->lm_tiles = lm_tiles;
     m->partial_floats = d.dtype == 1 ? pf : 0;
   }
@@ -230,20 +238,54 @@ int sr_model_create(const sr_model_desc* desc, void** handle) {
       rc = sr::gemm_bf16_plan(&m->p_qkv[l], T, m->qkv_width, H, (const bf*)m->h, H, (const bf*)w[1], H,
                               m->qkv, m->qkv_width, sr::kEpiStoreBf16, (const float*)w[2], 0);
       if (!rc) rc = sr::gemm_bf16_plan(&m->p_o[l], T, H, nqd, (const bf*)m->attn, nqd, (const bf*)w[3], nqd,
-                                       m->x, H, sr::kEpiResidualF32, nullptr, 0);
+                                       m->x, H, sr::kEpiResidualNorm, nullptr, 0);
       if (!rc) rc = sr::gemm_bf16_plan(&m->p_gu[l], T, 2 * I, H, (const bf*)m->h, H, (const bf*)w[5], H,
                                        m->act, I, sr::kEpiSwiGLU, nullptr, 0);
       if (!rc) rc = sr::gemm_bf16_plan(&m->p_down[l], T, H, I, (const bf*)m->act, I, (const bf*)w[6], I,
-                                       m->x, H, sr::kEpiResidualF32, nullptr, 0);
+                                       m->x, H, sr::kEpiResidualNorm, nullptr, 0);
       if (rc) { delete m; return rc; }
     }
-    rc = sr::gemm_bf16_plan(&m->p_lm_argmax, T, d.vocab, H, (const bf*)m->h_sel, H, (const bf*)d.lm_head, H,
-                            m->part_val, m->lm_tiles, sr::kEpiArgmax, nullptr, 0, m->part_idx);
+    for (int sel = 0; sel < 2 && !rc; ++sel) {
+      const bf* a_in = (const bf*)(sel ? m->h_sel : m->h);
+      rc = sr::gemm_bf16_plan(sel ? &m->p_lm_argmax_sel : &m->p_lm_argmax, T, d.vocab, H, a_in, H,
+                              (const bf*)d.lm_head, H, m->part_val, m->lm_tiles, sr::kEpiArgmax, nullptr, 0,
+                              m->part_idx);
+      if (!rc && m->logits)
+        rc = sr::gemm_bf16_plan(sel ? &m->p_lm_logits_sel : &m->p_lm_logits, T, d.vocab, H, a_in, H,
+                                (const bf*)d.lm_head, H, m->logits, (d.vocab + 7) / 8 * 8, sr::kEpiStoreF32,
+                                nullptr, 0);
+    }
     if (!rc) m->lm_tiles = sr::gemm_num_n_tiles(d.vocab, m->p_lm_argmax.bn);
-    if (!rc && m->logits)
-      rc = sr::gemm_bf16_plan(&m->p_lm_logits, T, d.vocab, H, (const bf*)m->h_sel, H, (const bf*)d.lm_head, H,
-                              m->logits, (d.vocab + 7) / 8 * 8, sr::kEpiStoreF32, nullptr, 0);
     if (rc) { delete m; return rc; }
+    // Fused RMSNorm wiring: o / down write bf16(x o w_next) + partials; qkv /
+    // gate_up / lm_head scale rows by r from the producer's partials.
+    auto producer = [&](sr::GemmPlan& p, const float* wn) {
+      p.norm.h_out = (bf*)m->h;
+      p.norm.w = wn;
+      p.norm.ssq_out = m->ssq;
+      p.norm.ld_h = H;
+      return sr::gemm_num_n_tiles(H, p.bn);
+    };
+    auto consumer = [&](sr::GemmPlan& p, const float* ssq, int parts) {
+      p.norm.ssq_in = ssq;
+      p.norm.parts_in = parts;
+      p.norm.hdim = (float)H;
+      p.norm.eps = d.rms_eps;
+    };
+    int parts = m->prep_parts = sr::gemm_num_n_tiles(H, m->p_down[0].bn);
+    for (int l = 0; l < d.layers; ++l) {
+      const void* const* w = m->layer_ptrs.data() + (size_t)l * sr::kLayerPtrs;
+      const void* const* wn = l + 1 < d.layers ? w + sr::kLayerPtrs : nullptr;
+      consumer(m->p_qkv[l], m->ssq, parts);
+      const int po = producer(m->p_o[l], (const float*)w[4]);
+      consumer(m->p_gu[l], m->ssq, po);
+      parts = producer(m->p_down[l], wn ? (const float*)wn[0] : d.final_norm);
+    }
+    consumer(m->p_lm_argmax, m->ssq, parts);
+    consumer(m->p_lm_logits, m->ssq, parts);
+    consumer(m->p_lm_argmax_sel, m->ssq_sel, parts);
+    consumer(m->p_lm_logits_sel, m->ssq_sel, parts);
+    m->lm_parts = parts;
   }
   *handle = m;
   return SR_OK;
@@ -282,12 +324,10 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
   if (d.dtype == 1) {
     using bf = __nv_bfloat16;
     SR_TRY(sr::embed_rows<bf>((const bf*)d.embed, a->token_ids, M, H, m->x, st));
+    // input norm of layer 0; every later norm is fused into the o / down GEMMs
+    SR_TRY(sr::norm_prep_rows(m->x, (const float*)m->layer_ptrs[0], M, H, m->prep_parts, (bf*)m->h, m->ssq, st));
     for (int l = 0; l < d.layers; ++l) {
-      const void* const* w = m->layer_ptrs.data() + (size_t)l * sr::kLayerPtrs;
       auto& P = m->prof;
-      P.begin(sr::kProfOther, st);
-      SR_TRY(sr::rmsnorm_rows<bf>(m->x, (const float*)w[0], M, H, d.rms_eps, (bf*)m->h, st));
-      P.end(st);
       P.begin(sr::kProfQkv, st);
       SR_TRY(sr::gemm_bf16_launch(m->p_qkv[l], st, M));
       P.end(st);
@@ -306,9 +346,6 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
       P.begin(sr::kProfO, st);
       SR_TRY(sr::gemm_bf16_launch(m->p_o[l], st, M));
       P.end(st);
-      P.begin(sr::kProfOther, st);
-      SR_TRY(sr::rmsnorm_rows<bf>(m->x, (const float*)w[4], M, H, d.rms_eps, (bf*)m->h, st));
-      P.end(st);
       P.begin(sr::kProfGateUp, st);
       SR_TRY(sr::gemm_bf16_launch(m->p_gu[l], st, M));
       P.end(st);
@@ -316,22 +353,25 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
       SR_TRY(sr::gemm_bf16_launch(m->p_down[l], st, M));
       P.end(st);
     }
-    SR_TRY(sr::rmsnorm_rows<bf>(m->x, d.final_norm, M, H, d.rms_eps, (bf*)m->h, st));
-    if (a->logit_rows) {
+    // the last down GEMM left bf16(x o final_norm) in h and its partials in ssq
+    const bool sel = a->logit_rows != nullptr;
+    if (sel) {
       sr::launch_k(sr::gather_rows_kernel, R, 256, 0, st, m->h, a->logit_rows, H, 2, m->h_sel);
       SR_TRY(sr::check_launch("gather_rows_kernel"));
-    } else {
-      SR_CHECK_CUDA(cudaMemcpyAsync(m->h_sel, m->h, (size_t)M * H * 2, cudaMemcpyDeviceToDevice, st));
+      sr::launch_k(sr::gather_rows_kernel, R, 256, 0, st, (const void*)m->ssq, a->logit_rows, m->lm_parts, 4,
+                   (void*)m->ssq_sel);
+      SR_TRY(sr::check_launch("gather_rows_kernel"));
     }
     if (a->output == 1) {
-      SR_TRY(sr::gemm_bf16_launch(m->p_lm_logits, st, R));
+      SR_TRY(sr::gemm_bf16_launch(sel ? m->p_lm_logits_sel : m->p_lm_logits, st, R));
       const size_t vpad = (size_t)(d.vocab + 7) / 8 * 8;
       SR_CHECK_CUDA(cudaMemcpy2DAsync(a->out, (size_t)d.vocab * 4, m->logits, vpad * 4, (size_t)d.vocab * 4, R,
                                       cudaMemcpyDeviceToDevice, st));
     } else {
       m->prof.begin(sr::kProfLmHead, st);
-      m->p_lm_argmax.sample = sample;
-      SR_TRY(sr::gemm_bf16_launch(m->p_lm_argmax, st, R));
+      sr::GemmPlan& lm = sel ? m->p_lm_argmax_sel : m->p_lm_argmax;
+      lm.sample = sample;
+      SR_TRY(sr::gemm_bf16_launch(lm, st, R));
       m->prof.end(st);
       m->prof.begin(sr::kProfOther, st);
       SR_TRY(sr::argmax_reduce(m->part_val, m->part_idx, R, m->lm_tiles, (int32_t*)a->out, a->out_val, st));
