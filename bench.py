@@ -24,6 +24,7 @@ import argparse
 import ctypes
 import json
 import os
+import re
 import statistics
 import subprocess
 import sys
@@ -136,7 +137,8 @@ def traffic_bytes():
     f = ROOT / "profiles" / "r01" / "ncu_step_layer0.json"
     try:
         for d in json.loads(f.read_text()):
-            if "gemm" in d["kernel"] and ", 2>" in d["kernel"]:
+            m = re.search(r"gemm_\w*kernel<(\d+), (\d+)", d["kernel"])
+            if m and m.group(2) == "2":  # epilogue 2 = SwiGLU: the gate_up GEMM
                 return d["dram_read_bytes"] + d["dram_write_bytes"]
     except Exception:
         return None
@@ -342,7 +344,7 @@ def probe_ngram(RolloutEngine, NgramDrafter, model, prompts, budget, truth, step
 # -- CPU baseline (oracle port of the same path) ----------------------------------------
 
 
-def cpu_baseline(s, model, prompts, requests=2, prompt_cap=128, windows=6):
+def cpu_baseline(s, model, prompts, requests=8, prompt_cap=128, windows=24):
     """Bounded sample of the same workload through the CPU oracle port."""
     import torch
 
