@@ -75,10 +75,17 @@ class SyntheticDrafter:
 
 class ModelDrafter:
     """Small-model drafter (K5; reference methods ``draft-0.5b``/``draft-1.5b``,
-    ``scenarios.py:25-29``): k greedy decode steps of its own decoder per
-    window, with its own paged KV cache.  Each window first catches the
-    drafter's cache up on the tokens committed since the previous window
-    (``sr_draft_model_batch`` step 0), then decodes k-1 more tokens."""
+    ``scenarios.py:25-29``): k decode steps of its own decoder per window,
+    with its own paged KV cache.  Each window first catches the drafter's
+    cache up on the tokens committed since the previous window
+    (``sr_draft_model_batch`` step 0), then decodes k-1 more tokens.
+
+    Under a sampled target (engine temperature T > 0) the drafter samples
+    with the *same* keyed Gumbel noise (seed, request, position) at the same
+    T: Gumbel-coupled speculative sampling.  Every committed token is the
+    target's keyed sample, so the output equals plain sampled decoding bit
+    for bit, and a draft is accepted exactly when the two models' perturbed
+    argmaxes agree (probability -> 1 as q -> p)."""
 
     name = "model"
 
@@ -111,7 +118,8 @@ class ModelDrafter:
             if step < e.k:
                 self.m.forward(self.token_ids, self.positions, self.seqs, num_seqs=e.B,
                                max_q_len=e.k + 2, max_key=e.max_key, out=self.out,
-                               logit_rows=self.logit_rows)
+                               logit_rows=self.logit_rows, output=e._out_mode,
+                               temperature=e.temperature, seed=e.seed)
 
 
 def prefill_model(m: DeviceModel, tokens, lens) -> None:

@@ -299,6 +299,42 @@ def test_model_drafter_exactness_and_self_drafting():
     assert len(live) and (live[:, 1] == live[:, 0]).all()   # every draft accepted
 
 
+def test_model_drafter_coupled_sampling():
+    """T = 1: the drafter samples with the target's keyed Gumbel noise.  The
+    output equals plain sampled decoding bit for bit; a drafter that is the
+    target gets every draft accepted, a different one strictly fewer."""
+    from paper_2511_16193_b200.engine import ModelDrafter, RolloutEngine
+    from paper_2511_16193_b200.model import DeviceModel, init_weights
+
+    B, k, T, seed = 4, 4, 1.0, 31
+    s, w, m = make("tiny", "bf16", B=B)
+    prompts = prompts_for(s.vocab, B, 14)
+    max_new = [40, 21, 33, 9]
+    from paper_2511_16193_b200.engine import NgramDrafter
+
+    plain = RolloutEngine(m, prompts, max_new, k=0, drafters=(NgramDrafter(),), history=256,
+                          temperature=T, seed=seed)
+    plain.prefill()
+    plain.run()
+
+    def drafter(wseed):
+        d = DeviceModel(s, init_weights(s, seed=wseed), dtype="bf16", max_requests=B, max_len=512,
+                        max_tokens=512, max_seqs=B * 3)
+        return ModelDrafter(d)
+
+    rates = []
+    for wseed in (0, 7):
+        eng = RolloutEngine(m, prompts, max_new, k=k, drafters=(drafter(wseed),), history=256,
+                            temperature=T, seed=seed)
+        eng.prefill()
+        steps = eng.run()
+        assert eng.outputs() == plain.outputs()
+        rows = eng.outcome_rows(steps).reshape(-1, 4)
+        live = rows[rows[:, 0] > 0]
+        rates.append(live[:, 1].sum() / live[:, 0].sum())
+    assert rates[0] == 1.0 and rates[1] < 1.0
+
+
 def test_engine_outcomes_match_reference_coupled_golden():
     """Model-mode rollout (real tiny target, reference-acceptance drafter,
     w = k = 4, bonus off) reproduces the reference simulator's per-request
