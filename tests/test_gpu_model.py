@@ -402,3 +402,44 @@ def test_decoupled_outcomes_match_reference_golden():
         got = [tuple(int(x) for x in row) for row in rows[:, b, :] if row[0] or row[2]]
         exp = [tuple(o[5:9]) for o in rec["outcomes"] if o[0] == r.id]
         assert got == exp, f"request {r.id}"
+
+
+def test_configs2_7b_shape_bon_ngram_and_model_drafters():
+    """configs[2] widths (Qwen2.5-7B: H 3584, I 18944, 28/4 heads, G = 7), 2
+    layers: Best-of-N with n-gram + small-model (0.5B-shaped) drafters commits
+    exactly the plain greedy sequence."""
+    from paper_2511_16193_b200.engine import ModelDrafter, NgramDrafter
+    from paper_2511_16193_b200.model import DeviceModel, init_weights, shape
+
+    B = 4
+    s, w, m = make("qwen2.5-7b", "bf16", layers=2, B=B, branches=2 * B, max_len=512)
+    prompts = prompts_for(min(s.vocab, 151936), B, 6)
+    max_new = [40, 17, 29, 8]
+    plain, _ = run_engine(m, prompts, max_new, k=0)
+    ds = shape("qwen2.5-0.5b", 2)
+    d = DeviceModel(ds, init_weights(ds, seed=3), dtype="bf16", max_requests=B, max_len=512,
+                    max_tokens=512, max_seqs=B * 3)
+    bon, steps = run_engine(m, prompts, max_new, k=4,
+                            drafters=(NgramDrafter(1, 3), ModelDrafter(d), NgramDrafter(2, 4)))
+    assert bon.outputs() == plain.outputs()
+
+
+def test_configs4_32b_shape_sampled_bon4():
+    """configs[4] widths (Qwen2.5-32B: H 5120, I 27648, 40/8 heads), 1 layer,
+    T = 1 keyed sampling with Best-of-N N = 4: identical to plain sampling."""
+    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine
+
+    B = 2
+    s, w, m = make("qwen2.5-32b", "bf16", layers=1, B=2 * B, branches=3 * B, max_len=256)
+    prompts = prompts_for(s.vocab, B, 10)
+    max_new = [24, 13]
+
+    def run(k, drafters):
+        eng = RolloutEngine(m, prompts, max_new, k=k, drafters=drafters, history=128,
+                            temperature=1.0, seed=44)
+        eng.prefill()
+        eng.run()
+        return eng.outputs()
+
+    plain = run(0, (NgramDrafter(),))
+    assert run(4, (NgramDrafter(1, 3), NgramDrafter(2, 2), NgramDrafter(1, 1), NgramDrafter(3, 4))) == plain
