@@ -251,16 +251,28 @@ def run_ours(args, rank, world, dist):
     gen1 = eng.gen_len.sum()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for _ in range(args.steps):
-        eng.max_new.copy_(budget_h, non_blocking=True)          # H2D: per-step request budgets
-        seq_before = eng.seq_len.clone()
-        eng.step()
-        idx = (seq_before[:, None] + torch.arange(K + 2, device="cuda")[None, :]).clamp(max=eng.stride - 1)
-        res = torch.cat([eng.history[0], torch.gather(eng.tokens, 1, idx.long())], 1)
-        out_h.copy_(res, non_blocking=True)                     # D2H: outcomes + new tokens
-        st.synchronize()
-    e1.record(st)
+    if args.eager:
+        e0.record(st)
+        for _ in range(args.steps):
+            eng.max_new.copy_(budget_h, non_blocking=True)      # H2D: per-step request budgets
+            seq_before = eng.seq_len.clone()
+            eng.step()
+            idx = (seq_before[:, None] + torch.arange(K + 2, device="cuda")[None, :]).clamp(max=eng.stride - 1)
+            res = torch.cat([eng.history[0], torch.gather(eng.tokens, 1, idx.long())], 1)
+            out_h.copy_(res, non_blocking=True)                 # D2H: outcomes + new tokens
+            st.synchronize()
+        e1.record(st)
+    else:
+        # the public API's host-facing step: H2D budgets -> step -> D2H results,
+        # one graph per step; the host synchronizes and reads every result
+        eng.capture_io(budget_h, out_h)
+        check_sum = 0
+        e0.record(st)
+        for _ in range(args.steps):
+            eng.step_io()
+            st.synchronize()
+            check_sum += int(out_h[0, 2])                       # host reads the step's result
+        e1.record(st)
     barrier()
     e2e_ms = e0.elapsed_time(e1)
     e2e_committed = int((eng.gen_len.sum() - gen1).item())

@@ -281,6 +281,40 @@ class RolloutEngine:
             self.graph = g
         return g
 
+    def capture_io(self, budget_host: torch.Tensor, result_host: torch.Tensor):
+        """Host-facing step as one CUDA graph: H2D of the per-request budgets
+        (``budget_host``, pinned int32 [B]), the speculation step, and D2H of
+        each request's outcome row and its next k+2 token slots
+        (``result_host``, pinned int32 [B, 4 + k + 2]).  :meth:`step_io`
+        replays it; the caller synchronizes before reading ``result_host``."""
+        if self.history.shape[0] != 1:
+            raise ConfigError("graph capture needs history=0/1 (the graph writes slot 0)")
+        w = self.k + 2
+        if tuple(result_host.shape) != (self.B, 4 + w) or budget_host.numel() != self.B:
+            raise ConfigError("result_host must be [B, 4 + k + 2] and budget_host [B]")
+        self._seq_before = torch.empty_like(self.seq_len)
+        self._slots = torch.arange(w, device=self.dev, dtype=torch.int32)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            g.capture_begin()
+            self.max_new.copy_(budget_host, non_blocking=True)
+            self._seq_before.copy_(self.seq_len)
+            self._enqueue_step(0)
+            idx = (self._seq_before[:, None] + self._slots[None, :]).clamp_(max=self.stride - 1)
+            res = torch.cat([self.history[0][: self.B], torch.gather(self.tokens, 1, idx.long())], 1)
+            result_host.copy_(res, non_blocking=True)
+            g.capture_end()
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph_io = g
+        return g
+
+    def step_io(self) -> None:
+        self.graph_io.replay()
+        self.steps += 1
+
     # -- host views -------------------------------------------------------------
 
     def done(self) -> bool:

@@ -443,3 +443,37 @@ def test_configs4_32b_shape_sampled_bon4():
 
     plain = run(0, (NgramDrafter(),))
     assert run(4, (NgramDrafter(1, 3), NgramDrafter(2, 2), NgramDrafter(1, 1), NgramDrafter(3, 4))) == plain
+
+
+def test_capture_io_step_matches_graph_step():
+    """The host-facing step graph (H2D budgets -> step -> D2H results) advances
+    the rollout exactly like the plain step graph and returns each step's
+    outcome row and committed tokens."""
+    import torch
+
+    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine
+
+    B, k = 4, 4
+    s, w, m = make("tiny", "bf16", B=B)
+    prompts = prompts_for(s.vocab, B, 20)
+    max_new = [30, 30, 30, 30]
+    a = RolloutEngine(m, prompts, max_new, k=k, drafters=(NgramDrafter(),), history=1)
+    a.prefill()
+    a.capture()
+    b = RolloutEngine(m, prompts, max_new, k=k, drafters=(NgramDrafter(),), history=1)
+    b.prefill()
+    budget = torch.tensor(max_new, dtype=torch.int32).pin_memory()
+    res = torch.zeros((B, 4 + k + 2), dtype=torch.int32).pin_memory()
+    b.capture_io(budget, res)
+    for _ in range(6):
+        before = b.seq_len.clone()
+        a.step()
+        b.step_io()
+        torch.cuda.synchronize()
+        assert torch.equal(a.history[0], b.history[0])
+        assert torch.equal(res[:, :4], b.history[0][:B].cpu())
+        for r in range(B):
+            c = int(res[r, 2])
+            got = res[r, 4:4 + c].tolist()
+            assert got == b.tokens[r, int(before[r]): int(before[r]) + c].tolist()
+    assert a.outputs() == b.outputs()
