@@ -178,8 +178,10 @@ attn_bf16_kernel(AttnArgs A) {
         const __nv_bfloat16* kb = cache + ((int64_t)btab[t] * 2 * nkv + h) * psz * HD;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         sm100::mbar_arrive_expect_tx(&full[stage], 2 * kTileBytes);
-        sm100::bulk_load(k_dst, kb, kTileBytes, &full[stage]);
-        sm100::bulk_load(v_dst, kb + (int64_t)nkv * psz * HD, kTileBytes, &full[stage]);
+        // KV pages are read once per layer: evict-first keeps them from
+        // displacing the weights prefetched into L2 for the next GEMMs
+        sm100::bulk_load_hint(k_dst, kb, kTileBytes, &full[stage], sm100::kEvictFirst);
+        sm100::bulk_load_hint(v_dst, kb + (int64_t)nkv * psz * HD, kTileBytes, &full[stage], sm100::kEvictFirst);
       }
       return;
     }
