@@ -152,6 +152,18 @@ def peaks():
     return 1590.0, 1400.0, 6650.0, "fallback"
 
 
+def workload_config(args, s, world):
+    """The bench's workload description, shared by both arms."""
+    B = args.batch
+    return {"workload": f"configs[1]: {args.model}-shaped target, batch {B}/GPU, k={K}, "
+                        f"single {args.drafter} drafter, greedy exact match, bonus token",
+            "model": args.model, "layers": s.layers, "batch_per_gpu": B, "global_batch": B * world,
+            "k": K, "verify_rows_per_step": B * (K + 1), "prompt_len": "U[128,1024] (default_trace_spec)",
+            "parallelism": f"prompt-sharded x{world} (no data-path collective)",
+            "l2": "inputs larger than L2 (3.1 GB weights + paged KV per step)",
+            "cuda_graph": not args.eager}
+
+
 def run_ours(args, rank, world, dist):
     import torch
 
@@ -297,13 +309,7 @@ def run_ours(args, rank, world, dist):
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init N(0,0.02) weights; keyed-stream prompt tokens; reference trace lengths)",
-        "config": {"workload": f"configs[1]: {args.model}-shaped target, batch {B}/GPU, k={K}, "
-                               f"single {args.drafter} drafter, greedy exact match, bonus token",
-                   "model": args.model, "layers": s.layers, "batch_per_gpu": B, "global_batch": B * world,
-                   "k": K, "verify_rows_per_step": rows, "prompt_len": "U[128,1024] (default_trace_spec)",
-                   "parallelism": f"prompt-sharded x{world} (no data-path collective)",
-                   "l2": "inputs larger than L2 (3.1 GB weights + paged KV per step)",
-                   "cuda_graph": not args.eager},
+        "config": workload_config(args, s, world),
         "mean_accepted_length": accepted_mean,
         "drafter": (f"synthetic: target's greedy continuation, accepted iff reference keyed "
                     f"accept_draw u < latent_accept['{args.accept_method}'] (sim.py:322-336)"
@@ -432,7 +438,7 @@ def run_reference(args):
     return {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic", "config": {"workload": "configs[1] bounded CPU sample", "model": s.name},
+            "data": "synthetic", "config": workload_config(args, s, args.gpus),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -343,6 +343,20 @@ __device__ __forceinline__ void tma_load_3d_pair(void* smem_dst, const void* des
       : "memory");
 }
 
+// TMA tensor prefetch into L2 (no shared memory, no barrier).
+__device__ __forceinline__ void tma_prefetch_2d(const void* desc, int crd0, int crd1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(desc)),
+               "r"(crd0), "r"(crd1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const void* desc, int crd0, int crd1, int crd2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(desc)),
+               "r"(crd0), "r"(crd1), "r"(crd2)
+               : "memory");
+}
+
 // Pair load multicast to the CTAs in cta_mask (same smem offset in each);
 // every destination signals the barrier of its own pair leader.
 __device__ __forceinline__ void tma_load_2d_pair_mc(void* smem_dst, const void* desc, uint64_t* bar,
