@@ -49,10 +49,31 @@ class NcclChannel:
             w.wait()
 
 
-class DraftSide:
-    """Drafter GPU state: committed-token mirror + the in-flight window."""
+def _graph(fn):
+    """Capture ``fn`` (static-shape device work, no host syncs) into a CUDA
+    graph; returns the graph (replay() reruns ``fn`` on the same buffers)."""
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        g.capture_begin()
+        fn()
+        g.capture_end()
+    torch.cuda.current_stream().wait_stream(s)
+    return g
 
-    def __init__(self, prompts, max_new, k: int, drafter, device="cuda"):
+
+class DraftSide:
+    """Drafter GPU state: committed-token mirror + the in-flight window.
+
+    Per round: :meth:`draft` fills ``out_drafts`` / ``out_nd`` (sent to the
+    verifier), :meth:`apply` folds the verifier's decisions received into
+    ``in_verified`` / ``in_accepted`` / ``in_committed`` / ``in_ctoks``.  Both
+    are static-buffer device work, replayed from CUDA graphs after the first
+    round (``graphs=True``)."""
+
+    def __init__(self, prompts, max_new, k: int, drafter, device="cuda", graphs: bool = True):
         if isinstance(drafter, SyntheticDrafter) or isinstance(drafter, NgramDrafter):
             self.drafter = drafter
         else:
@@ -66,43 +87,55 @@ class DraftSide:
         for i, p in enumerate(prompts):
             tok[i, : len(p)] = p
         d = self.dev
+        B = self.B
         self.tokens = torch.from_numpy(tok).to(d)
         self.seq_len = torch.tensor(lens, dtype=torch.int32, device=d)
-        self.gen_len = torch.zeros(self.B, dtype=torch.int32, device=d)
+        self.gen_len = torch.zeros(B, dtype=torch.int32, device=d)
         self.max_new = torch.tensor(max_new, dtype=torch.int32, device=d)
-        self.inflight = torch.zeros(self.B, dtype=torch.int32, device=d)   # drafted tokens in flight
-        self.drafts = torch.full((self.B, k), -1, dtype=torch.int32, device=d)
-        self.nd = torch.zeros(self.B, dtype=torch.int32, device=d)
-        self.scratch = torch.zeros(2 * self.B, dtype=torch.int64, device=d)
+        self.inflight = torch.zeros(B, dtype=torch.int32, device=d)   # drafted tokens in flight
+        self.drafts = torch.full((B, k), -1, dtype=torch.int32, device=d)
+        self.nd = torch.zeros(B, dtype=torch.int32, device=d)
+        self.g0 = torch.zeros(B, dtype=torch.int32, device=d)
+        self.ctx = torch.zeros(B, dtype=torch.int32, device=d)
+        self.scratch = torch.zeros(2 * B, dtype=torch.int64, device=d)
         self.ar = torch.arange(k, device=d)
+        # round I/O (static: graph-replayable, NCCL-sendable)
+        self.out_drafts = torch.full((B, k), -1, dtype=torch.int32, device=d)
+        self.out_nd = torch.zeros(B, dtype=torch.int32, device=d)
+        self.in_verified = torch.zeros(B, dtype=torch.int32, device=d)
+        self.in_accepted = torch.zeros(B, dtype=torch.int32, device=d)
+        self.in_committed = torch.zeros(B, dtype=torch.int32, device=d)
+        self.in_ctoks = torch.zeros((B, k + 1), dtype=torch.int32, device=d)
+        self.use_graphs = graphs
+        self._g_draft = self._g_apply = None
 
-    def draft(self) -> tuple[torch.Tensor, torch.Tensor]:
-        """Next window of every request: successor of the in-flight one, or
-        fresh.  Returns (drafts [B, k], nd [B]); nd = 0 means no window."""
+    def _draft(self) -> None:
         st = _native.stream_handle()
-        g0 = self.gen_len + self.inflight                       # first drafted output position
-        ctx = self.seq_len + self.inflight                      # context incl. in-flight drafts
-        room = (self.max_new - g0).clamp(min=0)
+        self.g0.copy_(self.gen_len + self.inflight)             # first drafted output position
+        self.ctx.copy_(self.seq_len + self.inflight)            # context incl. in-flight drafts
+        room = (self.max_new - self.g0).clamp(min=0)
         if isinstance(self.drafter, SyntheticDrafter):
             d = self.drafter
             _native.check(self.lib.sr_synthetic_draft(
                 self.B, self.k, d.truth.data_ptr(), d.stride, self.max_new.data_ptr(), d.uniforms.data_ptr(),
-                d.stride, d.p.data_ptr(), g0.contiguous().data_ptr(), self._vocab, self.drafts.data_ptr(),
+                d.stride, d.p.data_ptr(), self.g0.data_ptr(), self._vocab, self.drafts.data_ptr(),
                 self.nd.data_ptr(), st), "sr_synthetic_draft")
         else:
             d = self.drafter
             _native.check(self.lib.sr_ngram_propose(
-                self.B, self.tokens.data_ptr(), self.stride, ctx.contiguous().data_ptr(), d.min_n, d.max_n, self.k,
+                self.B, self.tokens.data_ptr(), self.stride, self.ctx.data_ptr(), d.min_n, d.max_n, self.k,
                 self.drafts.data_ptr(), self.nd.data_ptr(), self.scratch.data_ptr(), st), "sr_ngram_propose")
-        self.nd = torch.minimum(self.nd, room.to(torch.int32))
+        self.nd.copy_(torch.minimum(self.nd, room.to(torch.int32)))
         # append the new window after the in-flight one (context of the next successor)
-        cols = (ctx[:, None] + self.ar[None, :]).clamp(max=self.stride - 1).long()
+        cols = (self.ctx[:, None] + self.ar[None, :]).clamp(max=self.stride - 1).long()
         keep = self.ar[None, :] < self.nd[:, None]
         self.tokens.scatter_(1, cols, torch.where(keep, self.drafts, self.tokens.gather(1, cols)))
-        return self.drafts.clone(), self.nd.clone()
+        self.out_drafts.copy_(self.drafts)
+        self.out_nd.copy_(self.nd)
 
-    def apply(self, sent_nd, verified, accepted, committed, ctoks) -> None:
-        """Fold the verifier's decisions for the windows that were in flight."""
+    def _apply(self) -> None:
+        verified = self.in_verified > 0
+        accepted, committed, ctoks = self.in_accepted, self.in_committed, self.in_ctoks
         full = verified & (accepted == self.inflight)
         part = verified & ~full
         # partial: accepted prefix + corrected token
@@ -113,37 +146,73 @@ class DraftSide:
         self.seq_len += adv
         self.gen_len += adv
         # in flight next round: the window just drafted, unless its predecessor was rejected
-        survive = ~part
-        self.inflight = torch.where(survive, sent_nd, torch.zeros_like(sent_nd))
+        self.inflight.copy_(torch.where(~part, self.out_nd, torch.zeros_like(self.out_nd)))
+
+    def draft(self) -> tuple[torch.Tensor, torch.Tensor]:
+        """Next window of every request: successor of the in-flight one, or
+        fresh.  Returns (drafts [B, k], nd [B]); nd = 0 means no window."""
+        if not self.use_graphs:
+            self._draft()
+        elif self._g_draft is None:
+            self._draft()
+            self._g_draft = _graph(self._draft)
+        else:
+            self._g_draft.replay()
+        return self.out_drafts, self.out_nd
+
+    def apply(self) -> None:
+        """Fold the verifier's decisions (``in_*``) for the windows that were in flight."""
+        if not self.use_graphs:
+            self._apply()
+        elif self._g_apply is None:
+            self._apply()
+            self._g_apply = _graph(self._apply)
+        else:
+            self._g_apply.replay()
 
     _vocab = 0
 
 
 class VerifySide:
     """Verifier GPU: the target model, the authoritative token buffer, and the
-    windows received from the drafter."""
+    windows received from the drafter (``in_drafts`` / ``in_nd``).
 
-    def __init__(self, model: DeviceModel, prompts, max_new, k: int):
+    Per round: :meth:`verify` checks the pending windows and fills the
+    decision buffers ``out_verified`` / ``out_accepted`` / ``out_committed``
+    / ``out_ctoks`` (sent to the drafter) and ``rows`` (outcome rows);
+    :meth:`receive` installs the next windows.  Both replay CUDA graphs."""
+
+    def __init__(self, model: DeviceModel, prompts, max_new, k: int, graphs: bool = True):
         from .engine import RolloutEngine
 
         self.eng = RolloutEngine(model, prompts, max_new, k=k, drafters=(NgramDrafter(),), bonus_token=False,
                                  history=1)
         self.k, self.B = k, len(prompts)
         d = self.eng.dev
-        self.pending = torch.full((self.B, k), -1, dtype=torch.int32, device=d)
-        self.pending_nd = torch.full((self.B,), -1, dtype=torch.int32, device=d)  # -1: no window
+        B = self.B
+        self.pending = torch.full((B, k), -1, dtype=torch.int32, device=d)
+        self.pending_nd = torch.full((B,), -1, dtype=torch.int32, device=d)  # -1: no window
+        self.seq_before = torch.zeros(B, dtype=torch.int32, device=d)
+        self.slots = torch.arange(k + 1, device=d)
+        self.out_verified = torch.zeros(B, dtype=torch.int32, device=d)
+        self.out_accepted = torch.zeros(B, dtype=torch.int32, device=d)
+        self.out_committed = torch.zeros(B, dtype=torch.int32, device=d)
+        self.out_ctoks = torch.zeros((B, k + 1), dtype=torch.int32, device=d)
+        self.rows = torch.zeros((B, 4), dtype=torch.int32, device=d)
+        self.in_drafts = torch.full((B, k), -1, dtype=torch.int32, device=d)
+        self.in_nd = torch.zeros(B, dtype=torch.int32, device=d)
+        self.use_graphs = graphs
+        self._g_verify = self._g_receive = None
 
     def prefill(self):
         self.eng.prefill()
 
-    def verify(self):
-        """Verify the pending windows; returns (verified mask, accepted,
-        committed, committed tokens [B, k+1], outcome rows [B, 4])."""
+    def _verify(self) -> None:
         e = self.eng
         lib, st = e.lib, _native.stream_handle()
         e.drafts[0].copy_(self.pending)
         e.ndraft[0].copy_(self.pending_nd)
-        seq_before = e.seq_len.clone()
+        self.seq_before.copy_(e.seq_len)
         _native.check(lib.sr_build_verify_batch(
             e.B, 1, e.k, e.tokens.data_ptr(), e.stride, e.seq_len.data_ptr(), e.gen_len.data_ptr(),
             e.max_new.data_ptr(), e.drafts.data_ptr(), e.ndraft.data_ptr(), e.token_ids.data_ptr(),
@@ -155,51 +224,81 @@ class VerifySide:
             e.B, 1, e.seqs.data_ptr(), e.token_ids.data_ptr(), e.target_ids.data_ptr(), e.tokens.data_ptr(),
             e.stride, e.seq_len.data_ptr(), e.gen_len.data_ptr(), e.max_new.data_ptr(), 0, out.data_ptr(),
             e.bon.data_ptr(), st), "sr_accept_commit")
-        rows = out.clone()
-        verified = e.bon >= 0
-        accepted, committed = rows[:, 1].clone(), rows[:, 2].clone()
-        cols = (seq_before[:, None] + torch.arange(self.k + 1, device=e.dev)[None, :]).clamp(max=e.stride - 1)
-        ctoks = e.tokens.gather(1, cols.long())
-        return verified, accepted, committed, ctoks, rows
+        self.rows.copy_(out[: self.B])
+        self.out_verified.copy_((e.bon >= 0).to(torch.int32))
+        self.out_accepted.copy_(self.rows[:, 1])
+        self.out_committed.copy_(self.rows[:, 2])
+        cols = (self.seq_before[:, None] + self.slots[None, :]).clamp(max=e.stride - 1)
+        self.out_ctoks.copy_(e.tokens.gather(1, cols.long()))
 
-    def receive(self, drafts, nd, verified, accepted, rows):
-        """Install the drafter's windows; successors of rejected windows are
-        dropped and charged to the rejected outcome (depth-2 waste)."""
-        full = verified & (accepted == rows[:, 0])
+    def _receive(self) -> None:
+        verified = self.out_verified > 0
+        nd = self.in_nd
+        full = verified & (self.out_accepted == self.rows[:, 0])
         part = verified & ~full
         ok = (~verified | full) & (nd > 0)
-        self.pending.copy_(drafts)
+        self.pending.copy_(self.in_drafts)
         self.pending_nd.copy_(torch.where(ok, nd, torch.full_like(nd, -1)))
-        rows[:, 3] += torch.where(part, nd, torch.zeros_like(nd))
-        return rows
+        self.rows[:, 3] += torch.where(part, nd, torch.zeros_like(nd))
+
+    def verify(self) -> None:
+        """Verify the pending windows into the ``out_*`` buffers and ``rows``."""
+        if not self.use_graphs:
+            self._verify()
+        elif self._g_verify is None:
+            self._verify()
+            self._g_verify = _graph(self._verify)
+        else:
+            self._g_verify.replay()
+
+    def receive(self) -> torch.Tensor:
+        """Install the drafter's windows (``in_*``); successors of rejected
+        windows are dropped and charged to the rejected outcome (depth-2
+        waste).  Returns the round's outcome rows (device, [B, 4])."""
+        if not self.use_graphs:
+            self._receive()
+        elif self._g_receive is None:
+            self._receive()
+            self._g_receive = _graph(self._receive)
+        else:
+            self._g_receive.replay()
+        return self.rows
 
     def done(self) -> bool:
         return self.eng.done()
 
 
-def run_local(model: DeviceModel, prompts, max_new, k: int, drafter, max_rounds: int = 100000):
+def run_local(model: DeviceModel, prompts, max_new, k: int, drafter, max_rounds: int = 100000,
+              graphs: bool = True):
     """Both roles on one GPU (tests): returns (outputs, outcome rows per round)."""
     if isinstance(drafter, SyntheticDrafter):
         DraftSide._vocab = drafter.vocab or model.s.vocab
-    D = DraftSide(prompts, max_new, k, drafter, device=model.dev)
-    V = VerifySide(model, prompts, max_new, k)
+    D = DraftSide(prompts, max_new, k, drafter, device=model.dev, graphs=graphs)
+    V = VerifySide(model, prompts, max_new, k, graphs=graphs)
     V.prefill()
     history = []
-    # round 0: draft-only (nothing in flight yet)
+    # round 0: draft-only (nothing in flight yet); the verifier's decision
+    # buffers start as "nothing verified"
     drafts, nd = D.draft()
-    V.receive(drafts, nd, torch.zeros(D.B, dtype=torch.bool, device=model.dev),
-              torch.zeros_like(nd), torch.zeros((D.B, 4), dtype=torch.int32, device=model.dev))
-    D.apply(nd, torch.zeros(D.B, dtype=torch.bool, device=model.dev), torch.zeros_like(nd),
-            torch.zeros_like(nd), torch.zeros((D.B, k + 1), dtype=torch.int32, device=model.dev))
+    V.in_drafts.copy_(drafts)
+    V.in_nd.copy_(nd)
+    V.receive()
+    D.apply()
     for _ in range(max_rounds):
         if V.done():
             break
-        verified, accepted, committed, ctoks, rows = V.verify()
+        V.verify()
         drafts, nd = D.draft()                    # concurrent with verify on two GPUs
-        rows = V.receive(drafts, nd, verified, accepted, rows)
-        D.apply(nd, verified, accepted, committed, ctoks)
-        history.append(rows.cpu().numpy())
-    return V.eng.outputs(), np.stack(history) if history else np.zeros((0, D.B, 4), np.int32)
+        V.in_drafts.copy_(drafts)
+        V.in_nd.copy_(nd)
+        for dst, src in ((D.in_verified, V.out_verified), (D.in_accepted, V.out_accepted),
+                         (D.in_committed, V.out_committed), (D.in_ctoks, V.out_ctoks)):
+            dst.copy_(src)
+        rows = V.receive()
+        D.apply()
+        history.append(rows.clone())
+    h = torch.stack(history).cpu().numpy() if history else np.zeros((0, D.B, 4), np.int32)
+    return V.eng.outputs(), h
 
 
 def pairing(world: int, drafters: int) -> dict:
@@ -211,58 +310,57 @@ def pairing(world: int, drafters: int) -> dict:
 
 
 def run_ranks(dist, rank: int, world: int, drafters: int, shards: dict, k: int, make_drafter,
-              make_model=None, max_rounds: int = 1_000_000):
+              make_model=None, max_rounds: int = 1_000_000, graphs: bool = True):
     """Decoupled rollout across ranks (one process per GPU).
 
     ``shards[v]`` = (prompts, max_new) of verifier rank v.  Drafter ranks run
     one :class:`DraftSide` per verifier they serve; verifier ranks run a
     :class:`VerifySide` on ``make_model()``.  Each round is one batched NCCL
-    isend/irecv per (drafter, verifier) pair.  Returns (outputs, outcome
+    isend/irecv per (drafter, verifier) pair on static buffers; each side's
+    per-round device work replays a CUDA graph.  Returns (outputs, outcome
     rows, rounds) on verifier ranks, (None, None, rounds) on drafter ranks.
     """
     dev = torch.device("cuda", torch.cuda.current_device())
     pairs = pairing(world, drafters)
     if rank < drafters:
         mine = [v for v, d in pairs.items() if d == rank]
-        sides = {}
+        sides, done = {}, {}
         for v in mine:
             prompts, max_new = shards[v]
             drafter = make_drafter(v)
             if isinstance(drafter, SyntheticDrafter):
                 DraftSide._vocab = drafter.vocab
-            sides[v] = DraftSide(prompts, max_new, k, drafter, device=dev)
+            sides[v] = DraftSide(prompts, max_new, k, drafter, device=dev, graphs=graphs)
+            done[v] = torch.zeros(1, dtype=torch.int32, device=dev)
         live = set(mine)
         rounds = 0
         while live and rounds < max_rounds:
             for v in sorted(live):
                 D = sides[v]
                 drafts, nd = D.draft()
-                B = D.B
-                dec = [torch.empty(B, dtype=torch.int32, device=dev) for _ in range(3)]
-                ctoks = torch.empty((B, k + 1), dtype=torch.int32, device=dev)
-                done = torch.empty(1, dtype=torch.int32, device=dev)
-                NcclChannel(dist, v).exchange([drafts, nd], dec + [ctoks, done])
-                D.apply(nd, dec[0] > 0, dec[1], dec[2], ctoks)
-                if int(done.item()):
+                NcclChannel(dist, v).exchange(
+                    [drafts, nd], [D.in_verified, D.in_accepted, D.in_committed, D.in_ctoks, done[v]])
+                D.apply()
+                if int(done[v].item()):
                     live.discard(v)
             rounds += 1
         return None, None, rounds
     prompts, max_new = shards[rank]
-    V = VerifySide(make_model(), prompts, max_new, k)
+    V = VerifySide(make_model(), prompts, max_new, k, graphs=graphs)
     V.prefill()
     peer = pairs[rank]
+    done = torch.zeros(1, dtype=torch.int32, device=dev)
     history, rounds = [], 0
     while rounds < max_rounds:
-        verified, accepted, committed, ctoks, rows = V.verify()
-        done = torch.tensor([1 if V.done() else 0], dtype=torch.int32, device=dev)
-        drafts = torch.empty((V.B, k), dtype=torch.int32, device=dev)
-        nd = torch.empty(V.B, dtype=torch.int32, device=dev)
-        NcclChannel(dist, peer).exchange([verified.to(torch.int32), accepted, committed, ctoks, done],
-                                         [drafts, nd])
-        rows = V.receive(drafts, nd, verified, accepted, rows)
+        V.verify()
+        done.fill_(1 if V.done() else 0)
+        NcclChannel(dist, peer).exchange(
+            [V.out_verified, V.out_accepted, V.out_committed, V.out_ctoks, done], [V.in_drafts, V.in_nd])
+        rows = V.receive()
         if rounds > 0:
-            history.append(rows.cpu().numpy())
+            history.append(rows.clone())
         rounds += 1
         if int(done.item()):
             break
-    return V.eng.outputs(), np.stack(history) if history else None, rounds
+    h = torch.stack(history).cpu().numpy() if history else None
+    return V.eng.outputs(), h, rounds
