@@ -198,6 +198,10 @@ class RolloutEngine:
         self.target_ids = torch.zeros(R, dtype=torch.int32, device=dev)
         self.history = torch.zeros((max(history, 1), S, 4), dtype=torch.int32, device=dev)
         self.bon = torch.zeros(self.B, dtype=torch.int32, device=dev)
+        # per-request window caps (request-level reconfiguration, reference
+        # planner.reconfigure / sim.py:445-510): one batch mixes windows
+        # 0..k; rows beyond a request's window are simply not verified
+        self.window = torch.full((self.B,), k, dtype=torch.int32, device=dev)
         self.steps = 0
         self.max_key = need - 1
         self.graph = None
@@ -236,6 +240,7 @@ class RolloutEngine:
                     self.B, self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(), d.min_n, d.max_n,
                     self.k, self.drafts[n].data_ptr(), self.ndraft[n].data_ptr(),
                     self.ngram_scratch.data_ptr(), st), "sr_ngram_propose")
+            self.ndraft.copy_(torch.minimum(self.ndraft, self.window[None, :]))
             drafts_ptr, nd_ptr = self.drafts.data_ptr(), self.ndraft.data_ptr()
         _native.check(lib.sr_build_verify_batch(
             self.B, self.N, self.k, self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(),
@@ -314,6 +319,15 @@ class RolloutEngine:
     def step_io(self) -> None:
         self.graph_io.replay()
         self.steps += 1
+
+    def set_windows(self, windows) -> None:
+        """Per-request window caps in [0, k] (0 = plain decoding for that
+        request), e.g. the windows of ``planner.reconfigure``'s request plans.
+        In place, so captured step graphs pick them up."""
+        w = torch.as_tensor(windows, dtype=torch.int32)
+        if w.shape != (self.B,) or int(w.min()) < 0 or int(w.max()) > self.k:
+            raise ConfigError(f"windows must be {self.B} values in [0, {self.k}]")
+        self.window.copy_(w.to(self.dev))
 
     # -- host views -------------------------------------------------------------
 

@@ -477,3 +477,26 @@ def test_capture_io_step_matches_graph_step():
             got = res[r, 4:4 + c].tolist()
             assert got == b.tokens[r, int(before[r]): int(before[r]) + c].tolist()
     assert a.outputs() == b.outputs()
+
+
+def test_mixed_windows_per_request():
+    """Request-level reconfiguration: one batch with per-request windows
+    0..k (0 = plain decoding) commits the plain sequence and never proposes
+    more than a request's window."""
+    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine
+
+    B, k = 5, 4
+    s, w, m = make("tiny", "bf16", B=B)
+    prompts = prompts_for(s.vocab, B, 5)
+    max_new = [40, 31, 27, 33, 19]
+    plain, _ = run_engine(m, prompts, max_new, k=0)
+    windows = [0, 1, 2, 3, 4]
+    eng = RolloutEngine(m, prompts, max_new, k=k, drafters=(NgramDrafter(),), history=256)
+    eng.set_windows(windows)
+    eng.prefill()
+    steps = eng.run()
+    assert eng.outputs() == plain.outputs()
+    rows = eng.outcome_rows(steps)
+    for b, wb in enumerate(windows):
+        assert int(rows[:, b, 0].max()) <= wb
+    assert int(rows[:, 4, 0].max()) > 0   # the k = 4 request did speculate
