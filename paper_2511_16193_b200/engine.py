@@ -124,28 +124,36 @@ class ModelDrafter:
 
 def prefill_model(m: DeviceModel, tokens, lens) -> None:
     """Chunked prompt forward writing KV for positions [0, lens[b]) of every
-    request b into ``m``'s paged cache (the logits are not needed)."""
+    request b into ``m``'s paged cache (the logits are not needed).  Prompts
+    longer than the model's ``max_tokens`` are split into pieces; a piece
+    attends to its request's earlier pieces through the cache."""
     dev = tokens.device
-    order = [b for b in range(len(lens)) if lens[b] > 0]
+    pieces = []
+    for b, L in enumerate(lens):
+        off = 0
+        while off < L:
+            n = min(m.max_tokens, L - off)
+            pieces.append((b, off, n))
+            off += n
     i = 0
-    while i < len(order):
+    while i < len(pieces):
         rows, tok_rows, pos_rows = [], [], []
-        start, max_q = 0, 0
-        while i < len(order):
-            b = order[i]
-            L = lens[b]
-            if rows and (start + L > m.max_tokens or len(rows) + 1 > m.max_prefill_seqs(max(max_q, L))):
+        start, max_q, max_key = 0, 0, 0
+        while i < len(pieces):
+            b, off, n = pieces[i]
+            if rows and (start + n > m.max_tokens or len(rows) + 1 > m.max_prefill_seqs(max(max_q, n))):
                 break
-            rows.append((start, L, b, 0, -1))
-            tok_rows.append(tokens[b, :L])
-            pos_rows.append(torch.arange(L, dtype=torch.int32, device=dev))
-            start += L
-            max_q = max(max_q, L)
+            rows.append((start, n, b, off, -1))
+            tok_rows.append(tokens[b, off:off + n])
+            pos_rows.append(torch.arange(off, off + n, dtype=torch.int32, device=dev))
+            start += n
+            max_q = max(max_q, n)
+            max_key = max(max_key, off + n - 1)
             i += 1
         lr = torch.tensor([r[0] + r[1] - 1 for r in rows], dtype=torch.int32, device=dev)
         out = torch.empty(len(rows), dtype=torch.int32, device=dev)
         m.forward(torch.cat(tok_rows), torch.cat(pos_rows), seq_table(rows, dev), num_seqs=len(rows),
-                  max_q_len=max_q, max_key=max_q - 1, out=out, logit_rows=lr)
+                  max_q_len=max_q, max_key=max_key, out=out, logit_rows=lr)
 
 
 class RolloutEngine:

@@ -1,0 +1,120 @@
+"""Request migration between rollout engines (straggler pull / tail
+rebalancing as real data movement; reference ``sim.py:546-625``
+``pull_straggler`` / ``_rebalance_tail`` and the ``scale_charge`` cost model
+``bon.py:65-72``, ``scenarios.py:84-88``, which the reference prices at 50 ms
++ 0.01 ms/token).
+
+A request's state is its token row, its lengths and budget, and the KV of
+every committed position but the last (the engine invariant) in each layer.
+The paged cache keeps a request's pages in its block-table row, so the KV
+moves as whole 64-token pages in the cache's native layout (bf16 pages keep
+their slot swizzle: same slot, same bytes).  Locally the copy is a device /
+peer copy; across ranks it is one batched NCCL send/recv over NVLink.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from .errors import ConfigError
+
+PAGE = 64
+
+
+def _pages(eng, b: int) -> int:
+    kv_len = int(eng.seq_len[b]) - 1
+    return max(0, math.ceil(kv_len / PAGE))
+
+
+def _check_compatible(src, dst) -> None:
+    a, b = src.m, dst.m
+    if (a.s.layers, a.s.kv_heads, a.s.head_dim, a.dtype_code) != (b.s.layers, b.s.kv_heads, b.s.head_dim,
+                                                                   b.dtype_code):
+        raise ConfigError("migration needs engines over the same model shape and dtype")
+    if src.k != dst.k:
+        raise ConfigError("migration needs the same window k")
+
+
+def pack_request(eng, b: int) -> dict:
+    """Gather request ``b``'s state into contiguous device tensors."""
+    n = _pages(eng, b)
+    pages = eng.m.block_table[b, :n].long()
+    L = int(eng.seq_len[b])
+    return {
+        "lens": torch.stack([eng.seq_len[b], eng.gen_len[b], eng.max_new[b],
+                             torch.tensor(n, dtype=torch.int32, device=eng.dev)]).to(torch.int32),
+        "tokens": eng.tokens[b, :L].clone(),
+        "kv": eng.m.kv_cache[:, pages].contiguous(),   # [layers, n, 2, kv_heads, 64, hd]
+    }
+
+
+def unpack_request(eng, b: int, st: dict) -> None:
+    """Install a packed request into slot ``b`` of ``eng`` (same model shape)."""
+    seq_len, gen_len, max_new, n = (int(x) for x in st["lens"].tolist())
+    if seq_len + eng.k + 2 > eng.stride or n > eng.m.pages_per_req:
+        raise ConfigError("destination slot too small for the migrated request")
+    eng.tokens[b, :seq_len].copy_(st["tokens"][:seq_len])
+    eng.seq_len[b] = seq_len
+    eng.gen_len[b] = gen_len
+    eng.max_new[b] = max_new
+    if n:
+        pages = eng.m.block_table[b, :n].long()
+        eng.m.kv_cache[:, pages] = st["kv"][:, :n].to(eng.m.kv_cache.device)
+
+
+def migrate_local(src, b_src: int, dst, b_dst: int) -> int:
+    """Move request ``b_src`` of ``src`` into slot ``b_dst`` of ``dst`` (same
+    or peer GPU); the source slot is retired (budget exhausted).  Returns the
+    bytes moved."""
+    _check_compatible(src, dst)
+    st = pack_request(src, b_src)
+    if src.dev != dst.dev:
+        st = {k: v.to(dst.dev, non_blocking=True) for k, v in st.items()}
+    unpack_request(dst, b_dst, st)
+    src.max_new[b_src] = src.gen_len[b_src]
+    return sum(v.numel() * v.element_size() for v in st.values())
+
+
+def send_requests(dist, eng, bs: list[int], peer: int) -> int:
+    """NCCL P2P: ship requests ``bs`` to rank ``peer`` (which calls
+    :func:`recv_requests` with the same count) as three messages -- a meta
+    table, all token rows, all KV pages -- and retire them here.  Returns the
+    bytes sent."""
+    sts = [pack_request(eng, b) for b in bs]
+    meta = torch.stack([st["lens"] for st in sts])
+    toks = torch.cat([st["tokens"] for st in sts])
+    kv = torch.cat([st["kv"] for st in sts], 1)
+    dist.send(meta, peer)
+    ops = [dist.P2POp(dist.isend, toks, peer)]
+    if kv.numel():
+        ops.append(dist.P2POp(dist.isend, kv.contiguous(), peer))
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
+    for b in bs:
+        eng.max_new[b] = eng.gen_len[b]
+    return meta.numel() * 4 + toks.numel() * 4 + kv.numel() * kv.element_size()
+
+
+def recv_requests(dist, eng, bs: list[int], peer: int) -> None:
+    """NCCL P2P: receive ``len(bs)`` requests from rank ``peer`` into slots ``bs``."""
+    m = eng.m
+    meta = torch.empty((len(bs), 4), dtype=torch.int32, device=eng.dev)
+    dist.recv(meta, peer)
+    lens = meta.tolist()
+    toks = torch.empty(sum(r[0] for r in lens), dtype=torch.int32, device=eng.dev)
+    npages = sum(r[3] for r in lens)
+    kv = torch.empty((m.s.layers, npages) + tuple(m.kv_cache.shape[2:]), dtype=m.kv_cache.dtype,
+                     device=eng.dev)
+    ops = [dist.P2POp(dist.irecv, toks, peer)]
+    if kv.numel():
+        ops.append(dist.P2POp(dist.irecv, kv, peer))
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
+    t0 = p0 = 0
+    for i, b in enumerate(bs):
+        seq_len, n = lens[i][0], lens[i][3]
+        unpack_request(eng, b, {"lens": meta[i], "tokens": toks[t0:t0 + seq_len], "kv": kv[:, p0:p0 + n]})
+        t0 += seq_len
+        p0 += n

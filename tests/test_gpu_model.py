@@ -500,3 +500,57 @@ def test_mixed_windows_per_request():
     for b, wb in enumerate(windows):
         assert int(rows[:, b, 0].max()) <= wb
     assert int(rows[:, 4, 0].max()) > 0   # the k = 4 request did speculate
+
+
+def test_migrate_requests_between_engines():
+    """Straggler pull / tail rebalancing as data movement: requests moved
+    mid-rollout (token row, lengths, KV pages) into other slots of another
+    engine continue to exactly the plain-decoding output."""
+    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine
+    from paper_2511_16193_b200.migrate import migrate_local
+    from paper_2511_16193_b200.model import DeviceModel
+
+    B = 4
+    s, w, m1 = make("tiny", "bf16", B=B)
+    m2 = DeviceModel(s, w, dtype="bf16", max_requests=B, max_len=512, max_tokens=512, max_seqs=B * 3)
+    prompts = prompts_for(s.vocab, B, 8)
+    max_new = [50, 41, 37, 45]
+    plain, _ = run_engine(m1, prompts, max_new, k=0)
+    src = RolloutEngine(m1, prompts, max_new, k=4, drafters=(NgramDrafter(),), history=64)
+    src.prefill()
+    for _ in range(5):
+        src.step()
+    perm = [2, 0, 3, 1]                       # source slot b -> destination slot perm[b]
+    dprompts = [None] * B
+    for b in range(B):
+        dprompts[perm[b]] = prompts[b]
+    dmax = [0] * B
+    for b in range(B):
+        dmax[perm[b]] = max_new[b]
+    dst = RolloutEngine(m2, dprompts, dmax, k=4, drafters=(NgramDrafter(),), history=64)
+    dst.prefill()
+    moved = sum(migrate_local(src, b, dst, perm[b]) for b in range(B))
+    assert moved > 0 and src.done()
+    dst.run()
+    out = dst.outputs()
+    assert [out[perm[b]] for b in range(B)] == plain.outputs()
+
+
+def test_prefill_prompts_longer_than_max_tokens():
+    """Chunked prefill: prompts longer than the model's max_tokens are split
+    into pieces; decoding afterwards matches a model that prefilled them whole."""
+    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine
+    from paper_2511_16193_b200.model import DeviceModel
+
+    B = 2
+    s, w, big = make("tiny", "bf16", B=B, max_tokens=1024)
+    small = DeviceModel(s, w, dtype="bf16", max_requests=B, max_len=512, max_tokens=64, max_seqs=B * 3)
+    prompts = prompts_for(s.vocab, B, 9, lo=150, hi=300)
+    max_new = [20, 17]
+    outs = []
+    for m in (big, small):
+        e = RolloutEngine(m, prompts, max_new, k=0, drafters=(NgramDrafter(),), history=1)
+        e.prefill()
+        e.run()
+        outs.append(e.outputs())
+    assert outs[0] == outs[1]
