@@ -24,6 +24,7 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 from paper_2511_16193_b200 import _native  # noqa: E402
+from paper_2511_16193_b200.artifacts import write_samples  # noqa: E402
 from paper_2511_16193_b200.costmodel import CostModel, ProfileSample, VerifyConfig, fit_affine  # noqa: E402
 from paper_2511_16193_b200.model import DeviceModel, init_weights, seq_table, shape  # noqa: E402
 from paper_2511_16193_b200.planner import search_plan, search_plan_coupled  # noqa: E402
@@ -122,6 +123,8 @@ def main():
         configs=[VerifyConfig(id=cfg_id, gpus=1, parallelism="replica")])
     Path(a.out).parent.mkdir(parents=True, exist_ok=True)
     model.save(a.out)
+    # the reference CLI's `fit` input (b,latency_ms,key), next to the model
+    write_samples(Path(a.out).with_name("costmodel_samples.csv"), [s for v in samples.values() for s in v])
     report = {"samples_ms": {k: {s.b: round(s.latency_ms, 4) for s in v} for k, v in samples.items()},
               "costmodel": str(Path(a.out).resolve().relative_to(Path(__file__).resolve().parent.parent))
               if Path(a.out).resolve().is_relative_to(Path(__file__).resolve().parent.parent) else a.out,

@@ -172,6 +172,32 @@ def gen_ngram():
     return cases
 
 
+def gen_cli_artifacts():
+    """The reference CLI's `simulate` artifacts (cli.py:473-487) for one run,
+    as SHA-256 digests of each file's bytes."""
+    import tempfile
+
+    from specrollout import cli, scenarios
+    from specrollout.sim import SimConfig, simulate
+    from specrollout.workload import gen_trace
+
+    bon = tuple(scenarios.BON_METHODS)
+    m = simulate(SimConfig(
+        trace=gen_trace(scenarios.default_trace_spec(batch=10, seed=1)), model=scenarios.default_cost_model(),
+        method=scenarios.DEFAULT_METHOD, seed=1, scale_cost=scenarios.default_scale_cost(),
+        estimator_priors=scenarios.estimator_priors(), policy="decoupled", reconfig=True, bon=True,
+        bon_methods=bon))
+    with tempfile.TemporaryDirectory() as d:
+        out = Path(d)
+        cli._write_json(out / "summary.json", cli._summary_dict(m))
+        cli._write_csv(out / "requests.csv", cli._REQUEST_HEADER, cli._request_rows(m))
+        cli._write_csv(out / "workers.csv", cli._WORKER_HEADER, cli._worker_rows(m))
+        cli._write_events(out / "events.jsonl", m.events)
+        return {"run": {"batch": 10, "trace_seed": 1, "seed": 1, "policy": "decoupled", "reconfig": True,
+                        "bon": True},
+                "sha256": {f.name: hashlib.sha256(f.read_bytes()).hexdigest() for f in sorted(out.iterdir())}}
+
+
 def main():
     sys.path.insert(0, str(REF))
     (OUT / "sim_runs.json").write_text(json.dumps(gen_sim_runs()))
@@ -179,6 +205,7 @@ def main():
     (OUT / "workload.json").write_text(json.dumps(gen_workload()))
     (OUT / "closed_forms.json").write_text(json.dumps(gen_closed_forms()))
     (OUT / "ngram_vllm.json").write_text(json.dumps(gen_ngram()))
+    (OUT / "cli_artifacts.json").write_text(json.dumps(gen_cli_artifacts(), indent=1))
     print("wrote", sorted(p.name for p in OUT.glob("*.json")))
 
 
