@@ -299,14 +299,20 @@ class RolloutEngine:
         (``budget_host``, pinned int32 [B]), the speculation step, and D2H of
         each request's outcome row and its next k+2 token slots
         (``result_host``, pinned int32 [B, 4 + k + 2]).  :meth:`step_io`
-        replays it; the caller synchronizes before reading ``result_host``."""
+        replays the latest one (or pass the returned graph); the caller waits
+        for the step (synchronize or an event recorded after the replay)
+        before reading ``result_host``.  Capturing two graphs over two result
+        buffers lets a host loop read step i while step i+1 runs."""
         if self.history.shape[0] != 1:
             raise ConfigError("graph capture needs history=0/1 (the graph writes slot 0)")
         w = self.k + 2
         if tuple(result_host.shape) != (self.B, 4 + w) or budget_host.numel() != self.B:
             raise ConfigError("result_host must be [B, 4 + k + 2] and budget_host [B]")
-        self._seq_before = torch.empty_like(self.seq_len)
-        self._slots = torch.arange(w, device=self.dev, dtype=torch.int32)
+        seq_before = torch.empty_like(self.seq_len)
+        slots = torch.arange(w, device=self.dev, dtype=torch.int32)
+        if not hasattr(self, "_io_keep"):
+            self._io_keep = []
+        self._io_keep.append((seq_before, slots))   # buffers the graph reads/writes stay alive
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()
@@ -314,9 +320,9 @@ class RolloutEngine:
         with torch.cuda.stream(s):
             g.capture_begin()
             self.max_new.copy_(budget_host, non_blocking=True)
-            self._seq_before.copy_(self.seq_len)
+            seq_before.copy_(self.seq_len)
             self._enqueue_step(0)
-            idx = (self._seq_before[:, None] + self._slots[None, :]).clamp_(max=self.stride - 1)
+            idx = (seq_before[:, None] + slots[None, :]).clamp_(max=self.stride - 1)
             res = torch.cat([self.history[0][: self.B], torch.gather(self.tokens, 1, idx.long())], 1)
             result_host.copy_(res, non_blocking=True)
             g.capture_end()
@@ -324,8 +330,8 @@ class RolloutEngine:
         self.graph_io = g
         return g
 
-    def step_io(self) -> None:
-        self.graph_io.replay()
+    def step_io(self, graph=None) -> None:
+        (graph or self.graph_io).replay()
         self.steps += 1
 
     def set_windows(self, windows) -> None:
