@@ -25,6 +25,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace sr {
 
@@ -94,7 +95,10 @@ struct AttnArgs {
   int n_slots;         // S*nkv * qblocks * splits
 };
 
-int g_split_tiles = 32;  // 2048-key splits
+int g_split_tiles = [] {  // 2048-key splits (SR_ATTN_SPLIT overrides, for tuning)
+  const char* v = getenv("SR_ATTN_SPLIT");
+  return v ? atoi(v) : 32;
+}();
 
 __device__ __forceinline__ int block_max_key(const SeqInfo& sq, int r0, int rows, int G) {
   return sq.ctx_len + (r0 + rows - 1) / G;
