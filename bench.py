@@ -397,16 +397,20 @@ def cpu_baseline(s, model, prompts, requests=8, prompt_cap=128, windows=24):
 
 def weights_to_cpu(s, model):
     """Canonical fp32 weights rebuilt from the device model (identical values)."""
+    from paper_2511_16193_b200.model import pair_deinterleave_heads
     w = {"embed": model.embed.float().cpu(), "final_norm": model.final_norm.cpu(), "layers": []}
     w["lm_head"] = w["embed"] if s.tied else model.lm_head.float().cpu()
     nq, nkv, hd, I = s.q_heads * s.head_dim, s.kv_heads * s.head_dim, s.head_dim, s.intermediate
+    def unpair(x, heads):
+        return pair_deinterleave_heads(x, heads, hd) if model.fused_rope else x
+
     for t in model.layer_tensors:
         qkv, b = t["w_qkv"].float().cpu(), t["b_qkv"].cpu()
         gu = t["w_gu"].float().cpu().view(I // 16, 2, 16, s.hidden)
         w["layers"].append({
             "ln1": t["ln1"].cpu(), "ln2": t["ln2"].cpu(),
-            "wq": qkv[:nq], "wk": qkv[nq:nq + nkv], "wv": qkv[nq + nkv:],
-            "bq": b[:nq], "bk": b[nq:nq + nkv], "bv": b[nq + nkv:],
+            "wq": unpair(qkv[:nq], s.q_heads), "wk": unpair(qkv[nq:nq + nkv], s.kv_heads), "wv": qkv[nq + nkv:],
+            "bq": unpair(b[:nq], s.q_heads), "bk": unpair(b[nq:nq + nkv], s.kv_heads), "bv": b[nq + nkv:],
             "wo": t["w_o"].float().cpu(), "wg": gu[:, 0].reshape(I, s.hidden),
             "wu": gu[:, 1].reshape(I, s.hidden), "wd": t["w_down"].float().cpu()})
     return w

@@ -140,7 +140,10 @@ int sr_gemm(int dtype, int M, int N, int K, const void* A, int lda, const void* 
  * Weights layout (device, `dtype` unless noted f32):
  *   embed, lm_head [vocab, hidden] (lm_head may alias embed); final_norm f32
  *   layer_weights: HOST array of layers*7 device pointers, per layer:
- *     ln1 f32 [hidden]; w_qkv [(q+2kv)*hd, hidden]; b_qkv f32 [(q+2kv)*hd];
+ *     ln1 f32 [hidden]; w_qkv [(q+2kv)*hd, hidden]; b_qkv f32 [(q+2kv)*hd]
+ *       (bf16: the q and k rows of w_qkv / b_qkv pair-interleaved per head,
+ *       row 2i = dim i, row 2i+1 = dim i + hd/2 -- RoPE runs in the GEMM
+ *       epilogue; needs head_dim % 32 == 0);
  *     w_o [hidden, q*hd]; ln2 f32 [hidden];
  *     w_gu [2*inter, hidden], rows interleaved per 32 (16 gate, 16 up);
  *     w_down [hidden, inter]

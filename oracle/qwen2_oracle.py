@@ -11,8 +11,9 @@ Arithmetic (both modes): residual stream fp32; RMSNorm y = x*rsqrt(mean(x^2)+eps
 so the rounding point is bf16(x*w) and r scales the fp32 accumulator);
 RoPE on the NeoX halves with the shared float64->float32 cos/sin tables;
 softmax in fp32.  In "bf16" mode values are rounded to bf16 exactly where the
-GPU stores bf16: normed activations, qkv after bias, rotated q/k, softmax
-probabilities entering P.V, attention output, SwiGLU output.  GEMMs
+GPU stores bf16: normed activations, rotated q/k and v (RoPE runs in the
+qkv GEMM epilogue on the fp32 accumulator + bias), softmax probabilities
+entering P.V, attention output, SwiGLU output.  GEMMs
 accumulate in fp32 (double in "fp32" mode for a tighter reference).
 
 Acceptance semantics for spec decoding follow sim.py:983-1042 (exact match,
@@ -82,10 +83,10 @@ class Qwen2Oracle:
         G = nq // nkv
         mask = torch.triu(torch.ones(T, T, dtype=torch.bool), 1)
         for L in self.layers:
-            qkv = self._r(self._normed_proj(x, L["ln1"], L["wqkv"]) + L["bqkv"])
+            qkv = self._normed_proj(x, L["ln1"], L["wqkv"]) + L["bqkv"]
             q = qkv[:, : nq * hd].view(T, nq, hd)
             k = qkv[:, nq * hd: (nq + nkv) * hd].view(T, nkv, hd)
-            v = qkv[:, (nq + nkv) * hd:].view(T, nkv, hd)
+            v = self._r(qkv[:, (nq + nkv) * hd:].view(T, nkv, hd))
             q, k = self._rope(q, pos), self._rope(k, pos)
             k = k.repeat_interleave(G, dim=1)
             v = v.repeat_interleave(G, dim=1)
@@ -181,10 +182,10 @@ class CachedRollout:
         G = nq // nkv
         mask = torch.ones(T, start + T, dtype=torch.bool).triu(start + 1)
         for li, L in enumerate(o.layers):
-            qkv = o._r(o._normed_proj(x, L["ln1"], L["wqkv"]) + L["bqkv"])
+            qkv = o._normed_proj(x, L["ln1"], L["wqkv"]) + L["bqkv"]
             q = o._rope(qkv[:, : nq * hd].view(T, nq, hd), pos)
             k = o._rope(qkv[:, nq * hd: (nq + nkv) * hd].view(T, nkv, hd), pos)
-            v = qkv[:, (nq + nkv) * hd:].view(T, nkv, hd)
+            v = o._r(qkv[:, (nq + nkv) * hd:].view(T, nkv, hd))
             kc = torch.cat([self.k_cache[req][li][:start], k]) if start else k
             vc = torch.cat([self.v_cache[req][li][:start], v]) if start else v
             self.k_cache[req][li], self.v_cache[req][li] = kc, vc

@@ -21,6 +21,7 @@
 // batch, which makes speculative verify and plain decode bit-identical.
 #include "common.cuh"
 #include "gemm.cuh"
+#include "layers.cuh"
 #include "sampling.cuh"
 #include "sm100.cuh"
 
@@ -54,11 +55,84 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
 
 // Epilogue for W (16 or 32) consecutive accumulator columns [col, col+W) of one row.
+// Element offset of dim d of KV row `slot` (rows [slot][hd], bf16 chunk swizzle).
+__device__ __forceinline__ int64_t kv_elem(int slot, int d, int hd) {
+  return (int64_t)slot * hd + kv_phys<__nv_bfloat16>(slot, d);
+}
+
+__device__ __forceinline__ uint4 pack8_bf16(const float* f) {
+  uint4 w;
+  w.x = pack_bf16(f[0], f[1]);
+  w.y = pack_bf16(f[2], f[3]);
+  w.z = pack_bf16(f[4], f[5]);
+  w.w = pack_bf16(f[6], f[7]);
+  return w;
+}
+
+// kEpiQkvRope for one 32-column chunk of one row (see RopeArgs).
+__device__ __forceinline__ void qkv_rope_chunk(const float* f, int row, int col, const RopeArgs& ra) {
+  const int info = ra.kv_info[row];
+  if (info < 0) return;  // padding row of the verify batch
+  const int hd = ra.hd, half = hd >> 1;
+  const int hq = ra.nq * hd, hk = ra.nkv * hd;
+  const bool win = (info >> 16) & 1;
+  const int slot = info & 0xFFFF;
+  const int rows = win ? ra.window_max : ra.page;
+  __nv_bfloat16* kbase = (win ? ra.window : ra.cache) + ra.kv_dst[row];
+  if (col < hq + hk) {
+    const int hc = col % hd, d0 = hc >> 1;  // 16 pairs (d0 + i, d0 + i + half)
+    const int pos = ra.pos[row];
+    const float4* c4 = reinterpret_cast<const float4*>(ra.cos + (int64_t)pos * half + d0);
+    const float4* s4 = reinterpret_cast<const float4*>(ra.sin + (int64_t)pos * half + d0);
+    float y1[16], y2[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 c = c4[q], s = s4[q];
+      const float cs[4] = {c.x, c.y, c.z, c.w}, sn[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = 4 * q + u;
+        const float x1 = f[2 * i], x2 = f[2 * i + 1];
+        y1[i] = x1 * cs[u] - x2 * sn[u];
+        y2[i] = x2 * cs[u] + x1 * sn[u];
+      }
+    }
+    if (col < hq) {
+      __nv_bfloat16* q = ra.q_out + ((int64_t)row * ra.nq + col / hd) * hd;
+      *reinterpret_cast<uint4*>(q + d0) = pack8_bf16(y1);
+      *reinterpret_cast<uint4*>(q + d0 + 8) = pack8_bf16(y1 + 8);
+      *reinterpret_cast<uint4*>(q + d0 + half) = pack8_bf16(y2);
+      *reinterpret_cast<uint4*>(q + d0 + half + 8) = pack8_bf16(y2 + 8);
+    } else {
+      __nv_bfloat16* k = kbase + (int64_t)((col - hq) / hd) * rows * hd;
+      *reinterpret_cast<uint4*>(k + kv_elem(slot, d0, hd)) = pack8_bf16(y1);
+      *reinterpret_cast<uint4*>(k + kv_elem(slot, d0 + 8, hd)) = pack8_bf16(y1 + 8);
+      *reinterpret_cast<uint4*>(k + kv_elem(slot, d0 + half, hd)) = pack8_bf16(y2);
+      *reinterpret_cast<uint4*>(k + kv_elem(slot, d0 + half + 8, hd)) = pack8_bf16(y2 + 8);
+    }
+    return;
+  }
+  // V: natural column order, 32 dims of one head
+  const int vc = col - hq - hk, hc = vc % hd;
+  __nv_bfloat16* vb = kbase + (int64_t)ra.nkv * rows * hd + (int64_t)(vc / hd) * rows * hd;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(vb + kv_elem(slot, hc + 8 * q, hd)) = pack8_bf16(f + 8 * q);
+}
+
 template <int EPI, int W = 32>
 __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, int row, int col, int M, int N, void* C,
-                                               int ldc, const float* bias, const NormArgs& na, float& ss) {
+                                               int ldc, const float* bias, const NormArgs& na, float& ss,
+                                               const RopeArgs& ra) {
   if (row >= M) return;
   if constexpr (EPI == kEpiArgmax) return;  // handled in the tile loop
+  if constexpr (EPI == kEpiQkvRope) {
+    static_assert(EPI != kEpiQkvRope || W == 32, "RoPE chunks are 16 pairs");
+    float f[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) f[i] = __uint_as_float(v[i]) + (bias != nullptr ? bias[col + i] : 0.0f);
+    qkv_rope_chunk(f, row, col, ra);
+    return;
+  }
   float f[W];
 #pragma unroll
   for (int i = 0; i < W; ++i) f[i] = __uint_as_float(v[i]);
@@ -185,8 +259,9 @@ __device__ __forceinline__ void argmax_chunk(const uint32_t* v, int col, int N, 
 
 template <int EPI>
 __device__ __forceinline__ void epilogue32(const uint32_t (&v)[32], int row, int col, int M, int N, void* C,
-                                           int ldc, const float* bias, const NormArgs& na, float& ss) {
-  epilogue_chunk<EPI, 32>(v, row, col, M, N, C, ldc, bias, na, ss);
+                                           int ldc, const float* bias, const NormArgs& na, float& ss,
+                                           const RopeArgs& ra) {
+  epilogue_chunk<EPI, 32>(v, row, col, M, N, C, ldc, bias, na, ss, ra);
 }
 
 // Consumer side of the fused RMSNorm: r = rsqrt(sum of the row's partials
@@ -209,7 +284,7 @@ template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     int M, int N, int K, void* C, int ldc, const float* __restrict__ bias,
-                    int32_t* __restrict__ aux, SampleArgs sa, NormArgs na) {
+                    int32_t* __restrict__ aux, SampleArgs sa, NormArgs na, RopeArgs ra) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -323,7 +398,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         if constexpr (EPI == kEpiArgmax) {
           argmax_chunk<32>(v, col, N, row, M, sa, best, best_idx);
         } else {
-          if (col < N) epilogue32<EPI>(v, row, col, M, N, C, ldc, bias, na, ss);
+          if (col < N) epilogue32<EPI>(v, row, col, M, N, C, ldc, bias, na, ss, ra);
         }
       }
       if constexpr (EPI == kEpiArgmax) {
@@ -389,7 +464,7 @@ template <int BN, int EPI, int MC, int KC>
 __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  int M, int N, int K, void* C, int ldc, const float* __restrict__ bias,
-                 int32_t* __restrict__ aux, SampleArgs sa, NormArgs na) {
+                 int32_t* __restrict__ aux, SampleArgs sa, NormArgs na, RopeArgs ra) {
   static_assert(MC == 1 || KC == 1 || KC == MC, "A multicast splits rows (KC 1) or k chunks (KC == MC)");
   using Cfg = PairCfg<BN, KC>;
   constexpr int S = Cfg::kStages;
@@ -561,7 +636,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
               }
             }
           } else if (row_ok && col < N) {
-            epilogue_chunk<EPI, CW>(v, row, col, M, N, C, ldc, bias, na, ss);
+            epilogue_chunk<EPI, CW>(v, row, col, M, N, C, ldc, bias, na, ss, ra);
           }
         }
         if constexpr (EPI == kEpiResidualNorm) {
@@ -590,7 +665,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if constexpr (EPI == kEpiArgmax) {
           argmax_chunk<CW>(v, col, N, row, M, sa, best, best_idx);
         } else {
-          if (col < N) epilogue_chunk<EPI, CW>(v, row, col, M, N, C, ldc, bias, na, ss);
+          if (col < N) epilogue_chunk<EPI, CW>(v, row, col, M, N, C, ldc, bias, na, ss, ra);
         }
       }
       if constexpr (EPI == kEpiResidualNorm) {
@@ -657,7 +732,7 @@ int launch_typed(const GemmPlan& p, int M, cudaStream_t stream) {
   const int tiles = ((M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   sr::launch_k(kern, grid, kThreads, Cfg::kSmem, stream, p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux, p.sample,
-               p.norm);
+               p.norm, p.rope);
   return check_launch("gemm_tcgen05_kernel");
 }
 
@@ -667,6 +742,7 @@ int launch_bn(const GemmPlan& p, int M, cudaStream_t stream) {
     case kEpiStoreBf16: return launch_typed<BN, kEpiStoreBf16>(p, M, stream);
     case kEpiResidualF32: return launch_typed<BN, kEpiResidualF32>(p, M, stream);
     case kEpiResidualNorm: return launch_typed<BN, kEpiResidualNorm>(p, M, stream);
+    case kEpiQkvRope: return launch_typed<BN, kEpiQkvRope>(p, M, stream);
     case kEpiSwiGLU: return launch_typed<BN, kEpiSwiGLU>(p, M, stream);
     case kEpiStoreF32: return launch_typed<BN, kEpiStoreF32>(p, M, stream);
     case kEpiArgmax: return launch_typed<BN, kEpiArgmax>(p, M, stream);
@@ -688,7 +764,7 @@ int launch_pair_mc(const GemmPlan& p, int M, cudaStream_t stream) {
   const int slots = num_sms() / (2 * MC);
   const int clusters = tiles < slots ? tiles : slots;
   sr::launch_k(kern, 2 * MC * clusters, kThreads, Cfg::kSmem, stream, p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux,
-               p.sample, p.norm);
+               p.sample, p.norm, p.rope);
   return check_launch("gemm_pair_kernel");
 }
 
@@ -706,6 +782,9 @@ int launch_pair_bn(const GemmPlan& p, int M, cudaStream_t stream) {
     case kEpiStoreBf16: return launch_pair_typed<BN, kEpiStoreBf16>(p, M, stream);
     case kEpiResidualF32: return launch_pair_typed<BN, kEpiResidualF32>(p, M, stream);
     case kEpiResidualNorm: return launch_pair_typed<BN, kEpiResidualNorm>(p, M, stream);
+    case kEpiQkvRope:
+      if constexpr (BN % 32 == 0) return launch_pair_typed<BN, kEpiQkvRope>(p, M, stream);
+      return config_error("RoPE epilogue needs a tile width that is a multiple of 32");
     case kEpiStoreF32: return launch_pair_typed<BN, kEpiStoreF32>(p, M, stream);
     case kEpiArgmax: return launch_pair_typed<BN, kEpiArgmax>(p, M, stream);
     case kEpiSwiGLU:
@@ -745,7 +824,7 @@ void choose_pair_tile(int M, int N, int K, int epi, int* bn_out, int* mc_out) {
   int best = 256;
   double best_t = 1e30;
   for (int bn : cands) {
-    if (epi == kEpiSwiGLU && bn % 32 != 0) continue;
+    if ((epi == kEpiSwiGLU || epi == kEpiQkvRope) && bn % 32 != 0) continue;
     const int tiles = num_m * ((N + bn - 1) / bn);
     const int waves = (tiles + pairs - 1) / pairs;
     const double t = waves * ((double)kb * bn + 900.0);
@@ -830,6 +909,7 @@ int gemm_bf16_plan(GemmPlan* p, int M, int N, int K, const __nv_bfloat16* A, int
   }
   if (pair) SR_REQUIRE(bn % 16 == 0 && bn >= 64 && bn <= 256, "pair bn must be a multiple of 16 in [64, 256]");
   SR_REQUIRE(epi != kEpiSwiGLU || (N % 32 == 0 && bn % 32 == 0), "SwiGLU needs N and bn multiples of 32");
+  SR_REQUIRE(epi != kEpiQkvRope || (N % 32 == 0 && bn % 32 == 0), "qkv RoPE needs N and bn multiples of 32");
   p->M = M; p->N = N; p->K = K; p->bn = bn; p->epi = epi; p->c = C; p->ldc = ldc; p->bias = bias;
   p->aux = aux;
   p->pair = pair;
@@ -854,6 +934,11 @@ int gemm_bf16_launch(const GemmPlan& p, cudaStream_t stream, int m_override) {
   SR_REQUIRE(p.epi != kEpiResidualNorm ||
                  (p.norm.h_out != nullptr && p.norm.w != nullptr && p.norm.ssq_out != nullptr && p.N % 8 == 0),
              "residual+norm epilogue needs NormArgs (h_out, w, ssq_out) and N % 8 == 0");
+  SR_REQUIRE(p.epi != kEpiQkvRope ||
+                 (p.rope.pos != nullptr && p.rope.kv_dst != nullptr && p.rope.kv_info != nullptr &&
+                  p.rope.cos != nullptr && p.rope.q_out != nullptr && p.rope.cache != nullptr &&
+                  p.rope.hd % 32 == 0 && p.N == (p.rope.nq + 2 * p.rope.nkv) * p.rope.hd),
+             "qkv RoPE epilogue needs RopeArgs and head_dim % 32 == 0");
   if (M == 0) return SR_OK;
   if (p.pair) return launch_pair(p, M, stream);
   return p.bn == 256 ? launch_bn<256>(p, M, stream) : launch_bn<128>(p, M, stream);

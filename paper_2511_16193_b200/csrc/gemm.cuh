@@ -18,6 +18,29 @@ enum GemmEpilogue : int {
                         //   its lowest column index -> aux [M, tiles]
   kEpiResidualNorm = 5, // C f32 += acc, then RMSNorm producer side (NormArgs):
                         //   h[row, col] = bf16(C * w[col]), ssq[row, n tile] = sum C^2
+  kEpiQkvRope = 6,      // qkv projection + bias, RoPE on q/k, q -> q_out, k/v -> paged KV
+                        //   cache (RopeArgs); q/k weight rows pair-interleaved (d, d + hd/2)
+};
+
+// RoPE + KV scatter fused into the qkv GEMM epilogue (kEpiQkvRope).  The q and
+// k rows of W_qkv (and the bias) are stored pair-interleaved per head --
+// output column 2i holds dim i, column 2i+1 dim i + hd/2 -- so every 32-column
+// epilogue chunk holds 16 complete rotation pairs of one head.  Per row the
+// epilogue needs the position and where the row's K/V live (a paged-cache
+// slot or a drafter-branch window slot), precomputed once per forward
+// (kv_rows): kv_dst = element offset of the row's K block (kv head 0) inside
+// this layer's cache or window, kv_info = slot | window << 16, or -1 for a
+// padding row (no writes).
+struct RopeArgs {
+  const int32_t* pos = nullptr;      // [M]
+  const int64_t* kv_dst = nullptr;   // [M]
+  const int32_t* kv_info = nullptr;  // [M]
+  const float* cos = nullptr;        // [max_pos, hd / 2]
+  const float* sin = nullptr;
+  __nv_bfloat16* q_out = nullptr;    // [M, nq, hd]
+  __nv_bfloat16* cache = nullptr;    // this layer's paged cache
+  __nv_bfloat16* window = nullptr;   // this layer's branch windows
+  int nq = 0, nkv = 0, hd = 0, page = 64, window_max = 0;
 };
 
 // Fused RMSNorm.  norm(x) W = r (x o w) W with r = rsqrt(mean(x^2) + eps) per
@@ -52,6 +75,7 @@ struct GemmPlan {
   int32_t* aux;
   SampleArgs sample;  // argmax epilogue: keyed Gumbel sampling when inv_temp > 0
   NormArgs norm;      // fused RMSNorm (consumer scaling / producer outputs)
+  RopeArgs rope;      // fused RoPE + KV scatter (kEpiQkvRope)
 };
 
 // Build a plan (tensor maps) once; launch many times (graph-capturable).

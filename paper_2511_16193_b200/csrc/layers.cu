@@ -313,7 +313,45 @@ __global__ void row_keys_kernel(const SeqInfo* __restrict__ seqs, int S, const i
   key_pos[i] = positions[t] + 1;
 }
 
+// Per-row KV destination (same addressing as rope_scatter_kernel).
+__global__ void kv_rows_kernel(const SeqInfo* __restrict__ seqs, int S, const int32_t* __restrict__ positions,
+                               int M, KvLayout kv, int64_t* __restrict__ dst, int32_t* __restrict__ info) {
+  grid_dep_sync();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= M) return;
+  int lo = 0, hi = S - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (seqs[mid].q_start <= t) lo = mid; else hi = mid - 1;
+  }
+  const SeqInfo sq = seqs[lo];
+  const int j = t - sq.q_start;
+  if (j < 0 || j >= sq.q_len) {
+    info[t] = -1;
+    dst[t] = 0;
+    return;
+  }
+  const int hd = kv.head_dim, nkv = kv.kv_heads;
+  if (sq.branch < 0) {
+    const int pos = positions[t];
+    const int page = kv.block_table[(int64_t)sq.request * kv.max_pages + pos / kv.page];
+    dst[t] = (int64_t)page * 2 * nkv * kv.page * hd;
+    info[t] = pos % kv.page;
+  } else {
+    dst[t] = (int64_t)sq.branch * 2 * nkv * kv.window_max * hd;
+    info[t] = j | (1 << 16);
+  }
+}
+
 }  // namespace
+
+int kv_rows(const SeqInfo* seqs, int S, const int32_t* positions, int M, const KvLayout& kv, int64_t* dst,
+            int32_t* info, cudaStream_t s) {
+  if (M == 0) return SR_OK;
+  if (S == 0) return config_error("kv_rows: no sequences");
+  sr::launch_k(kv_rows_kernel, ceil_div(M, 256), 256, 0, s, seqs, S, positions, M, kv, dst, info);
+  return check_launch("kv_rows_kernel");
+}
 
 int sample_rows(const float* logits, int M, int V, int ld, const int32_t* req, const int32_t* pos, uint32_t seed,
                 float inv_temp, int32_t* ids, float* vals, cudaStream_t s) {

@@ -75,6 +75,13 @@ int sample_rows(const float* logits, int M, int V, int ld, const int32_t* req, c
 int row_keys(const SeqInfo* seqs, int S, const int32_t* positions, const int32_t* logit_rows, int R,
              int32_t* key_req, int32_t* key_pos, cudaStream_t s);
 
+// KV destination of every token row for the fused qkv + RoPE epilogue
+// (gemm.cuh RopeArgs): dst[t] = element offset of the row's K block inside a
+// layer's cache / window, info[t] = slot | window << 16; rows [0, M) not in a
+// sequence get info -1.
+int kv_rows(const SeqInfo* seqs, int S, const int32_t* positions, int M, const KvLayout& kv, int64_t* dst,
+            int32_t* info, cudaStream_t s);
+
 // Full-row argmax over fp32 logits [M, V] (lowest index on ties).
 int argmax_rows(const float* logits, int M, int V, int ld, int32_t* out_ids, float* out_val,
                 cudaStream_t s);

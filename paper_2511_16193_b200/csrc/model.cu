@@ -130,6 +130,8 @@ struct Model {
   int32_t* key_pos;
   float* ssq;          // fused RMSNorm partial sums of x^2 [T, parts] (bf16 path)
   float* ssq_sel;      // the same for the gathered lm_head rows
+  int64_t* kv_dst;     // per token row: KV destination for the fused qkv + RoPE epilogue
+  int32_t* kv_info;
   int prep_parts;      // slots the embedding-side norm prep writes (= qkv[0]'s consumer count)
   int lm_parts;        // partial slots behind the lm_head rows (last down's N tiles)
   // plans (bf16); *_sel read the gathered rows (h_sel, ssq_sel)
@@ -162,11 +164,14 @@ static size_t carve(const sr_model_desc& d, Model* m, char* base) {
   const int max_parts = (H + 63) / 64;  // residual GEMM N tiles (tile width >= 64)
   float* ssq = c.take<float>(d.dtype == 1 ? (size_t)T * max_parts : 0);
   float* ssq_sel = c.take<float>(d.dtype == 1 ? (size_t)T * max_parts : 0);
+  int64_t* kv_dst = c.take<int64_t>(d.dtype == 1 ? (size_t)T : 0);
+  int32_t* kv_info = c.take<int32_t>(d.dtype == 1 ? (size_t)T : 0);
   if (m != nullptr) {
     m->x = x; m->h = h; m->qkv = qkv; m->q = q; m->attn = attn; m->act = act; m->h_sel = h_sel;
     m->logits = logits; m->part_val = pv; m->part_idx = pi; m->attn_part = ap;
     m->key_req = kr; m->key_pos = kp;
     m->ssq = ssq; m->ssq_sel = ssq_sel;
+    m->kv_dst = kv_dst; m->kv_info = kv_info;
     m->esize = esize; m->qkv_width = qkv_w; m->lm_tiles = lm_tiles;
     m->partial_floats = d.dtype == 1 ? pf : 0;
   }
@@ -178,6 +183,7 @@ static int validate(const sr_model_desc& d) {
   SR_REQUIRE(d.hidden > 0 && d.intermediate > 0 && d.layers > 0 && d.vocab > 0, "bad model shape");
   SR_REQUIRE(d.q_heads > 0 && d.kv_heads > 0 && d.q_heads % d.kv_heads == 0, "q_heads % kv_heads != 0");
   SR_REQUIRE(d.head_dim % 16 == 0 && d.head_dim <= 128, "head_dim must be a multiple of 16, <= 128");
+  SR_REQUIRE(d.dtype == 0 || d.head_dim % 32 == 0, "bf16 models need head_dim % 32 == 0 (fused RoPE)");
   SR_REQUIRE(d.intermediate % 16 == 0, "intermediate must be a multiple of 16");
   SR_REQUIRE(d.page_size == 64, "page_size must be 64");
   SR_REQUIRE(d.max_tokens > 0 && d.max_seqs > 0, "max_tokens / max_seqs must be > 0");
@@ -236,7 +242,22 @@ int sr_model_create(const sr_model_desc* desc, void** handle) {
     for (int l = 0; l < d.layers; ++l) {
       const void* const* w = m->layer_ptrs.data() + (size_t)l * sr::kLayerPtrs;
       rc = sr::gemm_bf16_plan(&m->p_qkv[l], T, m->qkv_width, H, (const bf*)m->h, H, (const bf*)w[1], H,
-                              m->qkv, m->qkv_width, sr::kEpiStoreBf16, (const float*)w[2], 0);
+                              m->qkv, m->qkv_width, sr::kEpiQkvRope, (const float*)w[2], 0);
+      if (!rc) {
+        sr::RopeArgs& ra = m->p_qkv[l].rope;
+        ra.kv_dst = m->kv_dst;
+        ra.kv_info = m->kv_info;
+        ra.cos = d.rope_cos;
+        ra.sin = d.rope_sin;
+        ra.q_out = (bf*)m->q;
+        ra.cache = (bf*)d.kv_cache + l * kv.cache_layer_elems();
+        ra.window = d.window_kv ? (bf*)d.window_kv + l * kv.window_layer_elems() : nullptr;
+        ra.nq = d.q_heads;
+        ra.nkv = d.kv_heads;
+        ra.hd = d.head_dim;
+        ra.page = d.page_size;
+        ra.window_max = d.window_max;
+      }
       if (!rc) rc = sr::gemm_bf16_plan(&m->p_o[l], T, H, nqd, (const bf*)m->attn, nqd, (const bf*)w[3], nqd,
                                        m->x, H, sr::kEpiResidualNorm, nullptr, 0);
       if (!rc) rc = sr::gemm_bf16_plan(&m->p_gu[l], T, 2 * I, H, (const bf*)m->h, H, (const bf*)w[5], H,
@@ -326,14 +347,13 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
     SR_TRY(sr::embed_rows<bf>((const bf*)d.embed, a->token_ids, M, H, m->x, st));
     // input norm of layer 0; every later norm is fused into the o / down GEMMs
     SR_TRY(sr::norm_prep_rows(m->x, (const float*)m->layer_ptrs[0], M, H, m->prep_parts, (bf*)m->h, m->ssq, st));
+    // KV destination of every row, shared by all layers' qkv + RoPE epilogues
+    SR_TRY(sr::kv_rows(seqs, S, a->positions, M, m->kv, m->kv_dst, m->kv_info, st));
     for (int l = 0; l < d.layers; ++l) {
       auto& P = m->prof;
       P.begin(sr::kProfQkv, st);
+      m->p_qkv[l].rope.pos = a->positions;
       SR_TRY(sr::gemm_bf16_launch(m->p_qkv[l], st, M));
-      P.end(st);
-      P.begin(sr::kProfOther, st);
-      SR_TRY(sr::rope_scatter<bf>((const bf*)m->qkv, a->positions, seqs, S, a->max_q_len, d.rope_cos,
-                                  d.rope_sin, d.q_heads, l, m->kv, (bf*)m->q, st));
       P.end(st);
       P.begin(sr::kProfAttn, st);
       SR_TRY(sr::attention_bf16((const bf*)m->q, seqs, S, a->max_q_len, a->max_key, m->kv, l, d.q_heads,

@@ -108,6 +108,32 @@ def interleave_gate_up(wg: torch.Tensor, wu: torch.Tensor) -> torch.Tensor:
     return torch.stack([wg.view(I // 16, 16, H), wu.view(I // 16, 16, H)], dim=1).reshape(2 * I, H)
 
 
+def pair_interleave_heads(w: torch.Tensor, heads: int, hd: int) -> torch.Tensor:
+    """q/k projection rows (or bias) per head reordered (d, d + hd/2) pairwise:
+    row 2i = dim i, row 2i+1 = dim i + hd/2.  The fused qkv + RoPE GEMM
+    epilogue (gemm.cuh RopeArgs) then finds 16 whole rotation pairs in every
+    32-column accumulator chunk."""
+    half = hd // 2
+    rest = tuple(w.shape[1:])
+    return w.reshape(heads, 2, half, *rest).transpose(1, 2).reshape(heads * hd, *rest)
+
+
+def pair_deinterleave_heads(w: torch.Tensor, heads: int, hd: int) -> torch.Tensor:
+    """Inverse of :func:`pair_interleave_heads`."""
+    half = hd // 2
+    rest = tuple(w.shape[1:])
+    return w.reshape(heads, half, 2, *rest).transpose(1, 2).reshape(heads * hd, *rest)
+
+
+def qkv_rows(L: dict, s, fused_rope: bool):
+    """Concatenated W_qkv [(nq + 2 nkv) hd, H] and bias in kernel row order."""
+    wq, wk, bq, bk = L["wq"], L["wk"], L["bq"], L["bk"]
+    if fused_rope:
+        wq, bq = pair_interleave_heads(wq, s.q_heads, s.head_dim), pair_interleave_heads(bq, s.q_heads, s.head_dim)
+        wk, bk = pair_interleave_heads(wk, s.kv_heads, s.head_dim), pair_interleave_heads(bk, s.kv_heads, s.head_dim)
+    return torch.cat([wq, wk, L["wv"]], 0), torch.cat([bq, bk, L["bv"]], 0)
+
+
 def rope_tables(s: ModelShape, max_pos: int):
     """cos/sin [max_pos, hd/2] float32 computed in float64 (shared with the oracle)."""
     half = s.head_dim // 2
@@ -137,11 +163,15 @@ class DeviceModel:
         self.final_norm = put(weights["final_norm"], torch.float32)
         self.layer_tensors = []
         ptrs = []
+        # bf16: RoPE + KV scatter run in the qkv GEMM epilogue, which wants the
+        # q/k rows pair-interleaved (sr_model_desc, include/specrollout.h)
+        self.fused_rope = self.dtype_code == 1
         for L in weights["layers"]:
+            w_qkv, b_qkv = qkv_rows(L, s, self.fused_rope)
             t = {
                 "ln1": put(L["ln1"], torch.float32),
-                "w_qkv": put(torch.cat([L["wq"], L["wk"], L["wv"]], 0)),
-                "b_qkv": put(torch.cat([L["bq"], L["bk"], L["bv"]], 0), torch.float32),
+                "w_qkv": put(w_qkv),
+                "b_qkv": put(b_qkv, torch.float32),
                 "w_o": put(L["wo"]),
                 "ln2": put(L["ln2"], torch.float32),
                 "w_gu": put(interleave_gate_up(L["wg"].to(self.dev), L["wu"].to(self.dev))),

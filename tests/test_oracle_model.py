@@ -74,6 +74,19 @@ def test_interleave_gate_up_layout():
     assert torch.equal(w[32:48], g[16:32]) and torch.equal(w[48:64], u[16:32])
 
 
+def test_pair_interleave_heads_layout():
+    from paper_2511_16193_b200.model import pair_deinterleave_heads, pair_interleave_heads
+
+    w = torch.arange(2 * 8 * 3).view(16, 3).float()   # 2 heads, hd 8
+    p = pair_interleave_heads(w, 2, 8)
+    # head 0: rows 0,4,1,5,2,6,3,7; head 1 the same + 8
+    order = [0, 4, 1, 5, 2, 6, 3, 7]
+    assert torch.equal(p[:8], w[order]) and torch.equal(p[8:], w[[8 + i for i in order]])
+    assert torch.equal(pair_deinterleave_heads(p, 2, 8), w)
+    b = torch.arange(16).float()
+    assert torch.equal(pair_deinterleave_heads(pair_interleave_heads(b, 2, 8), 2, 8), b)
+
+
 def test_shapes_and_roofline_params():
     from paper_2511_16193_b200.model import SHAPES
 
