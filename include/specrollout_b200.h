@@ -149,6 +149,8 @@ int sr_gemm(int dtype, int M, int N, int K, const void* A, int lda, const void* 
  *     w_down [hidden, inter]
  * KV cache: [layers, num_pages, 2 (K,V), kv_heads, 64, head_dim], paged
  *   through block_table [max_requests, max_pages_per_req] (int32 page ids).
+ *   Zero-initialise it: attention streams whole pages, and the slots past a
+ *   sequence's last key must hold finite values (their weight is exactly 0).
  * window_kv: [layers, max_branches, 2, kv_heads, window_max, head_dim] holds
  *   the in-flight KV of Best-of-N drafter branches >= 1 (branch 0 writes its
  *   window straight into the paged cache).

@@ -25,6 +25,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v,-warn-spills"]
+# measurement builds only (e.g. -DSR_ATTN_PROBE=1, attention.cu)
+FLAGS += os.environ.get("SR_EXTRA_NVCC_FLAGS", "").split()
 
 
 def _digest(src: Path) -> str:

@@ -31,6 +31,10 @@ namespace sr {
 
 namespace {
 
+#ifndef SR_ATTN_PROBE
+#define SR_ATTN_PROBE 0
+#endif
+
 constexpr int kKT = 64;          // keys per tile (= page size)
 constexpr int kRows = 32;        // query rows per CTA
 constexpr int kMaxLayers = 128;  // per-layer work-claim counters
@@ -175,10 +179,17 @@ attn_bf16_kernel(AttnArgs A) {
     uint8_t* k_dst = sKV + stage * 2 * kTileBytes;
     uint8_t* v_dst = k_dst + kTileBytes;
     const int last = t * kKT + kKT - 1;
-    if (last <= max_key && (sq.branch < 0 || last < sq.ctx_len)) {
-      // a whole committed page: K and V of head h are two contiguous 16 KB
-      // blocks stored pre-swizzled -> two TMA bulk copies, no thread work
+    if (sq.branch < 0 || last < sq.ctx_len) {
+      // a page of the paged cache: K and V of head h are two contiguous 16 KB
+      // blocks stored pre-swizzled -> two TMA bulk copies, no thread work.
+      // Slots past max_key (the tail of the last page) hold stale finite
+      // values (the cache is zero-initialised, sr_model_desc): their scores
+      // are masked to -inf, so p = 0 and 0 * v adds exactly nothing.
       if (tid == 0) {
+#if SR_ATTN_PROBE == 2  // measurement build: compute only, no K/V traffic
+        sm100::mbar_arrive(&full[stage]);
+        return;
+#endif
         const __nv_bfloat16* kb = cache + ((int64_t)btab[t] * 2 * nkv + h) * psz * HD;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         sm100::mbar_arrive_expect_tx(&full[stage], 2 * kTileBytes);
@@ -189,7 +200,7 @@ attn_bf16_kernel(AttnArgs A) {
       }
       return;
     }
-    // partial page / drafter-branch window keys: synchronous swizzle-aware copy
+    // tile reaching drafter-branch window keys: synchronous swizzle-aware copy
     for (int e = tid; e < kKT * CH; e += kAttnThreads) {
       const int r = e / CH, pc = e % CH;        // destination row, physical chunk
       const int kp = t * kKT + r;
@@ -250,6 +261,9 @@ attn_bf16_kernel(AttnArgs A) {
     const uint32_t k_base = (uint32_t)__cvta_generic_to_shared(sKV + stage * 2 * kTileBytes);
     const uint32_t v_base = k_base + kTileBytes;
     const int key0 = t * kKT + kw * 16;
+#if SR_ATTN_PROBE == 1  // measurement build: K/V traffic only, no math
+    continue;
+#endif
     if (!active) continue;
     {
       const int mt = mw;
