@@ -833,7 +833,9 @@ void choose_pair_tile(int M, int N, int K, int epi, int* bn_out, int* mc_out) {
   const int num_n = (N + best - 1) / best;
   const int clusters = num_m * (num_n / 2);
   *bn_out = best;
-  *mc_out = (num_n % 2 == 0 && clusters <= num_sms() / 4) ? 2 : 1;
+  // A multicast couples the rings of two pairs; with the 3-stage ring of the
+  // widest tiles that stalls both (7B o / down: 2x slower), so only <= 160.
+  *mc_out = (num_n % 2 == 0 && clusters <= num_sms() / 4 && best <= 160) ? 2 : 1;
 }
 }  // namespace
 

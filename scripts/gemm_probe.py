@@ -19,6 +19,10 @@ SHAPES_15B = {  # name: (N, K, epilogue)
     "qkv": (2048, 1536, 0), "o": (1536, 1536, 1), "gate_up": (17920, 1536, 2),
     "down": (1536, 8960, 1), "lm_head": (151936, 1536, 3),
 }
+SHAPES_7B = {
+    "qkv": (4608, 3584, 0), "o": (3584, 3584, 1), "gate_up": (37888, 3584, 2),
+    "down": (3584, 18944, 1),
+}
 
 
 def time_it(fn, iters=20):
@@ -37,11 +41,18 @@ def time_it(fn, iters=20):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--m", type=int, default=1280)
+    ap.add_argument("--model", choices=["1.5b", "7b"], default="1.5b")
+    ap.add_argument("--only", default=None, help="comma-separated GEMM names")
+    ap.add_argument("--bns", type=int, nargs="+", default=[128, 256, -128, -160, -192, -256, -1152, -1184, 0],
+                    help="tile widths: >0 single-CTA, <0 CTA pair, <-1024 pair + A multicast, 0 auto")
     args = ap.parse_args()
     lib = _native.lib()
     M = args.m
     st = _native.stream_handle()
-    for name, (N, K, epi) in SHAPES_15B.items():
+    shapes = SHAPES_7B if args.model == "7b" else SHAPES_15B
+    for name, (N, K, epi) in shapes.items():
+        if args.only and name not in args.only.split(","):
+            continue
         A = torch.randn(M, K, device="cuda").bfloat16()
         W = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
         if epi == 1:
@@ -52,7 +63,7 @@ def main():
             C = torch.empty(M, N, device="cuda")
         else:
             C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-        for bn in (128, 256, -128, -160, -192, -256, -1152, -1184, 0):
+        for bn in args.bns:
             if False:
                 continue
 

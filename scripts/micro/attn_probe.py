@@ -34,11 +34,12 @@ def main():
     ap.add_argument("--nq", type=int, default=12)
     ap.add_argument("--nkv", type=int, default=2)
     ap.add_argument("--hd", type=int, default=128)
+    ap.add_argument("--ctx", type=int, nargs=2, default=[128, 1024], help="context range (inclusive)")
     a = ap.parse_args()
     lib = _native.lib()
     rng = np.random.default_rng(0)
     S, ql, nq, nkv, hd = a.seqs, a.q_len, a.nq, a.nkv, a.hd
-    ctx = rng.integers(128, 1025, S)
+    ctx = rng.integers(a.ctx[0], a.ctx[1] + 1, S)
     total = ctx + ql
     pages_per = (total + PAGE - 1) // PAGE
     P = int(pages_per.sum())
