@@ -177,7 +177,8 @@ def run_ours(args, rank, world, dist):
     steps_total = args.warmup + 2 * args.steps + 8
     trace, prompts, budget = workload(rank, args.batch, steps_total, s.vocab, world)
     max_len = max(len(p) for p in prompts) + budget[0] + K + 8
-    w = init_weights(s, seed=0, device="cuda")
+    big = s.linear_params() > 20e9   # fp32 + bf16 copies would not fit: convert layer by layer
+    w = init_weights(s, seed=0, device="cuda", lazy=big)
     B = len(prompts)
     model = DeviceModel(s, w, dtype="bf16", max_requests=B, max_len=max_len,
                         max_tokens=B * (K + 1), max_seqs=B)
@@ -474,7 +475,9 @@ def main():
         dist = tdist
     result, ctx = run_ours(args, rank, world, dist)
     if rank == 0:
-        if world == 1 and not args.no_cpu_baseline:
+        from paper_2511_16193_b200.model import shape
+        # the CPU sample of a >10B model would need its fp32 weights in host RAM
+        if world == 1 and not args.no_cpu_baseline and shape(args.model).linear_params() <= 10e9:
             result["cpu_baseline"] = cpu_baseline(*ctx)
         else:
             result["cpu_baseline"] = None

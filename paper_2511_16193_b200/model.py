@@ -73,29 +73,39 @@ def shape(name: str, layers: int | None = None) -> ModelShape:
     return s
 
 
-def init_weights(s: ModelShape, seed: int = 0, device="cpu", std: float = 0.02) -> dict:
+def init_weights(s: ModelShape, seed: int = 0, device="cpu", std: float = 0.02, lazy: bool = False) -> dict:
     """Canonical (HF-layout) fp32 weights, N(0, std), deterministic in seed.
 
     Norm weights are 1 + N(0, std) so the scale is exercised; biases N(0, std).
+    ``lazy``: ``w["layers"]`` is a one-pass iterable that creates each layer
+    when reached (own generator per layer), so a model whose fp32 weights do
+    not fit next to its bf16 copy (32B) converts layer by layer.
     """
     g = torch.Generator(device=device).manual_seed(seed)
 
-    def rnd(*shape_):
-        return torch.randn(*shape_, generator=g, device=device, dtype=torch.float32) * std
+    def rnd(*shape_, gen=g):
+        return torch.randn(*shape_, generator=gen, device=device, dtype=torch.float32) * std
 
     h, i, hd = s.hidden, s.intermediate, s.head_dim
+
+    def layer(gen):
+        return {
+            "ln1": 1.0 + rnd(h, gen=gen),
+            "wq": rnd(s.q_heads * hd, h, gen=gen), "wk": rnd(s.kv_heads * hd, h, gen=gen),
+            "wv": rnd(s.kv_heads * hd, h, gen=gen),
+            "bq": rnd(s.q_heads * hd, gen=gen), "bk": rnd(s.kv_heads * hd, gen=gen),
+            "bv": rnd(s.kv_heads * hd, gen=gen),
+            "wo": rnd(h, s.q_heads * hd, gen=gen),
+            "ln2": 1.0 + rnd(h, gen=gen),
+            "wg": rnd(i, h, gen=gen), "wu": rnd(i, h, gen=gen), "wd": rnd(h, i, gen=gen),
+        }
+
     w = {"embed": rnd(s.vocab, h)}
-    layers = []
-    for _ in range(s.layers):
-        layers.append({
-            "ln1": 1.0 + rnd(h),
-            "wq": rnd(s.q_heads * hd, h), "wk": rnd(s.kv_heads * hd, h), "wv": rnd(s.kv_heads * hd, h),
-            "bq": rnd(s.q_heads * hd), "bk": rnd(s.kv_heads * hd), "bv": rnd(s.kv_heads * hd),
-            "wo": rnd(h, s.q_heads * hd),
-            "ln2": 1.0 + rnd(h),
-            "wg": rnd(i, h), "wu": rnd(i, h), "wd": rnd(h, i),
-        })
-    w["layers"] = layers
+    if lazy:
+        w["layers"] = (layer(torch.Generator(device=device).manual_seed(seed * 1000 + 1 + li))
+                       for li in range(s.layers))
+    else:
+        w["layers"] = [layer(g) for _ in range(s.layers)]
     w["final_norm"] = 1.0 + rnd(h)
     w["lm_head"] = w["embed"] if s.tied else rnd(s.vocab, h)
     return w

@@ -19,6 +19,10 @@ SHAPES_15B = {  # name: (N, K, epilogue)
     "qkv": (2048, 1536, 0), "o": (1536, 1536, 1), "gate_up": (17920, 1536, 2),
     "down": (1536, 8960, 1), "lm_head": (151936, 1536, 3),
 }
+SHAPES_32B = {
+    "qkv": (7168, 5120, 0), "o": (5120, 5120, 1), "gate_up": (55296, 5120, 2),
+    "down": (5120, 27648, 1),
+}
 SHAPES_7B = {
     "qkv": (4608, 3584, 0), "o": (3584, 3584, 1), "gate_up": (37888, 3584, 2),
     "down": (3584, 18944, 1),
@@ -41,7 +45,7 @@ def time_it(fn, iters=20):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--m", type=int, default=1280)
-    ap.add_argument("--model", choices=["1.5b", "7b"], default="1.5b")
+    ap.add_argument("--model", choices=["1.5b", "7b", "32b"], default="1.5b")
     ap.add_argument("--only", default=None, help="comma-separated GEMM names")
     ap.add_argument("--bns", type=int, nargs="+", default=[128, 256, -128, -160, -192, -256, -1152, -1184, 0],
                     help="tile widths: >0 single-CTA, <0 CTA pair, <-1024 pair + A multicast, 0 auto")
@@ -49,7 +53,7 @@ def main():
     lib = _native.lib()
     M = args.m
     st = _native.stream_handle()
-    shapes = SHAPES_7B if args.model == "7b" else SHAPES_15B
+    shapes = {"7b": SHAPES_7B, "32b": SHAPES_32B}.get(args.model, SHAPES_15B)
     for name, (N, K, epi) in shapes.items():
         if args.only and name not in args.only.split(","):
             continue
