@@ -69,19 +69,36 @@ __device__ __forceinline__ uint4 pack8_bf16(const float* f) {
   return w;
 }
 
+// Per-row inputs of the RoPE epilogue, loaded before the accumulator is ready.
+struct RopeRow {
+  int info = -1, pos = 0;
+  int64_t dst = 0;
+};
+
+__device__ __forceinline__ RopeRow rope_row(const RopeArgs& ra, int row, int M) {
+  RopeRow r;
+  if (row < M) {
+    r.info = ra.kv_info[row];
+    r.pos = ra.pos[row];
+    r.dst = ra.kv_dst[row];
+  }
+  return r;
+}
+
 // kEpiQkvRope for one 32-column chunk of one row (see RopeArgs).
-__device__ __forceinline__ void qkv_rope_chunk(const float* f, int row, int col, const RopeArgs& ra) {
-  const int info = ra.kv_info[row];
+__device__ __forceinline__ void qkv_rope_chunk(const float* f, int row, int col, const RopeArgs& ra,
+                                               const RopeRow& rr) {
+  const int info = rr.info;
   if (info < 0) return;  // padding row of the verify batch
   const int hd = ra.hd, half = hd >> 1;
   const int hq = ra.nq * hd, hk = ra.nkv * hd;
   const bool win = (info >> 16) & 1;
   const int slot = info & 0xFFFF;
   const int rows = win ? ra.window_max : ra.page;
-  __nv_bfloat16* kbase = (win ? ra.window : ra.cache) + ra.kv_dst[row];
+  __nv_bfloat16* kbase = (win ? ra.window : ra.cache) + rr.dst;
   if (col < hq + hk) {
     const int hc = col % hd, d0 = hc >> 1;  // 16 pairs (d0 + i, d0 + i + half)
-    const int pos = ra.pos[row];
+    const int pos = rr.pos;
     const float4* c4 = reinterpret_cast<const float4*>(ra.cos + (int64_t)pos * half + d0);
     const float4* s4 = reinterpret_cast<const float4*>(ra.sin + (int64_t)pos * half + d0);
     float y1[16], y2[16];
@@ -122,7 +139,7 @@ __device__ __forceinline__ void qkv_rope_chunk(const float* f, int row, int col,
 template <int EPI, int W = 32>
 __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, int row, int col, int M, int N, void* C,
                                                int ldc, const float* bias, const NormArgs& na, float& ss,
-                                               const RopeArgs& ra) {
+                                               const RopeArgs& ra, const RopeRow& rr = RopeRow{}) {
   if (row >= M) return;
   if constexpr (EPI == kEpiArgmax) return;  // handled in the tile loop
   if constexpr (EPI == kEpiQkvRope) {
@@ -130,7 +147,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, int row, int c
     float f[W];
 #pragma unroll
     for (int i = 0; i < W; ++i) f[i] = __uint_as_float(v[i]) + (bias != nullptr ? bias[col + i] : 0.0f);
-    qkv_rope_chunk(f, row, col, ra);
+    qkv_rope_chunk(f, row, col, ra, rr);
     return;
   }
   float f[W];
@@ -261,7 +278,9 @@ template <int EPI>
 __device__ __forceinline__ void epilogue32(const uint32_t (&v)[32], int row, int col, int M, int N, void* C,
                                            int ldc, const float* bias, const NormArgs& na, float& ss,
                                            const RopeArgs& ra) {
-  epilogue_chunk<EPI, 32>(v, row, col, M, N, C, ldc, bias, na, ss, ra);
+  RopeRow rr;
+  if constexpr (EPI == kEpiQkvRope) rr = rope_row(ra, row, M);
+  epilogue_chunk<EPI, 32>(v, row, col, M, N, C, ldc, bias, na, ss, ra, rr);
 }
 
 // Consumer side of the fused RMSNorm: r = rsqrt(sum of the row's partials
@@ -649,6 +668,8 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         continue;
       }
       const float rs = norm_row_scale(na, row, M);
+      RopeRow rr;
+      if constexpr (EPI == kEpiQkvRope) rr = rope_row(ra, row, M);
       sm100::mbar_wait(&tfull[acc], acc_phase);
       sm100::tc_fence_after();
       float best = -INFINITY;
@@ -665,7 +686,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if constexpr (EPI == kEpiArgmax) {
           argmax_chunk<CW>(v, col, N, row, M, sa, best, best_idx);
         } else {
-          if (col < N) epilogue_chunk<EPI, CW>(v, row, col, M, N, C, ldc, bias, na, ss, ra);
+          if (col < N) epilogue_chunk<EPI, CW>(v, row, col, M, N, C, ldc, bias, na, ss, ra, rr);
         }
       }
       if constexpr (EPI == kEpiResidualNorm) {
