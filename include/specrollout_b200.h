@@ -291,11 +291,14 @@ int sr_draft_model_batch(int num_requests, int k, int step, const int32_t* token
  * [(b*N+n)*(k+1), +nd+1) = last committed token then the drafts.  drafts
  * [N, B, k] / ndraft [N, B] are drafter-major (each drafter kernel writes its
  * own [B, k] block); both NULL = plain decode; ndraft < 0 = the request has
- * no window this round (decoupled gap round, sim.py:1076-1080). */
+ * no window this round (decoupled gap round, sim.py:1076-1080).  window
+ * [B] (optional): per-request window w_r <= k, the mixed-window batch of
+ * request-level reconfiguration (planner.py:223-272); NULL = k for all. */
 int sr_build_verify_batch(int num_requests, int num_drafters, int k, const int32_t* tokens,
                           int64_t tok_stride, const int32_t* seq_len, const int32_t* gen_len,
                           const int32_t* max_new, const int32_t* drafts, const int32_t* ndraft,
-                          int32_t* token_ids, int32_t* positions, void* seqs, sr_stream_t stream);
+                          const int32_t* window, int32_t* token_ids, int32_t* positions, void* seqs,
+                          sr_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -113,8 +113,9 @@ __global__ void kv_commit_kernel(int N, const SeqInfo* __restrict__ seqs, const 
 __global__ void build_verify_kernel(int B, int N, int k, const int32_t* __restrict__ tokens, int64_t tok_stride,
                                     const int32_t* __restrict__ seq_len, const int32_t* __restrict__ gen_len,
                                     const int32_t* __restrict__ max_new, const int32_t* __restrict__ drafts,
-                                    const int32_t* __restrict__ ndraft, int32_t* __restrict__ token_ids,
-                                    int32_t* __restrict__ positions, SeqInfo* __restrict__ seqs) {
+                                    const int32_t* __restrict__ ndraft, const int32_t* __restrict__ window,
+                                    int32_t* __restrict__ token_ids, int32_t* __restrict__ positions,
+                                    SeqInfo* __restrict__ seqs) {
   grid_dep_sync();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= B * N) return;
@@ -127,6 +128,7 @@ __global__ void build_verify_kernel(int B, int N, int k, const int32_t* __restri
     nd = drafts != nullptr ? ndraft[n * B + b] : 0;
     active = nd >= 0;  // ndraft < 0: no window this round (decoupled gap round)
     nd = max(0, min(nd, min(k, remaining)));
+    if (window != nullptr) nd = min(nd, max(0, window[b]));  // per-request window (reconfiguration)
   }
   SeqInfo sq;
   sq.q_start = s * (k + 1);
@@ -289,15 +291,15 @@ extern "C" int sr_draft_model_batch(int num_requests, int k, int step, const int
 extern "C" int sr_build_verify_batch(int num_requests, int num_drafters, int k, const int32_t* tokens,
                                      int64_t tok_stride, const int32_t* seq_len, const int32_t* gen_len,
                                      const int32_t* max_new, const int32_t* drafts, const int32_t* ndraft,
-                                     int32_t* token_ids, int32_t* positions, void* seqs,
-                                     sr_stream_t stream) {
+                                     const int32_t* window, int32_t* token_ids, int32_t* positions,
+                                     void* seqs, sr_stream_t stream) {
   SR_REQUIRE(num_requests >= 0 && num_drafters >= 1 && k >= 0, "bad batch shape");
   if (num_requests == 0) return SR_OK;
   SR_REQUIRE(tokens && seq_len && gen_len && max_new && token_ids && positions && seqs, "null pointer");
   SR_REQUIRE(drafts == nullptr || ndraft != nullptr, "drafts without ndraft");
   const int S = num_requests * num_drafters;
   sr::launch_k(sr::build_verify_kernel, sr::ceil_div(S, 128), 128, 0, (cudaStream_t)stream, 
-      num_requests, num_drafters, k, tokens, tok_stride, seq_len, gen_len, max_new, drafts, ndraft,
+      num_requests, num_drafters, k, tokens, tok_stride, seq_len, gen_len, max_new, drafts, ndraft, window,
       token_ids, positions, reinterpret_cast<sr::SeqInfo*>(seqs));
   return sr::check_launch("build_verify_kernel");
 }

@@ -248,11 +248,10 @@ class RolloutEngine:
                     self.B, self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(), d.min_n, d.max_n,
                     self.k, self.drafts[n].data_ptr(), self.ndraft[n].data_ptr(),
                     self.ngram_scratch.data_ptr(), st), "sr_ngram_propose")
-            self.ndraft.copy_(torch.minimum(self.ndraft, self.window[None, :]))
             drafts_ptr, nd_ptr = self.drafts.data_ptr(), self.ndraft.data_ptr()
         _native.check(lib.sr_build_verify_batch(
             self.B, self.N, self.k, self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(),
-            self.gen_len.data_ptr(), self.max_new.data_ptr(), drafts_ptr, nd_ptr,
+            self.gen_len.data_ptr(), self.max_new.data_ptr(), drafts_ptr, nd_ptr, self.window.data_ptr(),
             self.token_ids.data_ptr(), self.positions.data_ptr(), self.seqs.data_ptr(), st),
             "sr_build_verify_batch")
         self.m.forward(self.token_ids, self.positions, self.seqs, num_seqs=self.B * self.N,
