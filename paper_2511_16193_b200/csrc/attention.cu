@@ -25,6 +25,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 namespace sr {
@@ -251,104 +252,115 @@ attn_bf16_kernel(AttnArgs A) {
   load_tile(t_begin + 1, (gi + 1) % kStages);
   cp_async_commit();
   cp_async_wait<0>();  // Q block
-  const uint32_t q_base = (uint32_t)__cvta_generic_to_shared(sQ);
+  // ldmatrix addresses, hoisted: a fragment row r reads logical chunk
+  // 2kk + b, stored at physical chunk (2kk + b) ^ (r & 7).  With kk = 4u + j
+  // that is 8u + ((2j + b) ^ (r & 7)), so four per-thread offsets (j) plus an
+  // immediate 128u bytes address every k step.
+  const int mi = lane >> 3, x7 = lane & 7;
+  uint32_t qo[4], ko[4], vo[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    qo[j] = (uint32_t)__cvta_generic_to_shared(sQ) + (mw * 16 + (mi & 1) * 8 + x7) * HD * 2 +
+            (((2 * j + (mi >> 1)) ^ x7) << 4);
+    ko[j] = (kw * 16 + (mi >> 1) * 8 + x7) * HD * 2 + (((2 * j + (mi & 1)) ^ x7) << 4);
+    vo[j] = (kw * 16 + (mi & 1) * 8 + x7) * HD * 2 + (((2 * j + (mi >> 1)) ^ x7) << 4);
+  }
+  const float sl2 = A.scale_log2;
+
+  // One 64-key tile for this warp's 16 rows x 16 keys; MASK: some key of the
+  // slice may lie past a row's query position (the block's last tiles).
+  auto tile_math = [&](auto mask_tag, uint32_t k_base, int key0) {
+    constexpr bool MASK = decltype(mask_tag)::value;
+    const uint32_t v_base = k_base + kTileBytes;
+    // S = Q K^T for this warp's 16 keys
+    float sacc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
+      ldsm_x4(qo[kk & 3] + (kk >> 2) * 128, a0, a1, a2, a3);
+      ldsm_x4(k_base + ko[kk & 3] + (kk >> 2) * 128, b0, b1, b2, b3);
+      mma_bf16(sacc[0], a0, a1, a2, a3, b0, b1);
+      mma_bf16(sacc[1], a0, a1, a2, a3, b2, b3);
+    }
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int hi = i >> 1;
+        if constexpr (MASK) {
+          const int kp = key0 + nt * 8 + 2 * (lane & 3) + (i & 1);
+          if (kp > qpos[hi]) sacc[nt][i] = -INFINITY;
+        }
+        mx[hi] = fmaxf(mx[hi], sacc[nt][i]);
+      }
+    uint32_t pa[4];
+    bool rescale = false;
+    float alpha[2];
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi) {
+      mx[hi] = fmaxf(mx[hi], __shfl_xor_sync(0xffffffffu, mx[hi], 1));
+      mx[hi] = fmaxf(mx[hi], __shfl_xor_sync(0xffffffffu, mx[hi], 2));
+      // lazy rescaling (FA4): keep the reference max m_run (raw score units)
+      // unless the new max exceeds it by more than 8 in log2 units; p can
+      // then reach 2^8, harmless in fp32/bf16.  The decision depends only on
+      // this row's keys in tile order, so it is batch invariant.
+      const float m_old = m_run[hi];
+      const bool up = mx[hi] != -INFINITY && (m_old == -INFINITY || (mx[hi] - m_old) * sl2 > 8.0f);
+      alpha[hi] = 1.0f;
+      if (up) {
+        alpha[hi] = m_old == -INFINITY ? 0.0f : fast_exp2((m_old - mx[hi]) * sl2);
+        m_run[hi] = mx[hi];
+        rescale = true;
+      }
+      const float m_ref = m_run[hi];
+      const float neg = m_ref == -INFINITY ? 0.0f : -m_ref * sl2;
+      float p[4];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) p[nt * 2 + c] = fast_exp2(fmaf(sacc[nt][hi * 2 + c], sl2, neg));
+      const float rs = ((p[0] + p[1]) + p[2]) + p[3];
+      l_run[hi] = l_run[hi] * alpha[hi] + rs;
+      __nv_bfloat162 lo = __floats2bfloat162_rn(p[0], p[1]);
+      __nv_bfloat162 hi2 = __floats2bfloat162_rn(p[2], p[3]);
+      pa[hi] = *reinterpret_cast<uint32_t*>(&lo);       // a0 (row g) / a1 (row g+8)
+      pa[2 + hi] = *reinterpret_cast<uint32_t*>(&hi2);  // a2 / a3
+    }
+    if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+      for (int nt = 0; nt < NO; ++nt) {
+        o[nt][0] *= alpha[0];
+        o[nt][1] *= alpha[0];
+        o[nt][2] *= alpha[1];
+        o[nt][3] *= alpha[1];
+      }
+    }
+    // O += P V over the warp's 16 keys
+#pragma unroll
+    for (int np = 0; np < NO / 2; ++np) {
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4_t(v_base + vo[np & 3] + (np >> 2) * 128, b0, b1, b2, b3);
+      mma_bf16(o[2 * np], pa[0], pa[1], pa[2], pa[3], b0, b1);
+      mma_bf16(o[2 * np + 1], pa[0], pa[1], pa[2], pa[3], b2, b3);
+    }
+  };
+
+  const uint32_t kv_base = (uint32_t)__cvta_generic_to_shared(sKV);
   for (int t = t_begin; t < t_end; ++t) {
     const uint32_t g = gi + (uint32_t)(t - t_begin);
     const int stage = g % kStages;
     sm100::mbar_wait(&full[stage], (g / kStages) & 1u);
     __syncthreads();  // tile t (incl. plain smem stores) visible; tile t-1's slot is free
     load_tile(t + 2, (g + 2) % kStages);
-    const uint32_t k_base = (uint32_t)__cvta_generic_to_shared(sKV + stage * 2 * kTileBytes);
-    const uint32_t v_base = k_base + kTileBytes;
-    const int key0 = t * kKT + kw * 16;
 #if SR_ATTN_PROBE == 1  // measurement build: K/V traffic only, no math
     continue;
 #endif
     if (!active) continue;
-    {
-      const int mt = mw;
-
-      // S = Q K^T for this warp's 16 keys
-      float sacc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
-#pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
-        const int mi = lane >> 3;
-        ldsm_x4(q_base + swz<HD>(mt * 16 + (mi & 1) * 8 + (lane & 7), kk * 2 + (mi >> 1)), a0, a1, a2, a3);
-        ldsm_x4(k_base + swz<HD>(kw * 16 + (mi >> 1) * 8 + (lane & 7), kk * 2 + (mi & 1)), b0, b1, b2, b3);
-        mma_bf16(sacc[0], a0, a1, a2, a3, b0, b1);
-        mma_bf16(sacc[1], a0, a1, a2, a3, b2, b3);
-      }
-      // mask (only tiles reaching the block's first query need it), row max
-      // over the quad; scale_log2 is applied inside the exponent FFMA
-      const bool need_mask = key0 + 15 > min_qpos;
-      float mx[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int hi = i >> 1;
-          if (need_mask) {
-            const int kp = key0 + nt * 8 + 2 * (lane & 3) + (i & 1);
-            if (kp > qpos[hi]) sacc[nt][i] = -INFINITY;
-          }
-          mx[hi] = fmaxf(mx[hi], sacc[nt][i]);
-        }
-      uint32_t pa[4];
-      bool rescale = false;
-      float alpha[2];
-#pragma unroll
-      for (int hi = 0; hi < 2; ++hi) {
-        mx[hi] = fmaxf(mx[hi], __shfl_xor_sync(0xffffffffu, mx[hi], 1));
-        mx[hi] = fmaxf(mx[hi], __shfl_xor_sync(0xffffffffu, mx[hi], 2));
-        // lazy rescaling (FA4): keep the reference max m_run (raw score units)
-        // unless the new max exceeds it by more than 8 in log2 units; p can
-        // then reach 2^8, harmless in fp32/bf16.  The decision depends only on
-        // this row's keys in tile order, so it is batch invariant.
-        const float m_old = m_run[hi];
-        float m_ref = m_old;
-        alpha[hi] = 1.0f;
-        if (mx[hi] != -INFINITY && (m_old == -INFINITY || (mx[hi] - m_old) * A.scale_log2 > 8.0f)) {
-          m_ref = mx[hi];
-          alpha[hi] = m_old == -INFINITY ? 0.0f : fast_exp2((m_old - m_ref) * A.scale_log2);
-          rescale = true;
-        }
-        m_run[hi] = m_ref;
-        const float neg = m_ref == -INFINITY ? 0.0f : -m_ref * A.scale_log2;
-        float rs = 0.0f;
-        float p[4];
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            p[nt * 2 + c] = fast_exp2(fmaf(sacc[nt][hi * 2 + c], A.scale_log2, neg));
-            rs += p[nt * 2 + c];
-          }
-        l_run[hi] = l_run[hi] * alpha[hi] + rs;
-        __nv_bfloat162 lo = __floats2bfloat162_rn(p[0], p[1]);
-        __nv_bfloat162 hi2 = __floats2bfloat162_rn(p[2], p[3]);
-        pa[hi] = *reinterpret_cast<uint32_t*>(&lo);       // a0 (row g) / a1 (row g+8)
-        pa[2 + hi] = *reinterpret_cast<uint32_t*>(&hi2);  // a2 / a3
-      }
-      if (__any_sync(0xffffffffu, rescale)) {
-#pragma unroll
-        for (int nt = 0; nt < NO; ++nt) {
-          o[nt][0] *= alpha[0];
-          o[nt][1] *= alpha[0];
-          o[nt][2] *= alpha[1];
-          o[nt][3] *= alpha[1];
-        }
-      }
-      // O += P V over the warp's 16 keys
-#pragma unroll
-      for (int np = 0; np < NO / 2; ++np) {
-        uint32_t b0, b1, b2, b3;
-        const int mi = lane >> 3;
-        ldsm_x4_t(v_base + swz<HD>(kw * 16 + (mi & 1) * 8 + (lane & 7), np * 2 + (mi >> 1)), b0, b1, b2, b3);
-        mma_bf16(o[2 * np], pa[0], pa[1], pa[2], pa[3], b0, b1);
-        mma_bf16(o[2 * np + 1], pa[0], pa[1], pa[2], pa[3], b2, b3);
-      }
-    }
+    const int key0 = t * kKT + kw * 16;
+    const uint32_t k_base = kv_base + stage * 2 * kTileBytes;
+    if (key0 + 15 > min_qpos) tile_math(std::true_type{}, k_base, key0);
+    else tile_math(std::false_type{}, k_base, key0);
   }
   __syncthreads();
 
