@@ -334,7 +334,9 @@ def run_ours(args, rank, world, dist):
                      "traffic": traffic_bytes(),
                      "traffic_note": "DRAM read+write bytes per launch of the largest verify GEMM (gate_up "
                                      "+SwiGLU) from profiles/r01/ncu_step_layer0.json (ncu --set full); "
-                                     "algorithmic = 55.0 MB weights + 3.9 MB activations + 2.3 MB output",
+                                     "algorithmic = 55.0 MB weights + 3.9 MB activations in + 22.9 MB "
+                                     "SwiGLU output (written to L2, consumed there by down: DRAM sees "
+                                     "weights + activations + a partial write-back)",
                      "algorithmic_flops_per_step": flops_step,
                      "gemm_ms_per_step": gemm_ms / args.steps,
                      "gemm_share_of_step": (gemm_ms / args.steps) / step_ms,
