@@ -259,6 +259,12 @@ int sr_accept_commit(int num_requests, int num_drafters, const void* seqs, const
                      int32_t* gen_len, const int32_t* max_new, int bonus_token, int32_t* outcome,
                      int32_t* bon, sr_stream_t stream);
 
+/* Host-facing step result (RolloutEngine.capture_io): out [B, 4 + width] =
+ * outcome row b (first 4 ints) then tokens[b, seq_before[b] + j] for
+ * j < width (clamped to the row) -- the committed window of the step. */
+int sr_pack_results(int num_requests, int width, const int32_t* outcome, const int32_t* tokens,
+                    int64_t tok_stride, const int32_t* seq_before, int32_t* out, sr_stream_t stream);
+
 /* Copy the winning branch's window KV into the paged cache (all layers). */
 int sr_kv_commit(void* model, int num_requests, int num_drafters, const void* seqs,
                  const int32_t* outcome, const int32_t* bon, sr_stream_t stream);

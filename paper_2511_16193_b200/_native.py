@@ -46,6 +46,7 @@ SIGNATURES: dict[str, list] = {
     "sr_synthetic_draft": [_i32, _i32, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i32, _vp, _vp, _vp],
     "sr_draft_model_batch": [_i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                              _vp, _vp, _vp],
+    "sr_pack_results": [_i32, _i32, _vp, _vp, _i64, _vp, _vp, _vp],
     "sr_build_verify_batch": [_i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               _vp, _vp, _vp],
 }

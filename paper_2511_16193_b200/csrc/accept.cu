@@ -241,7 +241,38 @@ int kv_commit(int B, int N, const SeqInfo* seqs, const int32_t* outcome, const i
   return check_launch("kv_commit_kernel");
 }
 
+// Host-facing step result: per request its outcome row then the token
+// slots [seq_before, seq_before + w) (clamped to the row), one thread per cell.
+__global__ void pack_results_kernel(int B, int w, const int32_t* __restrict__ outcome,
+                                    const int32_t* __restrict__ tokens, int64_t tok_stride,
+                                    const int32_t* __restrict__ seq_before, int32_t* __restrict__ out) {
+  grid_dep_sync();
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int cols = 4 + w;
+  if (e >= B * cols) return;
+  const int b = e / cols, c = e % cols;
+  int v;
+  if (c < 4) {
+    v = outcome[(int64_t)b * 4 + c];
+  } else {
+    const int64_t pos = min((int64_t)seq_before[b] + (c - 4), tok_stride - 1);
+    v = tokens[(int64_t)b * tok_stride + pos];
+  }
+  out[e] = v;
+}
+
 }  // namespace sr
+
+extern "C" int sr_pack_results(int num_requests, int width, const int32_t* outcome, const int32_t* tokens,
+                               int64_t tok_stride, const int32_t* seq_before, int32_t* out, sr_stream_t stream) {
+  SR_REQUIRE(num_requests >= 0 && width >= 0 && tok_stride > 0, "bad result shape");
+  if (num_requests == 0) return SR_OK;
+  SR_REQUIRE(outcome && tokens && seq_before && out, "null pointer");
+  const int n = num_requests * (4 + width);
+  sr::launch_k(sr::pack_results_kernel, sr::ceil_div(n, 256), 256, 0, (cudaStream_t)stream, num_requests, width,
+               outcome, tokens, tok_stride, seq_before, out);
+  return sr::check_launch("pack_results_kernel");
+}
 
 extern "C" int sr_accept_commit(int num_requests, int num_drafters, const void* seqs,
                                 const int32_t* token_ids, const int32_t* target, int32_t* tokens,

@@ -308,10 +308,10 @@ class RolloutEngine:
         if tuple(result_host.shape) != (self.B, 4 + w) or budget_host.numel() != self.B:
             raise ConfigError("result_host must be [B, 4 + k + 2] and budget_host [B]")
         seq_before = torch.empty_like(self.seq_len)
-        slots = torch.arange(w, device=self.dev, dtype=torch.int32)
+        res = torch.empty((self.B, 4 + w), dtype=torch.int32, device=self.dev)
         if not hasattr(self, "_io_keep"):
             self._io_keep = []
-        self._io_keep.append((seq_before, slots))   # buffers the graph reads/writes stay alive
+        self._io_keep.append((seq_before, res))   # buffers the graph reads/writes stay alive
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()
@@ -321,8 +321,9 @@ class RolloutEngine:
             self.max_new.copy_(budget_host, non_blocking=True)
             seq_before.copy_(self.seq_len)
             self._enqueue_step(0)
-            idx = (seq_before[:, None] + slots[None, :]).clamp_(max=self.stride - 1)
-            res = torch.cat([self.history[0][: self.B], torch.gather(self.tokens, 1, idx.long())], 1)
+            _native.check(self.lib.sr_pack_results(
+                self.B, w, self.history[0].data_ptr(), self.tokens.data_ptr(), self.stride,
+                seq_before.data_ptr(), res.data_ptr(), _native.stream_handle()), "sr_pack_results")
             result_host.copy_(res, non_blocking=True)
             g.capture_end()
         torch.cuda.current_stream().wait_stream(s)
