@@ -128,3 +128,47 @@ def test_waste_bounds(model, stack):
     for o in m.outcomes:
         limit = 2 * o.window - 1 if o.mode == "D" else o.window - 1
         assert o.wasted <= limit, o
+
+
+@pytest.mark.parametrize("p", [0.1, 0.5, 0.9])
+def test_synthetic_acceptance_law_matches_pmf(p):
+    """The device drafter under the reference's keyed accept_draw law
+    (sim.py:322-336): accepted-prefix histogram over 4096 requests x 8 window
+    offsets vs the closed form P(a, w) (costmodel.py:253-260), 5-sigma MC
+    tolerance, and tau within 2 % (reference tests/test_acceptance.py:85-104)."""
+    from paper_2511_16193_b200 import _native
+    from paper_2511_16193_b200.costmodel import accept_pmf, expected_tokens_decoupled
+    from paper_2511_16193_b200.verify import CHUNK, entropy_words, keyed_fill
+
+    lib = _native.lib()
+    R, offsets = 4096, 8
+    dev = "cuda"
+    uni = torch.empty((R, CHUNK), dtype=torch.float64, device=dev)
+    keyed_fill("uniforms", [entropy_words(0, rid, "accept_draw", "draft-0.5b", 0) for rid in range(R)],
+               CHUNK, uni)
+    truth = torch.zeros((R, CHUNK), dtype=torch.int32, device=dev)
+    truth_len = torch.full((R,), CHUNK, dtype=torch.int32, device=dev)
+    pr = torch.full((R,), p, dtype=torch.float64, device=dev)
+    st = _native.stream_handle()
+    for w in (1, 2, 4, 8):
+        counts = np.zeros(w + 1, dtype=np.int64)
+        for off in range(offsets):
+            gen = torch.full((R,), off * 16, dtype=torch.int32, device=dev)
+            drafts = torch.full((R, w), -1, dtype=torch.int32, device=dev)
+            nd = torch.zeros(R, dtype=torch.int32, device=dev)
+            _native.check(lib.sr_synthetic_draft(R, w, truth.data_ptr(), CHUNK, truth_len.data_ptr(),
+                                                 uni.data_ptr(), CHUNK, pr.data_ptr(), gen.data_ptr(), 50257,
+                                                 drafts.data_ptr(), nd.data_ptr(), st), "sr_synthetic_draft")
+            d = drafts.cpu().numpy()
+            assert (nd.cpu().numpy() == w).all()
+            hit = d == 0                       # proposed the true token
+            a = np.where(hit.all(1), w, (~hit).argmax(1))
+            counts += np.bincount(a, minlength=w + 1)
+        n = counts.sum()
+        freq = counts / n
+        pmf = np.array([accept_pmf(p, w, a) for a in range(w + 1)])
+        sigma = np.sqrt(pmf * (1 - pmf) / n)
+        assert np.all(np.abs(freq - pmf) <= 5 * sigma + 1e-9), (w, freq, pmf)
+        a_vals = np.arange(w + 1)
+        tau = float((freq * np.where(a_vals < w, (a_vals + 1) / 2.0, float(w))).sum())
+        assert abs(tau - expected_tokens_decoupled(p, w)) / expected_tokens_decoupled(p, w) < 0.02

@@ -58,3 +58,31 @@ def test_verify_window_edge_cases():
     assert rollout_oracle.verify_window(u, 0.95, 0, 4, 0, 4, True) == (4, 4, 0)  # no bonus at end
     assert rollout_oracle.verify_window(u, 0.05, 0, 4, 0, 10, False) == (0, 1, 3)
     assert rollout_oracle.verify_window(u, 0.5, 3, 0, 0, 10, False) == (0, 1, 0)  # plain
+
+
+def test_closed_forms_match_reference():
+    """Accepted-length law P(a, w) and the expected tokens per window
+    (reference costmodel.py:253-284) -- the statistical oracle of §8(a) a14."""
+    from paper_2511_16193_b200.costmodel import accept_pmf, expected_tokens_coupled, expected_tokens_decoupled
+
+    rows = golden("closed_forms.json")
+    assert len(rows) == 36
+    for r in rows:
+        p, w = r["p"], r["w"]
+        assert [accept_pmf(p, w, a) for a in range(w + 1)] == r["pmf"]
+        assert expected_tokens_decoupled(p, w) == r["tau_d"]
+        assert expected_tokens_coupled(p, w) == r["tau_c"]
+    assert expected_tokens_decoupled(0.5, 3) == 1.0625
+
+
+def test_gen_trace_matches_reference():
+    """Synthetic batch generator (reference workload.py:170-196,
+    scenarios.py:71-81): ids, prompt lengths, true lengths and latent
+    acceptance rates equal the reference's for two (batch, seed) specs."""
+    from paper_2511_16193_b200 import scenarios
+    from paper_2511_16193_b200.workload import gen_trace
+
+    for key, rows in golden("workload.json").items():
+        batch, seed = (int(x) for x in key.split("_"))
+        tr = gen_trace(scenarios.default_trace_spec(batch=batch, seed=seed))
+        assert [[r.id, r.prompt_len, r.true_len, r.latent_accept] for r in tr] == rows
