@@ -146,7 +146,15 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, int row, int c
     static_assert(EPI != kEpiQkvRope || W == 32, "RoPE chunks are 16 pairs");
     float f[W];
 #pragma unroll
-    for (int i = 0; i < W; ++i) f[i] = __uint_as_float(v[i]) + (bias != nullptr ? bias[col + i] : 0.0f);
+    for (int i = 0; i < W; ++i) f[i] = __uint_as_float(v[i]);
+    if (bias != nullptr) {  // 32 consecutive floats, 128-byte aligned: eight 16-byte loads
+      const float4* b4 = reinterpret_cast<const float4*>(bias + col);
+#pragma unroll
+      for (int q = 0; q < W / 4; ++q) {
+        const float4 b = b4[q];
+        f[4 * q] += b.x; f[4 * q + 1] += b.y; f[4 * q + 2] += b.z; f[4 * q + 3] += b.w;
+      }
+    }
     qkv_rope_chunk(f, row, col, ra, rr);
     return;
   }
