@@ -466,9 +466,16 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 // (256 clk) while 128-k stages (~450 clk vs 512 clk of MMA) do not.
 
 
+template <int BN, int EPI>
+constexpr bool kStagedEpi = (EPI == kEpiResidualF32 || EPI == kEpiResidualNorm) && BN <= 128 && BN % 32 == 0;
+
 template <int BN, int KC = 1>
 struct PairCfg {
   static constexpr int kBNH = BN / 2;
+  // residual epilogues (o, down) stage each warp's 32x32 fp32 chunk through
+  // shared memory so global stores are row-contiguous (full 32-byte sectors)
+  static constexpr uint32_t kStageRow = 36;  // floats per staged row (pad 4: conflict-free)
+  static constexpr uint32_t kEpiStageBytes = 4 * 32 * kStageRow * 4;
   static constexpr uint32_t kAChunk = kBM * kBK * 2;   // 128 rows x 128 B
   static constexpr uint32_t kBChunk = kBNH * kBK * 2;
   static constexpr uint32_t kABytes = KC * kAChunk;
@@ -534,6 +541,9 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   sm100::cluster_sync();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // after the barrier area (kSmem's trailing 256 B); launched with
+  // kEpiStageBytes more dynamic smem when kStagedEpi
+  float* epi_stage = reinterpret_cast<float*>(smem + S * Cfg::kStageBytes + 256);
   grid_dep_sync();  // prologue above touched no predecessor output
 
   if (warp == 0) {
@@ -641,6 +651,46 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           else sm100::tmem_ld_32x32b_x16(taddr + c * CW, v);
           sm100::tmem_ld_wait();
           const int col = n_blk * BN + c * CW;
+          if constexpr (kStagedEpi<BN, EPI>) {
+            if (n_blk * BN + BN <= N) {  // warp-uniform: full-width tile
+              // 1) thread = row: x_new = residual + acc, sum of squares in column order
+              float* T = epi_stage + quad * 32 * Cfg::kStageRow;
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                float xn[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  xn[i] = res[c * CW + 4 * q + i] + __uint_as_float(v[4 * q + i]);
+                  if constexpr (EPI == kEpiResidualNorm) ss = fmaf(xn[i], xn[i], ss);
+                }
+                *reinterpret_cast<float4*>(T + lane * Cfg::kStageRow + 4 * q) =
+                    make_float4(xn[0], xn[1], xn[2], xn[3]);
+              }
+              __syncwarp();
+              // 2) lane = (row it*4 + lane/8, columns 4*(lane%8)..+3): each
+              //    store instruction writes four full 128-byte row segments
+              const int qq = lane & 7;
+              const int row0 = row - lane;
+              float4 wv = make_float4(0, 0, 0, 0);
+              if constexpr (EPI == kEpiResidualNorm) wv = reinterpret_cast<const float4*>(na.w + col)[qq];
+#pragma unroll
+              for (int it = 0; it < 8; ++it) {
+                const int r = it * 4 + (lane >> 3);
+                const float4 xv = *reinterpret_cast<const float4*>(T + r * Cfg::kStageRow + 4 * qq);
+                if (row0 + r < M) {
+                  reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + (int64_t)(row0 + r) * ldc + col)[qq] = xv;
+                  if constexpr (EPI == kEpiResidualNorm) {
+                    uint2 hv;
+                    hv.x = pack_bf16(xv.x * wv.x, xv.y * wv.y);
+                    hv.y = pack_bf16(xv.z * wv.z, xv.w * wv.w);
+                    reinterpret_cast<uint2*>(na.h_out + (int64_t)(row0 + r) * na.ld_h + col)[qq] = hv;
+                  }
+                }
+              }
+              __syncwarp();  // T is rewritten by the next chunk
+              continue;
+            }
+          }
           if (vec) {
 #pragma unroll
             for (int q = 0; q < CW / 8; ++q) {
@@ -784,15 +834,17 @@ template <int BN, int EPI, int MC, int KC>
 int launch_pair_mc(const GemmPlan& p, int M, cudaStream_t stream) {
   using Cfg = PairCfg<BN, KC>;
   auto kern = gemm_pair_kernel<BN, EPI, MC, KC>;
+  constexpr size_t smem = Cfg::kSmem + (kStagedEpi<BN, EPI> ? Cfg::kEpiStageBytes : 0);
+  static_assert(smem <= 232448, "pair GEMM shared memory exceeds 227 KB");
   static bool attr_set = false;
   if (!attr_set) {
-    SR_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
+    SR_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
   }
   const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * (((p.N + BN - 1) / BN + MC - 1) / MC);
   const int slots = num_sms() / (2 * MC);
   const int clusters = tiles < slots ? tiles : slots;
-  sr::launch_k(kern, 2 * MC * clusters, kThreads, Cfg::kSmem, stream, p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux,
+  sr::launch_k(kern, 2 * MC * clusters, kThreads, smem, stream, p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux,
                p.sample, p.norm, p.rope);
   return check_launch("gemm_pair_kernel");
 }
