@@ -25,12 +25,13 @@ decoupled policy.  Bonus tokens are off (the successor starts at start + n).
 from __future__ import annotations
 
 import math
+import time
 
 import numpy as np
 import torch
 
 from . import _native
-from .engine import NgramDrafter, SyntheticDrafter
+from .engine import ModelDrafter, NgramDrafter, SyntheticDrafter, prefill_model
 from .errors import ConfigError
 from .model import DeviceModel
 
@@ -74,10 +75,10 @@ class DraftSide:
     round (``graphs=True``)."""
 
     def __init__(self, prompts, max_new, k: int, drafter, device="cuda", graphs: bool = True):
-        if isinstance(drafter, SyntheticDrafter) or isinstance(drafter, NgramDrafter):
+        if isinstance(drafter, (SyntheticDrafter, NgramDrafter, ModelDrafter)):
             self.drafter = drafter
         else:
-            raise ConfigError("decoupled mode supports the n-gram and reference-acceptance drafters")
+            raise ConfigError("decoupled mode supports the n-gram, small-model and reference-acceptance drafters")
         self.lib = _native.lib()
         self.dev = torch.device(device)
         self.B, self.k = len(prompts), k
@@ -108,6 +109,40 @@ class DraftSide:
         self.in_ctoks = torch.zeros((B, k + 1), dtype=torch.int32, device=d)
         self.use_graphs = graphs
         self._g_draft = self._g_apply = None
+        if isinstance(drafter, ModelDrafter):
+            self._attach_model(drafter, lens)
+
+    def _attach_model(self, drafter, lens) -> None:
+        """K5 on the drafter GPU: the small model's own paged KV cache over
+        this side's token mirror.  Its context for window j+1 is the committed
+        tokens plus in-flight window j; when window j is rejected the cached
+        length is pulled back to the corrected token, whose KV (and all after
+        it) the next catch-up recomputes (greedy drafting, T = 0)."""
+        m, B, k, d = drafter.m, self.B, self.k, self.dev
+        if m.max_tokens < B * (k + 2) or m.max_seqs < B or m.max_len < self.stride:
+            raise ConfigError("drafter model capacity too small for the batch")
+        self.dkv_len = torch.tensor([L - 1 for L in lens], dtype=torch.int32, device=d)
+        self.m_token_ids = torch.zeros(B * (k + 2), dtype=torch.int32, device=d)
+        self.m_positions = torch.zeros(B * (k + 2), dtype=torch.int32, device=d)
+        self.m_seqs = torch.zeros((B, 8), dtype=torch.int32, device=d)
+        self.m_logit_rows = torch.zeros(B, dtype=torch.int32, device=d)
+        self.m_out = torch.zeros(B, dtype=torch.int32, device=d)
+        self.max_key = self.stride - 1
+        prefill_model(m, self.tokens, [L - 1 for L in lens])
+
+    def _draft_model(self, st) -> None:
+        m, lib = self.drafter.m, self.lib
+        for step in range(self.k + 1):
+            _native.check(lib.sr_draft_model_batch(
+                self.B, self.k, step, self.tokens.data_ptr(), self.stride, self.ctx.data_ptr(),
+                self.g0.data_ptr(), self.max_new.data_ptr(), self.dkv_len.data_ptr(), self.m_out.data_ptr(),
+                self.drafts.data_ptr(), self.nd.data_ptr(), self.m_token_ids.data_ptr(),
+                self.m_positions.data_ptr(), self.m_seqs.data_ptr(), self.m_logit_rows.data_ptr(), st),
+                "sr_draft_model_batch")
+            if step < self.k:
+                m.forward(self.m_token_ids, self.m_positions, self.m_seqs, num_seqs=self.B,
+                          max_q_len=self.k + 2, max_key=self.max_key, out=self.m_out,
+                          logit_rows=self.m_logit_rows)
 
     def _draft(self) -> None:
         st = _native.stream_handle()
@@ -120,6 +155,8 @@ class DraftSide:
                 self.B, self.k, d.truth.data_ptr(), d.stride, self.max_new.data_ptr(), d.uniforms.data_ptr(),
                 d.stride, d.p.data_ptr(), self.g0.data_ptr(), self._vocab, self.drafts.data_ptr(),
                 self.nd.data_ptr(), st), "sr_synthetic_draft")
+        elif isinstance(self.drafter, ModelDrafter):
+            self._draft_model(st)
         else:
             d = self.drafter
             _native.check(self.lib.sr_ngram_propose(
@@ -145,6 +182,10 @@ class DraftSide:
         adv = torch.where(verified, committed, torch.zeros_like(committed))
         self.seq_len += adv
         self.gen_len += adv
+        if isinstance(self.drafter, ModelDrafter):
+            # the drafter's KV from the corrected token on was computed on
+            # rejected tokens: recompute from there next window
+            self.dkv_len.copy_(torch.where(part, torch.minimum(self.dkv_len, self.seq_len - 1), self.dkv_len))
         # in flight next round: the window just drafted, unless its predecessor was rejected
         self.inflight.copy_(torch.where(~part, self.out_nd, torch.zeros_like(self.out_nd)))
 
@@ -310,7 +351,7 @@ def pairing(world: int, drafters: int) -> dict:
 
 
 def run_ranks(dist, rank: int, world: int, drafters: int, shards: dict, k: int, make_drafter,
-              make_model=None, max_rounds: int = 1_000_000, graphs: bool = True):
+              make_model=None, max_rounds: int = 1_000_000, graphs: bool = True, round_times=None):
     """Decoupled rollout across ranks (one process per GPU).
 
     ``shards[v]`` = (prompts, max_new) of verifier rank v.  Drafter ranks run
@@ -319,6 +360,8 @@ def run_ranks(dist, rank: int, world: int, drafters: int, shards: dict, k: int, 
     isend/irecv per (drafter, verifier) pair on static buffers; each side's
     per-round device work replays a CUDA graph.  Returns (outputs, outcome
     rows, rounds) on verifier ranks, (None, None, rounds) on drafter ranks.
+    ``round_times`` (a list, verifier ranks): host time after each round's
+    exchange completed (the round's device work is done then).
     """
     dev = torch.device("cuda", torch.cuda.current_device())
     pairs = pairing(world, drafters)
@@ -351,8 +394,15 @@ def run_ranks(dist, rank: int, world: int, drafters: int, shards: dict, k: int, 
     peer = pairs[rank]
     done = torch.zeros(1, dtype=torch.int32, device=dev)
     history, rounds = [], 0
+    ev = []
     while rounds < max_rounds:
+        if round_times is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
         V.verify()
+        if round_times is not None:
+            e1.record()
+            ev.append((e0, e1))
         done.fill_(1 if V.done() else 0)
         NcclChannel(dist, peer).exchange(
             [V.out_verified, V.out_accepted, V.out_committed, V.out_ctoks, done], [V.in_drafts, V.in_nd])
@@ -360,7 +410,13 @@ def run_ranks(dist, rank: int, world: int, drafters: int, shards: dict, k: int, 
         if rounds > 0:
             history.append(rows.clone())
         rounds += 1
-        if int(done.item()):
+        finished = int(done.item())
+        if round_times is not None:
+            round_times.append(time.perf_counter())
+        if finished:
             break
     h = torch.stack(history).cpu().numpy() if history else None
+    if round_times is not None:
+        torch.cuda.synchronize()
+        round_times.append([a.elapsed_time(b) for a, b in ev])   # last entry: verify ms per round
     return V.eng.outputs(), h, rounds

@@ -38,6 +38,9 @@ def main():
     ap.add_argument("--method", default="draft-0.5b")
     ap.add_argument("--cap", type=int, default=300, help="max generated tokens per request")
     ap.add_argument("--check", action="store_true", help="compare outputs with plain decoding")
+    ap.add_argument("--steady", type=int, default=0,
+                    help="steady-state mode: no request finishes; time this many rounds after 5 warm-up "
+                         "rounds (the coupled bench's regime) instead of the long-tail trace")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
@@ -49,7 +52,10 @@ def main():
     for i, v in enumerate(range(a.drafters, world)):
         tr = shard(trace_all, i, nv)
         prompts = [stream(0, r.id, "prompt").integers(0, s.vocab, size=r.prompt_len).astype(np.int32) for r in tr]
-        shards[v] = (prompts, [min(r.true_len, a.cap) for r in tr])
+        lens = [min(r.true_len, a.cap) for r in tr]
+        if a.steady:
+            lens = [(a.steady + 8) * (a.k + 1) + 8] * len(tr)   # budget outlasts the timed rounds
+        shards[v] = (prompts, lens)
         traces[v] = tr
     truth = {}
     model = None
@@ -57,7 +63,7 @@ def main():
         prompts, lens = shards[rank]
         model = DeviceModel(s, init_weights(s, seed=0, device="cuda"), dtype="bf16", max_requests=len(prompts),
                             max_len=max(len(p) + L for p, L in zip(prompts, lens)) + 2 * a.k + 16,
-                            max_tokens=max(2048, len(prompts) * (a.k + 1)), max_seqs=len(prompts))
+                            max_tokens=len(prompts) * (a.k + 1), max_seqs=len(prompts))
         plain = RolloutEngine(model, prompts, lens, k=0, history=1)
         plain.prefill()
         plain.run()
@@ -78,10 +84,11 @@ def main():
     dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    times = []
     outs, rows, rounds = run_ranks(
         dist, rank, world, a.drafters, shards, a.k,
         make_drafter=lambda v: SyntheticDrafter(truth[v], traces[v], a.method, 0, vocab=s.vocab),
-        make_model=lambda: model)
+        make_model=lambda: model, max_rounds=(a.steady + 6) if a.steady else 1_000_000, round_times=times)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     res = {"rank": rank, "rounds": rounds, "seconds": dt}
@@ -89,8 +96,18 @@ def main():
         committed = int(sum(len(o) for o in outs))
         res.update(committed=committed, tokens_per_s=committed / dt,
                    mean_accepted=float(rows[:, :, 1][rows[:, :, 0] > 0].mean()))
+        if a.steady:
+            verify_ms = times.pop()   # per-round device time of the verify graph
+            # rows[i] = outcome of round i + 1; timed rounds 6 .. steady + 5
+            w0 = 5
+            res["steady_verify_ms_per_round"] = float(np.mean(verify_ms[w0:w0 + a.steady]))
+            dt_s = times[w0 + a.steady - 1] - times[w0 - 1]
+            c = int(rows[w0 - 1:w0 - 1 + a.steady, :, 2].clip(min=0).sum())
+            res.update(steady_rounds=a.steady, steady_committed=c, steady_tokens_per_s=c / dt_s,
+                       steady_ms_per_round=dt_s * 1e3 / a.steady)
         if a.check:
-            res["outputs_equal_plain"] = outs == truth[rank]
+            res["outputs_equal_plain"] = (all(o == t[: len(o)] for o, t in zip(outs, truth[rank])) if a.steady
+                                          else outs == truth[rank])
     print(json.dumps(res), flush=True)
     dist.barrier()
     dist.destroy_process_group()

@@ -404,6 +404,39 @@ def test_decoupled_outcomes_match_reference_golden():
         assert got == exp, f"request {r.id}"
 
 
+@pytest.mark.parametrize("same_weights", [True, False])
+def test_decoupled_small_model_drafter_equals_plain(same_weights):
+    """K5 on the drafter side of decoupled mode (reference sim.py:860-917
+    with a draft-model method): the drafter's context for window j+1 is the
+    committed tokens plus in-flight window j.  With the target's own weights
+    every verified window is fully accepted; with other weights windows are
+    rejected and the drafter's KV cache rolls back to the corrected token.
+    Both commit exactly the plain greedy sequence."""
+    from paper_2511_16193_b200.decoupled import run_local
+    from paper_2511_16193_b200.engine import ModelDrafter, RolloutEngine
+    from paper_2511_16193_b200.model import DeviceModel, init_weights
+
+    B, k = 6, 4
+    s, w, m = make("tiny", "bf16", B=B, max_len=256)
+    prompts = prompts_for(s.vocab, B, 20)
+    max_new = [30, 25, 40, 12, 33, 20]
+    plain = RolloutEngine(m, prompts, max_new, k=0, history=1)
+    plain.prefill()
+    plain.run()
+    truth = plain.outputs()
+    dw = w if same_weights else init_weights(s, seed=5)
+    dm = DeviceModel(s, dw, dtype="bf16", max_requests=B, max_len=256, max_tokens=B * (k + 2) * 4, max_seqs=B)
+    outs, rows = run_local(m, prompts, max_new, k, ModelDrafter(dm))
+    assert outs == truth
+    live = rows[rows[:, :, 0] > 0]
+    assert len(live) > 0
+    full = (live[:, 1] == live[:, 0]).mean()
+    if same_weights:
+        assert full == 1.0
+    else:
+        assert full < 1.0
+
+
 def test_configs2_7b_shape_bon_ngram_and_model_drafters():
     """configs[2] widths (Qwen2.5-7B: H 3584, I 18944, 28/4 heads, G = 7), 2
     layers: Best-of-N with n-gram + small-model (0.5B-shaped) drafters commits
