@@ -20,6 +20,11 @@ Exact-match semantics make the committed tokens identical to plain decoding;
 with the reference-acceptance drafter the per-request outcome stream
 (proposed, accepted, committed, wasted) equals the reference simulator's
 decoupled policy.  Bonus tokens are off (the successor starts at start + n).
+
+Drafters on the drafter side: the reference-acceptance drafter, the n-gram
+drafter (K4), and a small model (K5, ``ModelDrafter``) with its own paged KV
+cache whose context is the committed tokens plus the in-flight window; a
+rejected window pulls its cached length back to the corrected token.
 """
 
 from __future__ import annotations

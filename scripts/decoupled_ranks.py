@@ -22,7 +22,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2511_16193_b200 import scenarios  # noqa: E402
 from paper_2511_16193_b200.decoupled import pairing, run_ranks  # noqa: E402
 from paper_2511_16193_b200.dist import shard  # noqa: E402
-from paper_2511_16193_b200.engine import RolloutEngine, SyntheticDrafter  # noqa: E402
+from paper_2511_16193_b200.engine import ModelDrafter, NgramDrafter, RolloutEngine, SyntheticDrafter  # noqa: E402
 from paper_2511_16193_b200.model import DeviceModel, init_weights, shape  # noqa: E402
 from paper_2511_16193_b200.streams import stream  # noqa: E402
 from paper_2511_16193_b200.workload import gen_trace  # noqa: E402
@@ -36,6 +36,10 @@ def main():
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--method", default="draft-0.5b")
+    ap.add_argument("--drafter", choices=["synthetic", "model", "ngram"], default="synthetic",
+                    help="synthetic: reference accept_draw law over the target's greedy continuation; "
+                         "model: a random-init --draft-model decoder on the drafter GPU (K5); ngram: K4")
+    ap.add_argument("--draft-model", default="qwen2.5-0.5b")
     ap.add_argument("--cap", type=int, default=300, help="max generated tokens per request")
     ap.add_argument("--check", action="store_true", help="compare outputs with plain decoding")
     ap.add_argument("--steady", type=int, default=0,
@@ -84,10 +88,23 @@ def main():
     dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    def make_drafter(v):
+        if a.drafter == "synthetic":
+            return SyntheticDrafter(truth[v], traces[v], a.method, 0, vocab=s.vocab)
+        if a.drafter == "ngram":
+            return NgramDrafter()
+        ds = shape(a.draft_model)
+        prompts, lens = shards[v]
+        B = len(prompts)
+        max_len = max(len(p) + L for p, L in zip(prompts, lens)) + 4 * a.k + 32
+        dm = DeviceModel(ds, init_weights(ds, seed=1, device="cuda"), dtype="bf16", max_requests=B,
+                         max_len=max_len, max_tokens=B * (a.k + 2), max_seqs=B)
+        return ModelDrafter(dm)
+
     times = []
     outs, rows, rounds = run_ranks(
         dist, rank, world, a.drafters, shards, a.k,
-        make_drafter=lambda v: SyntheticDrafter(truth[v], traces[v], a.method, 0, vocab=s.vocab),
+        make_drafter=make_drafter,
         make_model=lambda: model, max_rounds=(a.steady + 6) if a.steady else 1_000_000, round_times=times)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
