@@ -587,3 +587,31 @@ def test_prefill_prompts_longer_than_max_tokens():
         e.run()
         outs.append(e.outputs())
     assert outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("k", [1, 2, 8])
+def test_edge_cases_spec_equals_plain(k):
+    """Ragged and degenerate batches: zero-budget requests (empty output),
+    one-token prompts, prompts ending on either side of a 64-token page
+    boundary, budgets that end mid-window, and window sizes 1 / 2 / 8 --
+    speculative output equals plain decoding and zero-budget requests
+    commit nothing."""
+    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine
+
+    B = 8
+    s, w, m = make("tiny", "bf16", B=B, max_len=512)
+    rng = np.random.default_rng(11)
+    words = rng.integers(0, s.vocab, size=12)
+    plens = [1, 63, 64, 65, 127, 128, 2, 200]
+    prompts = [words[rng.integers(0, 12, size=L)].astype(np.int32) for L in plens]
+    max_new = [0, 5, 1, 64, 0, 33, 70, k + 1]
+    plain = RolloutEngine(m, prompts, max_new, k=0, history=1)
+    plain.prefill()
+    plain.run()
+    ref = plain.outputs()
+    assert ref[0] == [] and ref[4] == []
+    assert [len(r) for r in ref] == max_new
+    spec = RolloutEngine(m, prompts, max_new, k=k, drafters=(NgramDrafter(1, 3),), history=1)
+    spec.prefill()
+    spec.run()
+    assert spec.outputs() == ref
