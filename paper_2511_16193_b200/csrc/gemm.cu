@@ -466,9 +466,6 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 // (256 clk) while 128-k stages (~450 clk vs 512 clk of MMA) do not.
 
 
-template <int BN, int EPI>
-constexpr bool kStagedEpi = (EPI == kEpiResidualF32 || EPI == kEpiResidualNorm) && BN <= 128 && BN % 32 == 0;
-
 template <int BN, int KC = 1>
 struct PairCfg {
   static constexpr int kBNH = BN / 2;
@@ -486,6 +483,12 @@ struct PairCfg {
   static constexpr int kChunk = BN % 32 == 0 ? 32 : 16;
   static constexpr size_t kSmem = 1024 + (size_t)kStages * kStageBytes + 256;
 };
+
+// residual epilogues stage through shared memory when the staging area fits
+// next to the ring (every shape the planner picks except 160-wide tiles)
+template <int BN, int EPI, int KC>
+constexpr bool kStagedEpi = (EPI == kEpiResidualF32 || EPI == kEpiResidualNorm) && BN % 32 == 0 &&
+                            PairCfg<BN, KC>::kSmem + PairCfg<BN, KC>::kEpiStageBytes <= 232448;
 
 // MC = 2: a cluster of two pairs computes two horizontally adjacent tiles
 // (n blocks 2j, 2j+1) of the same 256 rows.  Both pairs need the same
@@ -651,7 +654,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           else sm100::tmem_ld_32x32b_x16(taddr + c * CW, v);
           sm100::tmem_ld_wait();
           const int col = n_blk * BN + c * CW;
-          if constexpr (kStagedEpi<BN, EPI>) {
+          if constexpr (kStagedEpi<BN, EPI, KC>) {
             if (n_blk * BN + BN <= N) {  // warp-uniform: full-width tile
               // 1) thread = row: x_new = residual + acc, sum of squares in column order
               float* T = epi_stage + quad * 32 * Cfg::kStageRow;
@@ -724,6 +727,90 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if (lane == 0) sm100::mbar_arrive_cluster(leader_tempty + acc * 8);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         continue;
+      }
+      if constexpr (kStagedEpi<BN, EPI, KC> && BN > 128) {
+        // Wide residual tiles (7B / 32B o and down): the row's residual does
+        // not fit in registers, so it is read in the store layout instead --
+        // lane = (row it*4 + lane/8, 4 columns): coalesced 128-byte row
+        // segments, one chunk ahead of its use.  The sum of squares
+        // accumulates per lane and reduces over the row's 8 lanes at the end
+        // (fixed order).
+        if (n_blk * BN + BN <= N) {
+          float* T = epi_stage + quad * 32 * Cfg::kStageRow;
+          const int qq = lane & 7, row0 = row - lane;
+          float4 xres[8], xnext[8];
+          float ssp[8];
+          auto load_res = [&](int c, float4 (&dst)[8]) {
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int r = it * 4 + (lane >> 3);
+              dst[it] = row0 + r < M ? reinterpret_cast<const float4*>(reinterpret_cast<const float*>(C) +
+                                                                         (int64_t)(row0 + r) * ldc + n_blk * BN +
+                                                                         c * 32)[qq]
+                                     : make_float4(0, 0, 0, 0);
+            }
+          };
+          load_res(0, xres);
+#pragma unroll
+          for (int it = 0; it < 8; ++it) ssp[it] = 0.0f;
+          sm100::mbar_wait(&tfull[acc], acc_phase);
+          sm100::tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t v[32];
+            sm100::tmem_ld_32x32b_x32(taddr + c * 32, v);
+            if (c + 1 < BN / 32) load_res(c + 1, xnext);
+            sm100::tmem_ld_wait();
+            const int col = n_blk * BN + c * 32;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              *reinterpret_cast<float4*>(T + lane * Cfg::kStageRow + 4 * q) =
+                  make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                              __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+            __syncwarp();
+            float4 wv = make_float4(0, 0, 0, 0);
+            if constexpr (EPI == kEpiResidualNorm) wv = reinterpret_cast<const float4*>(na.w + col)[qq];
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int r = it * 4 + (lane >> 3);
+              const float4 a = *reinterpret_cast<const float4*>(T + r * Cfg::kStageRow + 4 * qq);
+              float4 xv = xres[it];
+              xv.x += a.x; xv.y += a.y; xv.z += a.z; xv.w += a.w;
+              if (row0 + r < M) {
+                reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + (int64_t)(row0 + r) * ldc + col)[qq] = xv;
+                if constexpr (EPI == kEpiResidualNorm) {
+                  ssp[it] = fmaf(xv.x, xv.x, ssp[it]);
+                  ssp[it] = fmaf(xv.y, xv.y, ssp[it]);
+                  ssp[it] = fmaf(xv.z, xv.z, ssp[it]);
+                  ssp[it] = fmaf(xv.w, xv.w, ssp[it]);
+                  uint2 hv;
+                  hv.x = pack_bf16(xv.x * wv.x, xv.y * wv.y);
+                  hv.y = pack_bf16(xv.z * wv.z, xv.w * wv.w);
+                  reinterpret_cast<uint2*>(na.h_out + (int64_t)(row0 + r) * na.ld_h + col)[qq] = hv;
+                }
+              }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int it = 0; it < 8; ++it) xres[it] = xnext[it];
+          }
+          if constexpr (EPI == kEpiResidualNorm) {
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              float s_ = ssp[it];
+              s_ += __shfl_xor_sync(0xffffffffu, s_, 1);
+              s_ += __shfl_xor_sync(0xffffffffu, s_, 2);
+              s_ += __shfl_xor_sync(0xffffffffu, s_, 4);
+              const int r = it * 4 + (lane >> 3);
+              if (qq == 0 && row0 + r < M) na.ssq_out[(int64_t)(row0 + r) * num_n + n_blk] = s_;
+            }
+          }
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive_cluster(leader_tempty + acc * 8);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          continue;
+        }
       }
       const float rs = norm_row_scale(na, row, M);
       RopeRow rr;
@@ -834,7 +921,7 @@ template <int BN, int EPI, int MC, int KC>
 int launch_pair_mc(const GemmPlan& p, int M, cudaStream_t stream) {
   using Cfg = PairCfg<BN, KC>;
   auto kern = gemm_pair_kernel<BN, EPI, MC, KC>;
-  constexpr size_t smem = Cfg::kSmem + (kStagedEpi<BN, EPI> ? Cfg::kEpiStageBytes : 0);
+  constexpr size_t smem = Cfg::kSmem + (kStagedEpi<BN, EPI, KC> ? Cfg::kEpiStageBytes : 0);
   static_assert(smem <= 232448, "pair GEMM shared memory exceeds 227 KB");
   static bool attr_set = false;
   if (!attr_set) {
