@@ -1067,6 +1067,10 @@ int gemm_bf16_plan(GemmPlan* p, int M, int N, int K, const __nv_bfloat16* A, int
   int mc = 1;
   if (bn == 0) {
     pair = M >= 256;
+    // gate_up at M = 256j + (<= 128) rows (e.g. 64 prompts x 5 = 320): the
+    // last 256-row pair block would be mostly padding; 128-row single-CTA
+    // tiles waste less (7B 99 -> 90 us, 32B 200 -> 190 us at M = 320)
+    if (pair && epi == kEpiSwiGLU && M % 256 != 0 && M % 256 <= 128) pair = false;
     if (pair) choose_pair_tile(M, N, K, epi, &bn, &mc);
     else bn = N >= 4096 ? 256 : 128;
   } else if (bn < 0) {
