@@ -85,9 +85,34 @@ __device__ __forceinline__ RopeRow rope_row(const RopeArgs& ra, int row, int M) 
   return r;
 }
 
+// cos / sin of the 16 rotation pairs a q/k chunk at column `col` needs for
+// this row (loaded one chunk ahead of their use).
+struct RopeTab {
+  float4 c[4], s[4];
+};
+
+__device__ __forceinline__ RopeTab rope_tab(const RopeArgs& ra, const RopeRow& rr, int col) {
+  RopeTab tb;
+  const int hd = ra.hd, half = hd >> 1;
+  if (rr.info >= 0 && col < (ra.nq + ra.nkv) * hd) {
+    const int d0 = (col % hd) >> 1;
+    const float4* c4 = reinterpret_cast<const float4*>(ra.cos + (int64_t)rr.pos * half + d0);
+    const float4* s4 = reinterpret_cast<const float4*>(ra.sin + (int64_t)rr.pos * half + d0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      tb.c[q] = c4[q];
+      tb.s[q] = s4[q];
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tb.c[q] = tb.s[q] = make_float4(0, 0, 0, 0);
+  }
+  return tb;
+}
+
 // kEpiQkvRope for one 32-column chunk of one row (see RopeArgs).
 __device__ __forceinline__ void qkv_rope_chunk(const float* f, int row, int col, const RopeArgs& ra,
-                                               const RopeRow& rr) {
+                                               const RopeRow& rr, const RopeTab& tb) {
   const int info = rr.info;
   if (info < 0) return;  // padding row of the verify batch
   const int hd = ra.hd, half = hd >> 1;
@@ -98,13 +123,10 @@ __device__ __forceinline__ void qkv_rope_chunk(const float* f, int row, int col,
   __nv_bfloat16* kbase = (win ? ra.window : ra.cache) + rr.dst;
   if (col < hq + hk) {
     const int hc = col % hd, d0 = hc >> 1;  // 16 pairs (d0 + i, d0 + i + half)
-    const int pos = rr.pos;
-    const float4* c4 = reinterpret_cast<const float4*>(ra.cos + (int64_t)pos * half + d0);
-    const float4* s4 = reinterpret_cast<const float4*>(ra.sin + (int64_t)pos * half + d0);
     float y1[16], y2[16];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float4 c = c4[q], s = s4[q];
+      const float4 c = tb.c[q], s = tb.s[q];
       const float cs[4] = {c.x, c.y, c.z, c.w}, sn[4] = {s.x, s.y, s.z, s.w};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -155,7 +177,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, int row, int c
         f[4 * q] += b.x; f[4 * q + 1] += b.y; f[4 * q + 2] += b.z; f[4 * q + 3] += b.w;
       }
     }
-    qkv_rope_chunk(f, row, col, ra, rr);
+    qkv_rope_chunk(f, row, col, ra, rr, rope_tab(ra, rr, col));
     return;
   }
   float f[W];
@@ -812,9 +834,48 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           continue;
         }
       }
+      if constexpr (EPI == kEpiQkvRope) {
+        // RoPE epilogue: the row's KV destination and the first chunk's
+        // cos/sin are loaded while the mainloop runs; each later chunk's
+        // tables one chunk ahead of their use
+        static_assert(EPI != kEpiQkvRope || CW == 32, "RoPE chunks are 32 columns");
+        const RopeRow rq = rope_row(ra, row, M);
+        const float rsq = norm_row_scale(na, row, M);
+        RopeTab tb = rope_tab(ra, rq, n_blk * BN);
+        sm100::mbar_wait(&tfull[acc], acc_phase);
+        sm100::tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t v[32];
+          sm100::tmem_ld_32x32b_x32(taddr + c * 32, v);
+          const int col = n_blk * BN + c * 32;
+          RopeTab tn;
+          if (c + 1 < BN / 32) tn = rope_tab(ra, rq, col + 32);
+          sm100::tmem_ld_wait();
+          if (na.ssq_in != nullptr) scale_chunk<32>(v, rsq);
+          if (row < M && col < N) {
+            float f[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+            if (bias != nullptr) {
+              const float4* b4 = reinterpret_cast<const float4*>(bias + col);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const float4 b = b4[q];
+                f[4 * q] += b.x; f[4 * q + 1] += b.y; f[4 * q + 2] += b.z; f[4 * q + 3] += b.w;
+              }
+            }
+            qkv_rope_chunk(f, row, col, ra, rq, tb);
+          }
+          if (c + 1 < BN / 32) tb = tn;
+        }
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive_cluster(leader_tempty + acc * 8);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        continue;
+      }
       const float rs = norm_row_scale(na, row, M);
-      RopeRow rr;
-      if constexpr (EPI == kEpiQkvRope) rr = rope_row(ra, row, M);
       sm100::mbar_wait(&tfull[acc], acc_phase);
       sm100::tc_fence_after();
       float best = -INFINITY;
@@ -831,7 +892,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if constexpr (EPI == kEpiArgmax) {
           argmax_chunk<CW>(v, col, N, row, M, sa, best, best_idx);
         } else {
-          if (col < N) epilogue_chunk<EPI, CW>(v, row, col, M, N, C, ldc, bias, na, ss, ra, rr);
+          if (col < N) epilogue_chunk<EPI, CW>(v, row, col, M, N, C, ldc, bias, na, ss, ra);
         }
       }
       if constexpr (EPI == kEpiResidualNorm) {
