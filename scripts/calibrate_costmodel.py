@@ -69,7 +69,6 @@ def model_step_ms(m: DeviceModel, b: int, rows_per: int) -> float:
 
 def ngram_ms(b: int, k: int) -> float:
     lib = _native.lib()
-    st = _native.stream_handle()
     L = CTX + 64
     tokens = torch.randint(0, 200, (b, L), dtype=torch.int32, device="cuda")
     lens = torch.full((b,), CTX, dtype=torch.int32, device="cuda")
@@ -78,7 +77,7 @@ def ngram_ms(b: int, k: int) -> float:
     scratch = torch.zeros(2 * b, dtype=torch.int64, device="cuda")
     return graph_ms(lambda: _native.check(lib.sr_ngram_propose(
         b, tokens.data_ptr(), L, lens.data_ptr(), 1, 3, k, drafts.data_ptr(), nd.data_ptr(),
-        scratch.data_ptr(), st), "ngram"))
+        scratch.data_ptr(), _native.stream_handle()), "ngram"))   # the capture stream
 
 
 def main():
