@@ -178,7 +178,9 @@ class DraftSide:
     def _apply(self) -> None:
         verified = self.in_verified > 0
         accepted, committed, ctoks = self.in_accepted, self.in_committed, self.in_ctoks
-        full = verified & (accepted == self.inflight)
+        # an empty window (nothing proposed) that committed the target's token
+        # leaves its successor misaligned by one: treat it as rejected
+        full = verified & (accepted == self.inflight) & ((self.inflight > 0) | (committed == 0))
         part = verified & ~full
         # partial: accepted prefix + corrected token
         pos = (self.seq_len + accepted).clamp(max=self.stride - 1).long()
@@ -196,7 +198,8 @@ class DraftSide:
 
     def draft(self) -> tuple[torch.Tensor, torch.Tensor]:
         """Next window of every request: successor of the in-flight one, or
-        fresh.  Returns (drafts [B, k], nd [B]); nd = 0 means no window."""
+        fresh.  Returns (drafts [B, k], nd [B]); nd = 0 is an empty window
+        (nothing proposed: verifying it commits the target's next token)."""
         if not self.use_graphs:
             self._draft()
         elif self._g_draft is None:
@@ -280,9 +283,11 @@ class VerifySide:
     def _receive(self) -> None:
         verified = self.out_verified > 0
         nd = self.in_nd
-        full = verified & (self.out_accepted == self.rows[:, 0])
+        full = verified & (self.out_accepted == self.rows[:, 0]) & ((self.rows[:, 0] > 0) | (self.out_committed == 0))
         part = verified & ~full
-        ok = (~verified | full) & (nd > 0)
+        # nd == 0 (the drafter proposed nothing) is still a window: verifying
+        # it commits the target's next token, as a plain decode step would
+        ok = (~verified | full) & (nd >= 0)
         self.pending.copy_(self.in_drafts)
         self.pending_nd.copy_(torch.where(ok, nd, torch.full_like(nd, -1)))
         self.rows[:, 3] += torch.where(part, nd, torch.zeros_like(nd))

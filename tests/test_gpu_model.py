@@ -437,6 +437,28 @@ def test_decoupled_small_model_drafter_equals_plain(same_weights):
         assert full < 1.0
 
 
+def test_decoupled_ngram_drafter_equals_plain():
+    """The real n-gram drafter (K4) on the drafter side of decoupled mode:
+    random prompts often give no proposal -- an empty window still commits
+    the target's token (and discards its misaligned successor) -- and
+    repetitive prompts give accepted drafts.  Output == plain greedy."""
+    from paper_2511_16193_b200.decoupled import run_local
+    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine
+
+    B, k = 6, 4
+    s, w, m = make("tiny", "bf16", B=B, max_len=256)
+    prompts = prompts_for(s.vocab, B, 21, alphabet=6)   # repetitive: n-gram matches
+    prompts[0] = np.random.default_rng(3).integers(0, s.vocab, 30).astype(np.int32)  # no matches
+    max_new = [20, 35, 40, 12, 33, 25]
+    plain = RolloutEngine(m, prompts, max_new, k=0, history=1)
+    plain.prefill()
+    plain.run()
+    truth = plain.outputs()
+    outs, rows = run_local(m, prompts, max_new, k, NgramDrafter(1, 3))
+    assert outs == truth
+    assert int(rows[:, :, 1].clip(min=0).sum()) > 0      # some drafts accepted
+
+
 def test_configs2_7b_shape_bon_ngram_and_model_drafters():
     """configs[2] widths (Qwen2.5-7B: H 3584, I 18944, 28/4 heads, G = 7), 2
     layers: Best-of-N with n-gram + small-model (0.5B-shaped) drafters commits
