@@ -108,6 +108,8 @@ def test_f32_gemm(M, N, K):
 PAIR_CASES = [(1280, 1536, 1536, -112), (1280, 2048, 1536, -160), (300, 1000, 192, -112),
               (77, 512, 8960, -128), (1280, 17920, 1536, -256), (513, 3000, 640, -96),
               (256, 4096, 256, -224), (1000, 768, 896, -64), (1280, 1536, 8960, -192),
+              # wide (> 128) residual tiles with ragged rows / a partial last tile
+              (300, 1000, 192, -256), (77, 3584, 640, -192),
               # two pairs per cluster, A multicast (-(1024 + width)); odd tile counts included
               (1280, 1536, 8960, -1152), (1280, 2048, 1536, -1184), (300, 1000, 192, -1136),
               (77, 512, 8960, -1152), (1280, 17920, 1536, -1280), (1000, 768, 896, -1088)]
