@@ -299,10 +299,15 @@ int sr_draft_model_batch(int num_requests, int k, int step, const int32_t* token
  * own [B, k] block); both NULL = plain decode; ndraft < 0 = the request has
  * no window this round (decoupled gap round, sim.py:1076-1080).  window
  * [B] (optional): per-request window w_r <= k, the mixed-window batch of
- * request-level reconfiguration (planner.py:223-272); NULL = k for all. */
+ * request-level reconfiguration (planner.py:223-272); NULL = k for all.
+ * max_new_cap [B] (optional): max_new is clamped to it IN PLACE first --
+ * the token row and KV pages of request b hold max_new_cap[b] outputs, and a
+ * retired request (cap = gen_len) stays retired whatever budget the host
+ * copies in. */
 int sr_build_verify_batch(int num_requests, int num_drafters, int k, const int32_t* tokens,
                           int64_t tok_stride, const int32_t* seq_len, const int32_t* gen_len,
-                          const int32_t* max_new, const int32_t* drafts, const int32_t* ndraft,
+                          int32_t* max_new, const int32_t* max_new_cap, const int32_t* drafts,
+                          const int32_t* ndraft,
                           const int32_t* window, int32_t* token_ids, int32_t* positions, void* seqs,
                           sr_stream_t stream);
 

@@ -47,7 +47,7 @@ SIGNATURES: dict[str, list] = {
     "sr_draft_model_batch": [_i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                              _vp, _vp, _vp],
     "sr_pack_results": [_i32, _i32, _vp, _vp, _i64, _vp, _vp, _vp],
-    "sr_build_verify_batch": [_i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+    "sr_build_verify_batch": [_i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               _vp, _vp, _vp],
 }
 _RESTYPES = {"sr_last_error": ctypes.c_char_p, "sr_model_workspace_bytes": ctypes.c_uint64,

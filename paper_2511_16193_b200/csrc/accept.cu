@@ -112,7 +112,8 @@ __global__ void kv_commit_kernel(int N, const SeqInfo* __restrict__ seqs, const 
 // [s*(k+1), s*(k+1) + nd + 1): the last committed token then its drafts.
 __global__ void build_verify_kernel(int B, int N, int k, const int32_t* __restrict__ tokens, int64_t tok_stride,
                                     const int32_t* __restrict__ seq_len, const int32_t* __restrict__ gen_len,
-                                    const int32_t* __restrict__ max_new, const int32_t* __restrict__ drafts,
+                                    int32_t* __restrict__ max_new, const int32_t* __restrict__ max_new_cap,
+                                    const int32_t* __restrict__ drafts,
                                     const int32_t* __restrict__ ndraft, const int32_t* __restrict__ window,
                                     int32_t* __restrict__ token_ids, int32_t* __restrict__ positions,
                                     SeqInfo* __restrict__ seqs) {
@@ -120,7 +121,15 @@ __global__ void build_verify_kernel(int B, int N, int k, const int32_t* __restri
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= B * N) return;
   const int b = s / N, n = s % N;
-  const int remaining = max_new[b] - gen_len[b];
+  // budgets arrive from the host each step (capture_io); the engine's token
+  // row and KV pages were sized for max_new_cap, so clamp in place (thread
+  // n == 0 stores; every thread of b computes the same value)
+  int mn = max_new[b];
+  if (max_new_cap != nullptr) {
+    mn = min(mn, max_new_cap[b]);
+    if (n == 0) max_new[b] = mn;
+  }
+  const int remaining = mn - gen_len[b];
   const int L = seq_len[b];
   int nd = 0;
   bool active = remaining > 0;
@@ -321,7 +330,8 @@ extern "C" int sr_draft_model_batch(int num_requests, int k, int step, const int
 
 extern "C" int sr_build_verify_batch(int num_requests, int num_drafters, int k, const int32_t* tokens,
                                      int64_t tok_stride, const int32_t* seq_len, const int32_t* gen_len,
-                                     const int32_t* max_new, const int32_t* drafts, const int32_t* ndraft,
+                                     int32_t* max_new, const int32_t* max_new_cap, const int32_t* drafts,
+                                     const int32_t* ndraft,
                                      const int32_t* window, int32_t* token_ids, int32_t* positions,
                                      void* seqs, sr_stream_t stream) {
   SR_REQUIRE(num_requests >= 0 && num_drafters >= 1 && k >= 0, "bad batch shape");
@@ -330,7 +340,8 @@ extern "C" int sr_build_verify_batch(int num_requests, int num_drafters, int k, 
   SR_REQUIRE(drafts == nullptr || ndraft != nullptr, "drafts without ndraft");
   const int S = num_requests * num_drafters;
   sr::launch_k(sr::build_verify_kernel, sr::ceil_div(S, 128), 128, 0, (cudaStream_t)stream, 
-      num_requests, num_drafters, k, tokens, tok_stride, seq_len, gen_len, max_new, drafts, ndraft, window,
+      num_requests, num_drafters, k, tokens, tok_stride, seq_len, gen_len, max_new, max_new_cap, drafts, ndraft,
+      window,
       token_ids, positions, reinterpret_cast<sr::SeqInfo*>(seqs));
   return sr::check_launch("build_verify_kernel");
 }

@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <type_traits>
+#include <cstdio>
 #include <cstdlib>
 
 namespace sr {
@@ -101,8 +102,18 @@ struct AttnArgs {
 };
 
 int g_split_tiles = [] {  // 2048-key splits (SR_ATTN_SPLIT overrides, for tuning)
+  // SR_ATTN_SPLIT counts 64-key TILES, like sr_set_attention_split, and gets
+  // the same [4, 1024] check: hist[] in attn_plan_kernel holds 1025 entries
+  // and the workspace bound assumes >= 4 tiles per split.  Out-of-range
+  // values are ignored (with a warning) rather than clamped silently.
   const char* v = getenv("SR_ATTN_SPLIT");
-  return v ? atoi(v) : 32;
+  if (!v) return 32;
+  const int t = atoi(v);
+  if (t < 4 || t > 1024) {
+    fprintf(stderr, "specrollout_b200: SR_ATTN_SPLIT=%s ignored (64-key tiles, must be in [4, 1024])\n", v);
+    return 32;
+  }
+  return t;
 }();
 
 __device__ __forceinline__ int block_max_key(const SeqInfo& sq, int r0, int rows, int G) {

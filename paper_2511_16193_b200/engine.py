@@ -107,6 +107,15 @@ class ModelDrafter:
         self.out = torch.zeros(B, dtype=torch.int32, device=dev)
         prefill_model(self.m, eng.tokens, [L - 1 for L in eng.prompt_lens])
 
+    def reset_slot(self, b: int) -> None:
+        """Rebuild slot ``b``'s drafter cache from the engine's token row (a
+        request was migrated into it): KV of [0, seq_len - 1), the catch-up
+        step then feeds the last committed token."""
+        L = int(self.eng.seq_len[b])
+        if L > 1:
+            prefill_model(self.m, self.eng.tokens, {b: L - 1})
+        self.dkv_len[b] = L - 1
+
     def enqueue(self, drafts, ndraft) -> None:
         e, lib, st = self.eng, self.eng.lib, _native.stream_handle()
         for step in range(e.k + 1):
@@ -124,12 +133,14 @@ class ModelDrafter:
 
 def prefill_model(m: DeviceModel, tokens, lens) -> None:
     """Chunked prompt forward writing KV for positions [0, lens[b]) of every
-    request b into ``m``'s paged cache (the logits are not needed).  Prompts
-    longer than the model's ``max_tokens`` are split into pieces; a piece
-    attends to its request's earlier pieces through the cache."""
+    request b into ``m``'s paged cache (the logits are not needed).  ``lens``
+    is a list over all slots or a ``{slot: length}`` dict (re-prefill of
+    single slots).  Prompts longer than the model's ``max_tokens`` are split
+    into pieces; a piece attends to its request's earlier pieces through the
+    cache."""
     dev = tokens.device
     pieces = []
-    for b, L in enumerate(lens):
+    for b, L in (lens.items() if isinstance(lens, dict) else enumerate(lens)):
         off = 0
         while off < L:
             n = min(m.max_tokens, L - off)
@@ -196,6 +207,10 @@ class RolloutEngine:
         self.seq_len = torch.tensor(lens, dtype=torch.int32, device=dev)
         self.gen_len = torch.zeros(self.B, dtype=torch.int32, device=dev)
         self.max_new = torch.tensor(max_new, dtype=torch.int32, device=dev)
+        # capacity of each slot (its token row / KV pages were sized for it):
+        # every step clamps max_new to it on device, so host budgets copied in
+        # by capture_io cannot overflow a row, and retire() is permanent
+        self.max_new_cap = self.max_new.clone()
         S, R = self.B * self.N, self.B * self.N * (k + 1)
         self.drafts = torch.full((self.N, self.B, k), -1, dtype=torch.int32, device=dev)
         self.ndraft = torch.zeros((self.N, self.B), dtype=torch.int32, device=dev)
@@ -251,7 +266,8 @@ class RolloutEngine:
             drafts_ptr, nd_ptr = self.drafts.data_ptr(), self.ndraft.data_ptr()
         _native.check(lib.sr_build_verify_batch(
             self.B, self.N, self.k, self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(),
-            self.gen_len.data_ptr(), self.max_new.data_ptr(), drafts_ptr, nd_ptr, self.window.data_ptr(),
+            self.gen_len.data_ptr(), self.max_new.data_ptr(), self.max_new_cap.data_ptr(), drafts_ptr, nd_ptr,
+            self.window.data_ptr(),
             self.token_ids.data_ptr(), self.positions.data_ptr(), self.seqs.data_ptr(), st),
             "sr_build_verify_batch")
         self.m.forward(self.token_ids, self.positions, self.seqs, num_seqs=self.B * self.N,
@@ -297,7 +313,9 @@ class RolloutEngine:
         """Host-facing step as one CUDA graph: H2D of the per-request budgets
         (``budget_host``, pinned int32 [B]), the speculation step, and D2H of
         each request's outcome row and its next k+2 token slots
-        (``result_host``, pinned int32 [B, 4 + k + 2]).  :meth:`step_io`
+        (``result_host``, pinned int32 [B, 4 + k + 2]).  Budgets are clamped
+        on device to the constructor's ``max_new`` (:attr:`max_new_cap`): a
+        larger host budget cannot grow a request past its slot.  :meth:`step_io`
         replays the latest one (or pass the returned graph); the caller waits
         for the step (synchronize or an event recorded after the replay)
         before reading ``result_host``.  Capturing two graphs over two result
@@ -333,6 +351,13 @@ class RolloutEngine:
     def step_io(self, graph=None) -> None:
         (graph or self.graph_io).replay()
         self.steps += 1
+
+    def retire(self, b: int) -> None:
+        """Stop request ``b`` where it is (its slot was migrated away): budget
+        and capacity both drop to the generated length, so no later host
+        budget revives it."""
+        self.max_new[b] = self.gen_len[b]
+        self.max_new_cap[b] = self.gen_len[b]
 
     def set_windows(self, windows) -> None:
         """Per-request window caps in [0, k] (0 = plain decoding for that

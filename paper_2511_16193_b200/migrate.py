@@ -50,18 +50,43 @@ def pack_request(eng, b: int) -> dict:
     }
 
 
+def _check_room(eng, seq_len: int, gen_len: int, max_new: int, n: int) -> None:
+    """The destination slot must hold the request to its END, not just its
+    current length: its remaining budget is written into the token row and
+    the KV pages, and attention runs with the engine's ``max_key``."""
+    final = seq_len + max(0, max_new - gen_len)
+    if final + eng.k + 2 > min(eng.stride, eng.max_key + 1) or n > eng.m.pages_per_req:
+        raise ConfigError(f"destination engine sized for {min(eng.stride, eng.max_key + 1)} positions per "
+                          f"request; the migrated request needs {final + eng.k + 2}")
+
+
 def unpack_request(eng, b: int, st: dict) -> None:
-    """Install a packed request into slot ``b`` of ``eng`` (same model shape)."""
+    """Install a packed request into slot ``b`` of ``eng`` (same model shape).
+
+    Host and drafter state of the slot follow the new occupant: the prompt
+    length (``outputs()`` slices at it), the slot capacity, and a model
+    drafter's cache (re-prefilled from the token row).  A synthetic drafter
+    proposes from a per-slot truth row of the previous occupant, so slots of
+    such engines cannot take migrated requests."""
+    from .engine import ModelDrafter, SyntheticDrafter
+
     seq_len, gen_len, max_new, n = (int(x) for x in st["lens"].tolist())
-    if seq_len + eng.k + 2 > eng.stride or n > eng.m.pages_per_req:
-        raise ConfigError("destination slot too small for the migrated request")
+    _check_room(eng, seq_len, gen_len, max_new, n)
+    if any(isinstance(d, SyntheticDrafter) for d in eng.drafters):
+        raise ConfigError("engines with a synthetic drafter hold per-slot truth rows; migrate into an "
+                          "engine with n-gram or model drafters")
     eng.tokens[b, :seq_len].copy_(st["tokens"][:seq_len])
     eng.seq_len[b] = seq_len
     eng.gen_len[b] = gen_len
     eng.max_new[b] = max_new
+    eng.max_new_cap[b] = max_new
+    eng.prompt_lens[b] = seq_len - gen_len
     if n:
         pages = eng.m.block_table[b, :n].long()
         eng.m.kv_cache[:, pages] = st["kv"][:, :n].to(eng.m.kv_cache.device)
+    for d in eng.drafters:
+        if isinstance(d, ModelDrafter) and d.eng is eng:
+            d.reset_slot(b)
 
 
 def migrate_local(src, b_src: int, dst, b_dst: int) -> int:
@@ -73,7 +98,7 @@ def migrate_local(src, b_src: int, dst, b_dst: int) -> int:
     if src.dev != dst.dev:
         st = {k: v.to(dst.dev, non_blocking=True) for k, v in st.items()}
     unpack_request(dst, b_dst, st)
-    src.max_new[b_src] = src.gen_len[b_src]
+    src.retire(b_src)
     return sum(v.numel() * v.element_size() for v in st.values())
 
 
@@ -93,7 +118,7 @@ def send_requests(dist, eng, bs: list[int], peer: int) -> int:
     for w in dist.batch_isend_irecv(ops):
         w.wait()
     for b in bs:
-        eng.max_new[b] = eng.gen_len[b]
+        eng.retire(b)
     return meta.numel() * 4 + toks.numel() * 4 + kv.numel() * kv.element_size()
 
 

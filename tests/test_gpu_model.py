@@ -591,6 +591,82 @@ def test_migrate_requests_between_engines():
     assert [out[perm[b]] for b in range(B)] == plain.outputs()
 
 
+def test_migrate_into_smaller_engine_rejected():
+    """A destination slot must hold the request's whole remaining budget, not
+    only its current length (a long straggler moved into an engine
+    sized for shorter requests would write past its token row)."""
+    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine
+    from paper_2511_16193_b200.errors import ConfigError
+    from paper_2511_16193_b200.migrate import migrate_local
+
+    s, w, m = make("tiny", "bf16", B=4)
+    prompts = prompts_for(s.vocab, 2, 8, lo=30, hi=31)
+    src = RolloutEngine(m, prompts[:1], [120], k=4, drafters=(NgramDrafter(),), history=8)
+    src.prefill()
+    src.step()
+    dst = RolloutEngine(m, prompts[1:], [8], k=4, drafters=(NgramDrafter(),), history=8)
+    with pytest.raises(ConfigError):
+        migrate_local(src, 0, dst, 0)
+    assert not src.done()           # a refused move leaves the source untouched
+
+
+def test_migrate_updates_slot_state_and_budget_cap():
+    """Unpack follows the new occupant: prompt length (outputs() slicing), the
+    slot capacity, a model drafter's cache; the retired source slot stays
+    retired even when the host-facing graph copies the old budgets in."""
+    from paper_2511_16193_b200.engine import ModelDrafter, NgramDrafter, RolloutEngine
+    from paper_2511_16193_b200.migrate import migrate_local
+    from paper_2511_16193_b200.model import DeviceModel
+
+    B = 2
+    s, w, m1 = make("tiny", "bf16", B=B)
+    m2 = DeviceModel(s, w, dtype="bf16", max_requests=B, max_len=512, max_tokens=512, max_seqs=B * 3)
+    md = DeviceModel(s, w, dtype="bf16", max_requests=B, max_len=512, max_tokens=512, max_seqs=B * 3)
+    prompts = prompts_for(s.vocab, 4, 12)
+    max_new = [60, 55]
+    plain, _ = run_engine(m1, prompts[:2], max_new, k=0)
+    src = RolloutEngine(m1, prompts[:2], max_new, k=4, drafters=(NgramDrafter(),), history=1)
+    src.prefill()
+    budget_h = torch.tensor(max_new, dtype=torch.int32).pin_memory()
+    res_h = torch.zeros((B, 4 + 6), dtype=torch.int32).pin_memory()
+    g = src.capture_io(budget_h, res_h)
+    for _ in range(3):
+        src.step_io(g)
+    # destination: other prompts (different lengths) and a model drafter that
+    # uses the target's own weights (drafts == target tokens once in sync)
+    dst = RolloutEngine(m2, prompts[2:], [70, 70], k=4, drafters=(ModelDrafter(md),), history=64)
+    dst.prefill()
+    migrate_local(src, 1, dst, 0)
+    torch.cuda.synchronize()
+    assert dst.prompt_lens[0] == len(prompts[1])
+    for _ in range(4):              # host budgets copied in again: slot 1 must not revive
+        src.step_io(g)
+    torch.cuda.synchronize()
+    assert int(src.gen_len[1]) == int(src.max_new[1]) == int(src.max_new_cap[1])
+    steps = dst.run()
+    assert dst.outputs()[0] == plain.outputs()[1]
+    rows = dst.outcome_rows(steps)
+    # the re-prefilled drafter cache proposes the target's tokens: windows accept
+    assert rows[:, 0, 1].sum() > 0.8 * rows[:, 0, 0].sum()
+
+
+def test_capture_io_budget_clamped_to_capacity():
+    """A host budget above the constructor's max_new is clamped on device."""
+    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine
+
+    s, w, m = make("tiny", "bf16", B=2)
+    prompts = prompts_for(s.vocab, 2, 13)
+    eng = RolloutEngine(m, prompts, [9, 5], k=4, drafters=(NgramDrafter(),), history=1)
+    eng.prefill()
+    budget_h = torch.tensor([10_000, 10_000], dtype=torch.int32).pin_memory()
+    res_h = torch.zeros((2, 4 + 6), dtype=torch.int32).pin_memory()
+    g = eng.capture_io(budget_h, res_h)
+    for _ in range(30):
+        eng.step_io(g)
+    torch.cuda.synchronize()
+    assert eng.gen_len.tolist() == [9, 5]
+
+
 def test_prefill_prompts_longer_than_max_tokens():
     """Chunked prefill: prompts longer than the model's max_tokens are split
     into pieces; decoding afterwards matches a model that prefilled them whole."""
