@@ -242,7 +242,7 @@ int sr_model_forward(void* handle, const sr_forward_args* args, sr_stream_t stre
 int sr_model_profile(void* handle, int enable, float* ms_out, int32_t* count_out);
 
 /* ---------------------------------------------------------------------------
- * K3  Acceptance + Best-of-N + write-back (model mode).  Replaces
+ * K3  Acceptance + Best-of-N + write-back (model mode), ONE kernel.  Replaces
  * `_verify_prefix` / `_apply_outcome` / `commit` (sim.py:977-1042, 340-353)
  * with real tokens, and the Best-of-N first-finisher (sim.py:340-361) with an
  * in-forward longest-accepted-prefix select over N drafters per request.
@@ -251,23 +251,46 @@ int sr_model_profile(void* handle, int enable, float* ms_out, int32_t* count_out
  * the verify inputs (slot j+1 holds draft d_{j+1}); target [M] the target
  * model's token per row.  Commits into tokens [B, tok_stride] at seq_len,
  * advances seq_len / gen_len (capped by max_new), and writes outcome
- * [B*N, 4] = (proposed, accepted, committed, wasted) and bon [B] (winner,
- * -1 = request inactive).
+ * [B*N, 4] (16-byte aligned) = (proposed, accepted, committed, wasted) and
+ * bon [B] (winner, -1 = request inactive).  When the winner verified in a
+ * drafter branch (N > 1), its committed slots' KV is copied from the
+ * model's branch window into the paged cache in the same kernel; `model`
+ * (the sr_model_create handle) NULL skips that write-back (N == 1, or every
+ * sequence verified in place, branch < 0).
  * ------------------------------------------------------------------------- */
-int sr_accept_commit(int num_requests, int num_drafters, const void* seqs, const int32_t* token_ids,
-                     const int32_t* target, int32_t* tokens, int64_t tok_stride, int32_t* seq_len,
-                     int32_t* gen_len, const int32_t* max_new, int bonus_token, int32_t* outcome,
-                     int32_t* bon, sr_stream_t stream);
+int sr_accept_commit(void* model, int num_requests, int num_drafters, const void* seqs,
+                     const int32_t* token_ids, const int32_t* target, int32_t* tokens, int64_t tok_stride,
+                     int32_t* seq_len, int32_t* gen_len, const int32_t* max_new, int bonus_token,
+                     int32_t* outcome, int32_t* bon, sr_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * K3, rejection-sampling mode (distribution-preserving speculative sampling,
+ * Leviathan et al.; semantics of vLLM 0.22 rejection_sampler.py:708-760,
+ * SURVEY §8c) for ONE stochastic drafter per request (N = 1): the model-mode
+ * counterpart of the reference's keyed acceptance draw (sim.py:322-336) when
+ * the drafter samples its window from its own distribution q.
+ *
+ * p_logits [M, ldp] f32: the target's verify-row logits (row q_start + j).
+ * q_logits f32: the drafter's logits behind draft j of request b at
+ *   q_logits + (j * B + b) * ldq  ([k, B, ldq]).
+ * Draft j is accepted iff u < p_j(d)/q_j(d) (u keyed by seed, request,
+ * position); the first rejected slot commits a sample of
+ * norm(max(0, p_j - q_j)); a full accept commits the bonus (if on) as the
+ * target's keyed sample of p_n; an empty window commits the keyed sample of
+ * p_0.  p, q = softmax(logits / temperature).  Commits, outcome rows and bon
+ * as sr_accept_commit.  stats: f32 workspace [M, 4] (16-byte aligned).
+ * ------------------------------------------------------------------------- */
+int sr_accept_rejection(int num_requests, int k, const void* seqs, const int32_t* token_ids,
+                        const float* p_logits, int64_t ldp, const float* q_logits, int64_t ldq, int vocab,
+                        float temperature, uint32_t seed, int32_t* tokens, int64_t tok_stride,
+                        int32_t* seq_len, int32_t* gen_len, const int32_t* max_new, int bonus_token,
+                        float* stats, int32_t* outcome, int32_t* bon, sr_stream_t stream);
 
 /* Host-facing step result (RolloutEngine.capture_io): out [B, 4 + width] =
  * outcome row b (first 4 ints) then tokens[b, seq_before[b] + j] for
  * j < width (clamped to the row) -- the committed window of the step. */
 int sr_pack_results(int num_requests, int width, const int32_t* outcome, const int32_t* tokens,
                     int64_t tok_stride, const int32_t* seq_before, int32_t* out, sr_stream_t stream);
-
-/* Copy the winning branch's window KV into the paged cache (all layers). */
-int sr_kv_commit(void* model, int num_requests, int num_drafters, const void* seqs,
-                 const int32_t* outcome, const int32_t* bon, sr_stream_t stream);
 
 /* Reference-acceptance drafter: for output position
  * g = gen_len[b] + j propose truth[b, g] (the target's own greedy token) when
@@ -286,12 +309,14 @@ int sr_synthetic_draft(int num_requests, int k, const int32_t* truth, int64_t tr
  * drafter has not cached, [dkv_len, seq_len) (advances dkv_len), logits at
  * the last one; step j in [1, k): decode the previous draft; step k: file the
  * last output and write ndraft.  prev_out [B] is the previous forward's
- * output and becomes draft (step-1).  drafts [B, k], ndraft [B]. */
+ * output and becomes draft (step-1).  drafts [B, k], ndraft [B].  key_pos
+ * [B] (optional): the output position of each request's logit row (the
+ * sampling key of a drafter that samples its own window, sr_sample_rows). */
 int sr_draft_model_batch(int num_requests, int k, int step, const int32_t* tokens, int64_t tok_stride,
                          const int32_t* seq_len, const int32_t* gen_len, const int32_t* max_new,
                          int32_t* dkv_len, const int32_t* prev_out, int32_t* drafts, int32_t* ndraft,
                          int32_t* token_ids, int32_t* positions, void* seqs, int32_t* logit_rows,
-                         sr_stream_t stream);
+                         int32_t* key_pos, sr_stream_t stream);
 
 /* Next verify batch from device state: for drafter n of request b, rows
  * [(b*N+n)*(k+1), +nd+1) = last committed token then the drafts.  drafts

@@ -52,6 +52,21 @@ class Qwen2Oracle:
         self.cos = torch.from_numpy(cos).to(self.acc)
         self.sin = torch.from_numpy(sin).to(self.acc)
 
+    def accumulating_in(self, dtype) -> "Qwen2Oracle":
+        """The same oracle (same weights, same bf16 rounding points) with its
+        GEMMs / reductions accumulated in ``dtype``.  bf16 results depend on
+        accumulation order, so comparing the fp32- and fp64-accumulating
+        variants measures the spread any two bf16 implementations can show
+        (the noise floor of GPU-vs-oracle bf16 parity)."""
+        import copy
+
+        o = copy.copy(self)
+        for name in ("embed", "lm_head", "final_norm", "cos", "sin"):
+            setattr(o, name, getattr(self, name).to(dtype))
+        o.layers = [{k: v.to(dtype) for k, v in L.items()} for L in self.layers]
+        o.acc = dtype
+        return o
+
     def _r(self, t):
         return t.bfloat16().to(self.acc) if self.bf16 else t
 
@@ -152,6 +167,78 @@ class Qwen2Oracle:
             out += y[:c]
             seq += y[:c]
         return out, rows
+
+
+    def spec_decode_bon(self, prompt, max_new: int, k: int, drafters, bonus: bool = False, sample=None):
+        """Best-of-N speculative decode with exact-match verification.
+
+        Every window, each of the N ``drafters`` (callables ``(seq, limit) ->
+        draft tokens``) proposes from the same committed context; the target
+        verifies each proposal (its token at every window position); the
+        drafter with the longest accepted prefix wins, ties to the lowest
+        index (incumbent first) -- the reference's first-finisher over
+        replicas that share one committed sequence (sim.py:340-361; replicas
+        from bon.py:79-139), collapsed into one window.  The winner's
+        window commits by the reference rule (sim.py:983-1042).
+
+        Returns (output tokens, windows, winners): ``windows[i]`` holds the N
+        outcome rows (proposed, accepted, committed, wasted) of window i --
+        losers commit 0 and waste their whole proposal, the winner wastes
+        n - a - 1 on a partial accept (sim.py:1001-1010) -- and
+        ``winners[i]`` the winning drafter index.
+        """
+        seq = list(prompt)
+        out, windows, winners = [], [], []
+        while len(out) < max_new:
+            remaining = max_new - len(out)
+            lim = min(k, remaining)
+            res = []
+            for dr in drafters:
+                d = list(dr(list(seq), lim))[:lim]
+                lg = self.logits(seq + d)
+                y = [self._pick(lg[len(seq) - 1 + j], len(seq) + j, sample) for j in range(len(d) + 1)]
+                a = 0
+                while a < len(d) and d[a] == y[a]:
+                    a += 1
+                res.append((len(d), a, y))
+            win = max(range(len(res)), key=lambda i: (res[i][1], -i))
+            n, a, y = res[win]
+            c = 1 if n == 0 else (n + (1 if bonus else 0) if a == n else a + 1)
+            c = min(c, remaining)
+            rows = []
+            for i, (ni, ai, _) in enumerate(res):
+                if i == win:
+                    rows.append((ni, ai, c, 0 if ai == ni else max(ni - ai - 1, 0)))
+                else:
+                    rows.append((ni, ai, 0, ni))
+            windows.append(rows)
+            winners.append(win)
+            out += y[:c]
+            seq += y[:c]
+        return out, windows, winners
+
+
+def ngram_drafter(k: int, min_n: int = 1, max_n: int = 3, max_model_len: int | None = None):
+    """Oracle n-gram drafter for :meth:`Qwen2Oracle.spec_decode_bon`."""
+    return lambda seq, lim: ngram_oracle.propose(seq, min_n, max_n, k, max_model_len)[:lim]
+
+
+class ModelDrafterOracle:
+    """Oracle small-model drafter: ``limit`` autoregressive steps of a draft
+    decoder from the committed context (greedy, or the keyed sample with the
+    target's noise at the same output positions -- the GPU ModelDrafter's
+    Gumbel coupling)."""
+
+    def __init__(self, oracle: Qwen2Oracle, sample=None):
+        self.o = oracle
+        self.sample = sample
+
+    def __call__(self, seq, lim):
+        d = []
+        for j in range(lim):
+            lg = self.o.logits(seq + d)[-1]
+            d.append(self.o._pick(lg, len(seq) + j, self.sample))
+        return d
 
 
 def margin(logits_row: torch.Tensor) -> float:

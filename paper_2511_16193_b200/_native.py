@@ -41,11 +41,12 @@ SIGNATURES: dict[str, list] = {
     "sr_model_forward": [_vp, _vp, _vp],
     "sr_model_profile": [_vp, _i32, _vp, _vp],
     "sr_launch_count": [],
-    "sr_accept_commit": [_i32, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp],
-    "sr_kv_commit": [_vp, _i32, _i32, _vp, _vp, _vp, _vp],
+    "sr_accept_commit": [_vp, _i32, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp],
     "sr_synthetic_draft": [_i32, _i32, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i32, _vp, _vp, _vp],
     "sr_draft_model_batch": [_i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                             _vp, _vp, _vp],
+                             _vp, _vp, _vp, _vp],
+    "sr_accept_rejection": [_i32, _i32, _vp, _vp, _vp, _i64, _vp, _i64, _i32, ctypes.c_float, ctypes.c_uint32,
+                            _vp, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp],
     "sr_pack_results": [_i32, _i32, _vp, _vp, _i64, _vp, _vp, _vp],
     "sr_build_verify_batch": [_i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               _vp, _vp, _vp],

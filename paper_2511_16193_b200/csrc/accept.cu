@@ -18,93 +18,112 @@
 
 namespace sr {
 
+int model_kv_layout(void* handle, KvLayout* kv, int* dtype);  // model.cu
+
 namespace {
 
-__global__ void accept_commit_kernel(int B, int N, const SeqInfo* __restrict__ seqs,
-                                     const int32_t* __restrict__ token_ids,
-                                     const int32_t* __restrict__ target, int32_t* __restrict__ tokens,
-                                     int64_t tok_stride, int32_t* __restrict__ seq_len,
-                                     int32_t* __restrict__ gen_len, const int32_t* __restrict__ max_new,
-                                     int bonus, int32_t* __restrict__ outcome,
-                                     int32_t* __restrict__ bon) {
+// K3, fused: one CTA per request.  Warp 0 finds every drafter's accepted
+// prefix (lane n = drafter n), picks the Best-of-N winner, commits its tokens
+// and writes the outcome rows; then, when the winner verified in a drafter
+// branch (its window KV sits in the branch buffer, not in the paged cache),
+// the whole CTA copies the committed slots' K and V of every layer into the
+// cache with 16-byte vector moves (swizzled chunk -> swizzled chunk).
+template <typename T>
+__global__ void __launch_bounds__(128)
+accept_commit_kernel(int B, int N, const SeqInfo* __restrict__ seqs, const int32_t* __restrict__ token_ids,
+                     const int32_t* __restrict__ target, int32_t* __restrict__ tokens, int64_t tok_stride,
+                     int32_t* __restrict__ seq_len, int32_t* __restrict__ gen_len,
+                     const int32_t* __restrict__ max_new, int bonus, int32_t* __restrict__ outcome,
+                     int32_t* __restrict__ bon, KvLayout kv) {
   grid_dep_sync();
-  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int b = blockIdx.x;
   const int lane = threadIdx.x & 31;
-  if (b >= B) return;
-  const int remaining = max_new[b] - gen_len[b];
-  // per-drafter accepted prefix (lane n handles drafter n)
-  int a = -1, n = 0, qs = 0;
-  if (lane < N) {
-    const SeqInfo sq = seqs[b * N + lane];
-    if (sq.q_len > 0 && remaining > 0) {
-      n = sq.q_len - 1;
-      qs = sq.q_start;
-      a = 0;
-      while (a < n && token_ids[qs + a + 1] == target[qs + a]) ++a;
+  __shared__ int s_branch, s_ctx, s_req, s_committed;
+  if (threadIdx.x < 32) {
+    const int remaining = max_new[b] - gen_len[b];
+    // per-drafter accepted prefix (lane n handles drafter n)
+    int a = -1, n = 0, qs = 0, branch = -1, ctx = 0, req = b;
+    if (lane < N) {
+      const SeqInfo sq = seqs[b * N + lane];
+      branch = sq.branch;
+      ctx = sq.ctx_len;
+      req = sq.request;
+      if (sq.q_len > 0 && remaining > 0) {
+        n = sq.q_len - 1;
+        qs = sq.q_start;
+        a = 0;
+        while (a < n && token_ids[qs + a + 1] == target[qs + a]) ++a;
+      }
+    }
+    // longest accepted prefix, lowest drafter index on ties
+    int best_a = a, best_n = lane < N ? lane : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const int oa = __shfl_xor_sync(0xffffffffu, best_a, o);
+      const int on = __shfl_xor_sync(0xffffffffu, best_n, o);
+      if (oa > best_a || (oa == best_a && on < best_n)) { best_a = oa; best_n = on; }
+    }
+    const int win_n = best_n & 31;
+    const int win_q = __shfl_sync(0xffffffffu, qs, win_n);
+    const int win_len = __shfl_sync(0xffffffffu, n, win_n);
+    const int win_branch = __shfl_sync(0xffffffffu, branch, win_n);
+    const int win_ctx = __shfl_sync(0xffffffffu, ctx, win_n);
+    const int win_req = __shfl_sync(0xffffffffu, req, win_n);
+    int committed = 0;
+    if (best_a >= 0) {
+      if (win_len == 0) committed = 1;
+      else if (best_a == win_len) committed = win_len + (bonus ? 1 : 0);
+      else committed = best_a + 1;
+      committed = min(committed, remaining);
+    }
+    const int base = seq_len[b];
+    for (int i = lane; i < committed; i += 32) tokens[(int64_t)b * tok_stride + base + i] = target[win_q + i];
+    if (lane < N) {
+      int4 o;
+      const bool active = a >= 0;
+      const bool win = active && lane == win_n;
+      o.x = active ? n : 0;
+      o.y = active ? a : 0;
+      o.z = win ? committed : 0;
+      o.w = !active ? 0 : (win ? (a == n ? 0 : max(n - a - 1, 0)) : n);
+      reinterpret_cast<int4*>(outcome)[b * N + lane] = o;
+    }
+    if (lane == 0) {
+      bon[b] = best_a >= 0 ? win_n : -1;
+      seq_len[b] = base + committed;
+      gen_len[b] += committed;
+      // window slots 0..committed-1 are positions ctx .. seq_len_new - 2:
+      // exactly the KV the engine invariant (valid below seq_len - 1) adds
+      s_branch = best_a >= 0 ? win_branch : -1;
+      s_ctx = win_ctx;
+      s_req = win_req;
+      s_committed = committed;
     }
   }
-  // longest accepted prefix, lowest drafter index on ties
-  int best_a = a, best_n = lane < N ? lane : 0x7fffffff;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const int oa = __shfl_xor_sync(0xffffffffu, best_a, o);
-    const int on = __shfl_xor_sync(0xffffffffu, best_n, o);
-    if (oa > best_a || (oa == best_a && on < best_n)) { best_a = oa; best_n = on; }
-  }
-  const int win_n = best_n;
-  const int win_q = __shfl_sync(0xffffffffu, qs, win_n & 31);
-  const int win_len = __shfl_sync(0xffffffffu, n, win_n & 31);
-  int committed = 0;
-  if (best_a >= 0) {
-    if (win_len == 0) committed = 1;
-    else if (best_a == win_len) committed = win_len + (bonus ? 1 : 0);
-    else committed = best_a + 1;
-    committed = min(committed, remaining);
-  }
-  const int base = seq_len[b];
-  for (int i = lane; i < committed; i += 32) tokens[(int64_t)b * tok_stride + base + i] = target[win_q + i];
-  if (lane < N) {
-    int32_t* o = outcome + (int64_t)(b * N + lane) * 4;
-    const bool active = a >= 0;
-    const bool win = active && lane == win_n;
-    o[0] = active ? n : 0;
-    o[1] = active ? a : 0;
-    o[2] = win ? committed : 0;
-    o[3] = !active ? 0 : (win ? (a == n ? 0 : max(n - a - 1, 0)) : n);
-  }
-  if (lane == 0) {
-    bon[b] = best_a >= 0 ? win_n : -1;
-    seq_len[b] = base + committed;
-    gen_len[b] += committed;
-  }
-}
-
-// Copy the winning drafter-branch window KV (slots [0, committed)) into the
-// paged cache at positions [ctx_len, ctx_len + committed), every layer.
-template <typename T>
-__global__ void kv_commit_kernel(int N, const SeqInfo* __restrict__ seqs, const int32_t* __restrict__ outcome,
-                                 const int32_t* __restrict__ bon, KvLayout kv) {
-  grid_dep_sync();
-  const int b = blockIdx.x, layer = blockIdx.y;
-  const int w = bon[b];
-  if (w < 0) return;
-  const SeqInfo sq = seqs[b * N + w];
-  if (sq.branch < 0) return;  // the winner wrote its KV in place
-  const int committed = outcome[(int64_t)(b * N + w) * 4 + 2];
-  const int hd = kv.head_dim, nkv = kv.kv_heads;
-  const T* wbase = reinterpret_cast<const T*>(kv.window) + layer * kv.window_layer_elems() +
-                   (int64_t)sq.branch * 2 * nkv * kv.window_max * hd;
-  T* cbase = reinterpret_cast<T*>(kv.cache) + layer * kv.cache_layer_elems();
-  const int32_t* btab = kv.block_table + (int64_t)sq.request * kv.max_pages;
-  const int per_slot = 2 * nkv * hd;
-  for (int e = threadIdx.x; e < committed * per_slot; e += blockDim.x) {
-    const int j = e / per_slot, r = e % per_slot;
-    const int kvsel = r / (nkv * hd), h = (r / hd) % nkv, d = r % hd;
-    const int pos = sq.ctx_len + j;
+  __syncthreads();
+  if (kv.window == nullptr || s_branch < 0 || s_committed <= 0) return;
+  // winner's window KV [layer][branch][K/V][head][slot j][hd] ->
+  // paged cache [layer][page][K/V][head][slot][hd] at position ctx + j
+  constexpr int kVec = 16 / sizeof(T);             // elements per 16-byte chunk
+  const int chunks = kv.head_dim / kVec;           // chunks per KV row
+  const int cm = s_committed, nkv = kv.kv_heads, hd = kv.head_dim;
+  const int total = kv.layers * 2 * nkv * cm * chunks;
+  const int32_t* btab = kv.block_table + (int64_t)s_req * kv.max_pages;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    int r = e;
+    const int c = r % chunks; r /= chunks;
+    const int j = r % cm; r /= cm;
+    const int h = r % nkv; r /= nkv;
+    const int sel = r & 1;
+    const int layer = r >> 1;
+    const int pos = s_ctx + j;
     const int page = btab[pos / kv.page];
     const int slot = pos % kv.page;
-    cbase[(((int64_t)page * 2 + kvsel) * nkv + h) * kv.page * hd + (int64_t)slot * hd + kv_phys<T>(slot, d)] =
-        wbase[((int64_t)kvsel * nkv + h) * kv.window_max * hd + (int64_t)j * hd + kv_phys<T>(j, d)];
+    const T* src = reinterpret_cast<const T*>(kv.window) + layer * kv.window_layer_elems() +
+                   ((((int64_t)s_branch * 2 + sel) * nkv + h) * kv.window_max + j) * hd + kv_phys<T>(j, c * kVec);
+    T* dst = reinterpret_cast<T*>(kv.cache) + layer * kv.cache_layer_elems() +
+             ((((int64_t)page * 2 + sel) * nkv + h) * kv.page + slot) * hd + kv_phys<T>(slot, c * kVec);
+    *reinterpret_cast<int4*>(dst) = *reinterpret_cast<const int4*>(src);
   }
 }
 
@@ -196,7 +215,7 @@ __global__ void draft_batch_kernel(int B, int k, int step, const int32_t* __rest
                                    const int32_t* __restrict__ prev_out, int32_t* __restrict__ drafts,
                                    int32_t* __restrict__ ndraft, int32_t* __restrict__ token_ids,
                                    int32_t* __restrict__ positions, SeqInfo* __restrict__ seqs,
-                                   int32_t* __restrict__ logit_rows) {
+                                   int32_t* __restrict__ logit_rows, int32_t* __restrict__ key_pos) {
   grid_dep_sync();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
@@ -225,6 +244,7 @@ __global__ void draft_batch_kernel(int B, int k, int step, const int32_t* __rest
       positions[b * rows + j] = (j < q) ? p : 0;
     }
     logit_rows[b] = b * rows + max(q - 1, 0);
+    if (key_pos != nullptr) key_pos[b] = L;  // the draft's output position
     if (q > 0) dkv_len[b] = L;
   } else {
     const int p = L - 1 + step;
@@ -233,22 +253,12 @@ __global__ void draft_batch_kernel(int B, int k, int step, const int32_t* __rest
     token_ids[b * rows] = prev_out[b];
     positions[b * rows] = p;
     logit_rows[b] = b * rows;
+    if (key_pos != nullptr) key_pos[b] = p + 1;
   }
   seqs[b] = sq;
 }
 
 }  // namespace
-
-int kv_commit(int B, int N, const SeqInfo* seqs, const int32_t* outcome, const int32_t* bon,
-              const KvLayout& kv, int dtype, cudaStream_t s) {
-  if (B == 0 || N <= 1) return SR_OK;
-  dim3 grid(B, kv.layers);
-  if (dtype == 1)
-    sr::launch_k(kv_commit_kernel<__nv_bfloat16>, grid, 256, 0, s, N, seqs, outcome, bon, kv);
-  else
-    sr::launch_k(kv_commit_kernel<float>, grid, 256, 0, s, N, seqs, outcome, bon, kv);
-  return check_launch("kv_commit_kernel");
-}
 
 // Host-facing step result: per request its outcome row then the token
 // slots [seq_before, seq_before + w) (clamped to the row), one thread per cell.
@@ -283,7 +293,7 @@ extern "C" int sr_pack_results(int num_requests, int width, const int32_t* outco
   return sr::check_launch("pack_results_kernel");
 }
 
-extern "C" int sr_accept_commit(int num_requests, int num_drafters, const void* seqs,
+extern "C" int sr_accept_commit(void* model, int num_requests, int num_drafters, const void* seqs,
                                 const int32_t* token_ids, const int32_t* target, int32_t* tokens,
                                 int64_t tok_stride, int32_t* seq_len, int32_t* gen_len,
                                 const int32_t* max_new, int bonus_token, int32_t* outcome,
@@ -293,9 +303,23 @@ extern "C" int sr_accept_commit(int num_requests, int num_drafters, const void* 
   SR_REQUIRE(num_drafters >= 1 && num_drafters <= 32, "num_drafters out of [1, 32]");
   SR_REQUIRE(seqs && token_ids && target && tokens && seq_len && gen_len && max_new && outcome && bon,
              "null pointer");
-  sr::launch_k(sr::accept_commit_kernel, sr::ceil_div(num_requests, 8), 256, 0, (cudaStream_t)stream, 
-      num_requests, num_drafters, reinterpret_cast<const sr::SeqInfo*>(seqs), token_ids, target, tokens,
-      tok_stride, seq_len, gen_len, max_new, bonus_token, outcome, bon);
+  SR_REQUIRE((reinterpret_cast<uintptr_t>(outcome) & 15) == 0, "outcome rows must be 16-byte aligned");
+  sr::KvLayout kv{};
+  int dtype = 1;
+  if (num_drafters > 1 && model != nullptr) {
+    const int rc = sr::model_kv_layout(model, &kv, &dtype);
+    if (rc) return rc;
+    SR_REQUIRE(kv.window != nullptr, "drafter branches need a window buffer");
+  }
+  const auto* sq = reinterpret_cast<const sr::SeqInfo*>(seqs);
+  if (dtype == 1)
+    sr::launch_k(sr::accept_commit_kernel<__nv_bfloat16>, num_requests, 128, 0, (cudaStream_t)stream,
+                 num_requests, num_drafters, sq, token_ids, target, tokens, tok_stride, seq_len, gen_len, max_new,
+                 bonus_token, outcome, bon, kv);
+  else
+    sr::launch_k(sr::accept_commit_kernel<float>, num_requests, 128, 0, (cudaStream_t)stream, num_requests,
+                 num_drafters, sq, token_ids, target, tokens, tok_stride, seq_len, gen_len, max_new, bonus_token,
+                 outcome, bon, kv);
   return sr::check_launch("accept_commit_kernel");
 }
 
@@ -316,7 +340,7 @@ extern "C" int sr_draft_model_batch(int num_requests, int k, int step, const int
                                     const int32_t* seq_len, const int32_t* gen_len, const int32_t* max_new,
                                     int32_t* dkv_len, const int32_t* prev_out, int32_t* drafts, int32_t* ndraft,
                                     int32_t* token_ids, int32_t* positions, void* seqs, int32_t* logit_rows,
-                                    sr_stream_t stream) {
+                                    int32_t* key_pos, sr_stream_t stream) {
   SR_REQUIRE(num_requests >= 0 && k >= 1 && step >= 0 && step <= k, "bad draft step");
   if (num_requests == 0) return SR_OK;
   SR_REQUIRE(tokens && seq_len && gen_len && max_new && dkv_len && drafts && ndraft && token_ids && positions &&
@@ -324,7 +348,7 @@ extern "C" int sr_draft_model_batch(int num_requests, int k, int step, const int
              "null pointer");
   sr::launch_k(sr::draft_batch_kernel, sr::ceil_div(num_requests, 128), 128, 0, (cudaStream_t)stream, 
       num_requests, k, step, tokens, tok_stride, seq_len, gen_len, max_new, dkv_len, prev_out, drafts, ndraft,
-      token_ids, positions, reinterpret_cast<sr::SeqInfo*>(seqs), logit_rows);
+      token_ids, positions, reinterpret_cast<sr::SeqInfo*>(seqs), logit_rows, key_pos);
   return sr::check_launch("draft_batch_kernel");
 }
 

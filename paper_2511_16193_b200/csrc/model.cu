@@ -33,8 +33,6 @@ int attention_bf16(const __nv_bfloat16* q, const SeqInfo* seqs, int num_seqs, in
                    __nv_bfloat16* out, cudaStream_t stream, int phase, bool plan);
 int attention_f32(const float* q, const SeqInfo* seqs, int num_seqs, int max_q_len, const KvLayout& kv,
                   int layer, int nq, float* out, cudaStream_t stream);
-int kv_commit(int B, int N, const SeqInfo* seqs, const int32_t* outcome, const int32_t* bon,
-              const KvLayout& kv, int dtype, cudaStream_t s);
 
 namespace {
 
@@ -189,6 +187,14 @@ static int validate(const sr_model_desc& d) {
   SR_REQUIRE(d.max_tokens > 0 && d.max_seqs > 0, "max_tokens / max_seqs must be > 0");
   SR_REQUIRE(d.max_key < d.max_pos, "max_key must be < max_pos (RoPE table)");
   SR_REQUIRE(d.q_heads / d.kv_heads * 1 <= 64, "group size too large");
+  return SR_OK;
+}
+
+int model_kv_layout(void* handle, KvLayout* kv, int* dtype) {
+  SR_REQUIRE(handle && kv && dtype, "null model");
+  const Model* m = reinterpret_cast<const Model*>(handle);
+  *kv = m->kv;
+  *dtype = m->d.dtype;
   return SR_OK;
 }
 
@@ -468,15 +474,6 @@ int sr_sample_rows(const float* logits, int rows, int vocab, int ld, const int32
   SR_REQUIRE(logits && req && pos && ids, "null pointer");
   return sr::sample_rows(logits, rows, vocab, ld, req, pos, seed, 1.0f / temperature, ids, nullptr,
                          (cudaStream_t)stream);
-}
-
-int sr_kv_commit(void* handle, int num_requests, int num_drafters, const void* seqs, const int32_t* outcome,
-                 const int32_t* bon, sr_stream_t stream) {
-  SR_REQUIRE(handle, "null model");
-  Model* m = reinterpret_cast<Model*>(handle);
-  if (num_drafters > 1) SR_REQUIRE(m->d.window_kv != nullptr, "drafter branches need a window buffer");
-  return sr::kv_commit(num_requests, num_drafters, reinterpret_cast<const sr::SeqInfo*>(seqs), outcome, bon,
-                       m->kv, m->d.dtype, (cudaStream_t)stream);
 }
 
 }  // extern "C"

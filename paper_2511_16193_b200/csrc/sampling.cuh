@@ -33,16 +33,34 @@ __host__ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k
   }
 }
 
+// Stream tags (third Philox counter word): the target's sampling noise, and
+// the rejection sampler's acceptance uniforms and residual noise.
+constexpr uint32_t kTagSample = 0x53414D50u;    // "SAMP"
+constexpr uint32_t kTagAccept = 0x41434350u;    // "ACCP"
+constexpr uint32_t kTagResidual = 0x52455344u;  // "RESD"
+
+// odd multiple of 2^-24: exactly representable, strictly inside (0, 1)
+__host__ __device__ __forceinline__ float unit_open(uint32_t x) {
+  return (float)(((x >> 9) << 1) | 1u) * 5.9604644775390625e-8f;
+}
+
 // Four Gumbel values for vocabulary ids [4*blk, 4*blk+4) at (req, pos).
-__device__ __forceinline__ void gumbel4(uint32_t seed, int req, int pos, int blk, float g[4]) {
-  uint32_t c[4] = {(uint32_t)pos, (uint32_t)blk, 0x53414D50u, 0u};
+__device__ __forceinline__ void gumbel4_tag(uint32_t seed, int req, int pos, int blk, uint32_t tag, float g[4]) {
+  uint32_t c[4] = {(uint32_t)pos, (uint32_t)blk, tag, 0u};
   philox4x32_10(c, seed, (uint32_t)req);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    // odd multiple of 2^-24: exactly representable, strictly inside (0, 1)
-    const float u = (float)(((c[i] >> 9) << 1) | 1u) * 5.9604644775390625e-8f;
-    g[i] = -logf(-logf(u));
-  }
+  for (int i = 0; i < 4; ++i) g[i] = -logf(-logf(unit_open(c[i])));
+}
+
+__device__ __forceinline__ void gumbel4(uint32_t seed, int req, int pos, int blk, float g[4]) {
+  gumbel4_tag(seed, req, pos, blk, kTagSample, g);
+}
+
+// One uniform in (0, 1) keyed by (seed, req, pos) on stream `tag`.
+__host__ __device__ __forceinline__ float keyed_uniform(uint32_t seed, int req, int pos, uint32_t tag) {
+  uint32_t c[4] = {(uint32_t)pos, 0u, tag, 0u};
+  philox4x32_10(c, seed, (uint32_t)req);
+  return unit_open(c[0]);
 }
 
 }  // namespace sr

@@ -55,6 +55,26 @@ class NcclChannel:
             w.wait()
 
 
+class HostChannel:
+    """The same exchange staged through host memory over a CPU process
+    group (gloo): lets the multi-process protocol run with several ranks on
+    ONE GPU (tests), where NCCL refuses duplicate devices.  Not a product
+    transport."""
+
+    def __init__(self, dist, peer: int):
+        self.dist, self.peer = dist, peer
+
+    def exchange(self, send: list, recv: list) -> None:
+        torch.cuda.synchronize()
+        reqs = [self.dist.isend(t.cpu(), self.peer) for t in send]
+        bufs = [torch.empty(t.shape, dtype=t.dtype) for t in recv]
+        reqs += [self.dist.irecv(b, self.peer) for b in bufs]
+        for r in reqs:
+            r.wait()
+        for t, b in zip(recv, bufs):
+            t.copy_(b)
+
+
 def _graph(fn):
     """Capture ``fn`` (static-shape device work, no host syncs) into a CUDA
     graph; returns the graph (replay() reruns ``fn`` on the same buffers)."""
@@ -142,7 +162,7 @@ class DraftSide:
                 self.B, self.k, step, self.tokens.data_ptr(), self.stride, self.ctx.data_ptr(),
                 self.g0.data_ptr(), self.max_new.data_ptr(), self.dkv_len.data_ptr(), self.m_out.data_ptr(),
                 self.drafts.data_ptr(), self.nd.data_ptr(), self.m_token_ids.data_ptr(),
-                self.m_positions.data_ptr(), self.m_seqs.data_ptr(), self.m_logit_rows.data_ptr(), st),
+                self.m_positions.data_ptr(), self.m_seqs.data_ptr(), self.m_logit_rows.data_ptr(), None, st),
                 "sr_draft_model_batch")
             if step < self.k:
                 m.forward(self.m_token_ids, self.m_positions, self.m_seqs, num_seqs=self.B,
@@ -271,7 +291,7 @@ class VerifySide:
                     out=e.target_ids)
         out = e.history[0]
         _native.check(lib.sr_accept_commit(
-            e.B, 1, e.seqs.data_ptr(), e.token_ids.data_ptr(), e.target_ids.data_ptr(), e.tokens.data_ptr(),
+            e.m.handle, e.B, 1, e.seqs.data_ptr(), e.token_ids.data_ptr(), e.target_ids.data_ptr(), e.tokens.data_ptr(),
             e.stride, e.seq_len.data_ptr(), e.gen_len.data_ptr(), e.max_new.data_ptr(), 0, out.data_ptr(),
             e.bon.data_ptr(), st), "sr_accept_commit")
         self.rows.copy_(out[: self.B])
@@ -362,7 +382,8 @@ def pairing(world: int, drafters: int) -> dict:
 
 
 def run_ranks(dist, rank: int, world: int, drafters: int, shards: dict, k: int, make_drafter,
-              make_model=None, max_rounds: int = 1_000_000, graphs: bool = True, round_times=None):
+              make_model=None, max_rounds: int = 1_000_000, graphs: bool = True, round_times=None,
+              channel=NcclChannel):
     """Decoupled rollout across ranks (one process per GPU).
 
     ``shards[v]`` = (prompts, max_new) of verifier rank v.  Drafter ranks run
@@ -373,6 +394,8 @@ def run_ranks(dist, rank: int, world: int, drafters: int, shards: dict, k: int, 
     rows, rounds) on verifier ranks, (None, None, rounds) on drafter ranks.
     ``round_times`` (a list, verifier ranks): host time after each round's
     exchange completed (the round's device work is done then).
+    ``channel``: :class:`NcclChannel` (device buffers over NVLink) or
+    :class:`HostChannel` (tests: several ranks sharing one GPU).
     """
     dev = torch.device("cuda", torch.cuda.current_device())
     pairs = pairing(world, drafters)
@@ -392,7 +415,7 @@ def run_ranks(dist, rank: int, world: int, drafters: int, shards: dict, k: int, 
             for v in sorted(live):
                 D = sides[v]
                 drafts, nd = D.draft()
-                NcclChannel(dist, v).exchange(
+                channel(dist, v).exchange(
                     [drafts, nd], [D.in_verified, D.in_accepted, D.in_committed, D.in_ctoks, done[v]])
                 D.apply()
                 if int(done[v].item()):
@@ -415,7 +438,7 @@ def run_ranks(dist, rank: int, world: int, drafters: int, shards: dict, k: int, 
             e1.record()
             ev.append((e0, e1))
         done.fill_(1 if V.done() else 0)
-        NcclChannel(dist, peer).exchange(
+        channel(dist, peer).exchange(
             [V.out_verified, V.out_accepted, V.out_committed, V.out_ctoks, done], [V.in_drafts, V.in_nd])
         rows = V.receive()
         if rounds > 0:

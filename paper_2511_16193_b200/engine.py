@@ -6,8 +6,8 @@ request of the batch, entirely on device:
     sr_ngram_propose      K4  n-gram drafts from the token buffer
     sr_build_verify_batch     verify rows [last token, d_1..d_k] per drafter
     sr_model_forward      K1+K2+K6  target verify forward, fused argmax
-    sr_accept_commit      K3  accepted prefix, Best-of-N select, commit
-    sr_kv_commit              winning branch KV -> paged cache (N > 1)
+    sr_accept_commit      K3  accepted prefix, Best-of-N select, commit, and
+                              the winning branch's KV -> paged cache (N > 1)
 
 This replaces one ``_Executor.begin_round``/``end_round`` pair of the
 reference (``sim.py:834-1092``) with real drafting and verification; the
@@ -73,6 +73,11 @@ class SyntheticDrafter:
         self.vocab = vocab
 
 
+# the drafter's own sampling stream in rejection mode (independent of the
+# target's keyed noise, which would couple the two samples)
+DRAFT_SEED_SALT = 0x6A09E667
+
+
 class ModelDrafter:
     """Small-model drafter (K5; reference methods ``draft-0.5b``/``draft-1.5b``,
     ``scenarios.py:25-29``): k decode steps of its own decoder per window,
@@ -85,7 +90,14 @@ class ModelDrafter:
     T: Gumbel-coupled speculative sampling.  Every committed token is the
     target's keyed sample, so the output equals plain sampled decoding bit
     for bit, and a draft is accepted exactly when the two models' perturbed
-    argmaxes agree (probability -> 1 as q -> p)."""
+    argmaxes agree (probability -> 1 as q -> p).
+
+    With ``RolloutEngine(acceptance="rejection")`` the drafter instead
+    samples its window from q with its own keyed stream and keeps q's logit
+    rows; K3 then runs Leviathan rejection sampling (``sr_accept_rejection``):
+    outputs follow the target's distribution (not its keyed sample), and a
+    draft is accepted with probability sum_v min(p_v, q_v), the maximum any
+    coupling reaches.  Its DeviceModel needs ``logits_capacity >= batch``."""
 
     name = "model"
 
@@ -118,13 +130,34 @@ class ModelDrafter:
 
     def enqueue(self, drafts, ndraft) -> None:
         e, lib, st = self.eng, self.eng.lib, _native.stream_handle()
+        rejection = e.acceptance == "rejection"
+        if rejection and not hasattr(self, "q_logits"):
+            if self.m.desc.logits_capacity < e.B:
+                raise ConfigError("rejection sampling: the drafter model needs logits_capacity >= batch")
+            self.q_logits = torch.empty((e.k, e.B, self.m.s.vocab), dtype=torch.float32, device=e.dev)
+            self.key_req = torch.arange(e.B, dtype=torch.int32, device=e.dev)
+            self.key_pos = torch.zeros(e.B, dtype=torch.int32, device=e.dev)
         for step in range(e.k + 1):
             _native.check(lib.sr_draft_model_batch(
                 e.B, e.k, step, e.tokens.data_ptr(), e.stride, e.seq_len.data_ptr(), e.gen_len.data_ptr(),
                 e.max_new.data_ptr(), self.dkv_len.data_ptr(), self.out.data_ptr(), drafts.data_ptr(),
                 ndraft.data_ptr(), self.token_ids.data_ptr(), self.positions.data_ptr(), self.seqs.data_ptr(),
-                self.logit_rows.data_ptr(), st), "sr_draft_model_batch")
-            if step < e.k:
+                self.logit_rows.data_ptr(), self.key_pos.data_ptr() if rejection else None, st),
+                "sr_draft_model_batch")
+            if step == e.k:
+                break
+            if rejection:
+                # the drafter samples its window from q = softmax(logits / T)
+                # with its own keyed noise, and keeps q's rows for K3
+                q = self.q_logits[step]
+                self.m.forward(self.token_ids, self.positions, self.seqs, num_seqs=e.B,
+                               max_q_len=e.k + 2, max_key=e.max_key, out=q, logit_rows=self.logit_rows,
+                               output=1)
+                _native.check(lib.sr_sample_rows(
+                    q.data_ptr(), e.B, q.shape[1], q.shape[1], self.key_req.data_ptr(), self.key_pos.data_ptr(),
+                    (e.seed ^ DRAFT_SEED_SALT) & 0xFFFFFFFF, e.temperature, self.out.data_ptr(), st),
+                    "sr_sample_rows")
+            else:
                 self.m.forward(self.token_ids, self.positions, self.seqs, num_seqs=e.B,
                                max_q_len=e.k + 2, max_key=e.max_key, out=self.out,
                                logit_rows=self.logit_rows, output=e._out_mode,
@@ -172,7 +205,7 @@ class RolloutEngine:
 
     def __init__(self, target: DeviceModel, prompts: list[np.ndarray], max_new: list[int], *, k: int = 4,
                  drafters: tuple = (NgramDrafter(),), bonus_token: bool = False, history: int = 0,
-                 temperature: float = 0.0, seed: int = 0):
+                 temperature: float = 0.0, seed: int = 0, acceptance: str = "exact"):
         if not prompts:
             raise ConfigError("empty batch")
         if len(prompts) != len(max_new):
@@ -189,6 +222,22 @@ class RolloutEngine:
         # verifies because the target's draw is keyed by (seed, request, position))
         self.temperature, self.seed = float(temperature), int(seed)
         self._out_mode = 2 if self.temperature > 0 else 0
+        # acceptance rule: "exact" -- exact match against the target's token
+        # (greedy, or its keyed sample at T > 0; every committed token equals
+        # plain decoding's), or "rejection" -- Leviathan rejection sampling
+        # for one stochastic model drafter (distribution-preserving)
+        if acceptance not in ("exact", "rejection"):
+            raise ConfigError(f"acceptance must be 'exact' or 'rejection', not {acceptance!r}")
+        self.acceptance = acceptance
+        if acceptance == "rejection":
+            if self.N != 1 or not isinstance(self.drafters[0], ModelDrafter):
+                raise ConfigError("rejection sampling needs exactly one model drafter (N = 1)")
+            if self.temperature <= 0:
+                raise ConfigError("rejection sampling needs temperature > 0")
+            if self.drafters[0].m.s.vocab != target.s.vocab:
+                raise ConfigError("rejection sampling needs drafter and target over the same vocabulary")
+            if target.desc.logits_capacity < self.B * (k + 1):
+                raise ConfigError("rejection sampling: the target needs logits_capacity >= B * (k + 1)")
         if self.N > 1 and target.branches < self.B * (self.N - 1):
             raise ConfigError("target model needs max_branches >= B*(N-1) for Best-of-N")
         if self.B * self.N > target.max_seqs or self.B * self.N * (k + 1) > target.max_tokens:
@@ -225,6 +274,9 @@ class RolloutEngine:
         # planner.reconfigure / sim.py:445-510): one batch mixes windows
         # 0..k; rows beyond a request's window are simply not verified
         self.window = torch.full((self.B,), k, dtype=torch.int32, device=dev)
+        if acceptance == "rejection":
+            self.p_logits = torch.empty((R, target.s.vocab), dtype=torch.float32, device=dev)
+            self.rs_stats = torch.zeros((R, 4), dtype=torch.float32, device=dev)
         self.steps = 0
         self.max_key = need - 1
         self.graph = None
@@ -270,18 +322,27 @@ class RolloutEngine:
             self.window.data_ptr(),
             self.token_ids.data_ptr(), self.positions.data_ptr(), self.seqs.data_ptr(), st),
             "sr_build_verify_batch")
+        out = self.history[slot]
+        if self.acceptance == "rejection":
+            d = self.drafters[0]
+            self.m.forward(self.token_ids, self.positions, self.seqs, num_seqs=self.B, max_q_len=self.k + 1,
+                           max_key=self.max_key, out=self.p_logits, output=1)
+            V = self.p_logits.shape[1]
+            _native.check(lib.sr_accept_rejection(
+                self.B, self.k, self.seqs.data_ptr(), self.token_ids.data_ptr(), self.p_logits.data_ptr(), V,
+                d.q_logits.data_ptr() if self.k else None, V, V, self.temperature, self.seed & 0xFFFFFFFF,
+                self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(), self.gen_len.data_ptr(),
+                self.max_new.data_ptr(), self.bonus, self.rs_stats.data_ptr(), out.data_ptr(), self.bon.data_ptr(),
+                st), "sr_accept_rejection")
+            return
         self.m.forward(self.token_ids, self.positions, self.seqs, num_seqs=self.B * self.N,
                        max_q_len=self.k + 1, max_key=self.max_key, out=self.target_ids,
                        output=self._out_mode, temperature=self.temperature, seed=self.seed)
-        out = self.history[slot]
         _native.check(lib.sr_accept_commit(
-            self.B, self.N, self.seqs.data_ptr(), self.token_ids.data_ptr(), self.target_ids.data_ptr(),
-            self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(), self.gen_len.data_ptr(),
-            self.max_new.data_ptr(), self.bonus, out.data_ptr(), self.bon.data_ptr(), st),
+            self.m.handle, self.B, self.N, self.seqs.data_ptr(), self.token_ids.data_ptr(),
+            self.target_ids.data_ptr(), self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(),
+            self.gen_len.data_ptr(), self.max_new.data_ptr(), self.bonus, out.data_ptr(), self.bon.data_ptr(), st),
             "sr_accept_commit")
-        if self.N > 1:
-            _native.check(lib.sr_kv_commit(self.m.handle, self.B, self.N, self.seqs.data_ptr(),
-                                           out.data_ptr(), self.bon.data_ptr(), st), "sr_kv_commit")
 
     def step(self) -> None:
         slot = self.steps % self.history.shape[0]

@@ -189,7 +189,7 @@ def test_accept_commit_kernel_vs_python():
             gen_len=gen_len, max_new=max_new).items()}
         outcome = torch.zeros((S, 4), dtype=torch.int32, device="cuda")
         bon = torch.zeros(B, dtype=torch.int32, device="cuda")
-        _native.check(lib.sr_accept_commit(B, N, dev["seqs"].data_ptr(), dev["token_ids"].data_ptr(),
+        _native.check(lib.sr_accept_commit(None, B, N, dev["seqs"].data_ptr(), dev["token_ids"].data_ptr(),
                                            dev["target"].data_ptr(), dev["tokens"].data_ptr(), stride,
                                            dev["seq_len"].data_ptr(), dev["gen_len"].data_ptr(),
                                            dev["max_new"].data_ptr(), bonus, outcome.data_ptr(),
