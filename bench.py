@@ -1,21 +1,31 @@
 """Benchmark of the B200 speculative-rollout hot path (BASELINE.json metric:
 rollout accepted tokens/s; mean accepted length; roofline %).
 
-Workload (BASELINE.json configs[1]): Qwen2.5-1.5B-shaped random-init target,
-256 prompts per GPU, k=4 n-gram drafter (vLLM prompt-lookup semantics,
-min_n=1, max_n=3), greedy exact-match verification, bonus token on.  Prompt
-lengths come from the reference trace generator (default_trace_spec: U[128,
-1024]), prompt tokens from the keyed stream (seed, rid, "prompt").  A step is
-one speculation window over the whole batch: n-gram draft -> verify forward
-(M = 256 x 5 rows through 28 layers + lm_head with fused argmax) -> accept /
-commit.  The batch is kept full (no request reaches its budget during the
-run), i.e. steady-state throughput.
+Headline workload (BASELINE.json configs[1]): Qwen2.5-1.5B-shaped random-init
+target, 256 prompts per GPU, k = 4, one drafter, greedy exact-match
+verification, bonus token on.  Prompt lengths come from the reference trace
+generator (default_trace_spec: U[128, 1024]), prompt tokens from the keyed
+stream (seed, rid, "prompt").  A step is one speculation window over the
+whole batch: draft -> verify forward (M = 256 x 5 rows through 28 layers +
+lm_head with fused argmax) -> fused accept / commit.  The batch is kept full
+(no request reaches its budget during the run): steady-state throughput.
+
+The headline drafter is the reference-acceptance drafter: the
+target's own greedy continuation, accepted by the reference's keyed
+``accept_draw`` law (sim.py:322-336).  Random-init weights give the real
+n-gram drafter ~0 acceptance, so it is reported beside it (``variants.ngram``),
+together with the configs[2] shape on one GPU (``variants.configs2_7b``: 7B
+target, 64 prompts = the per-GPU share of 512 over 8 GPUs, Best-of-N with
+n-gram + 0.5B + 1.5B-shaped model drafters) and the n-gram kernel alone at
+1024 x 20K context (``variants.ngram_kernel``).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
 N > 1 runs under torchrun, one rank per GPU, 256 prompts per rank (weak
 scaling by prompt sharding, no data-path collective).  Timing: CUDA events
 on the launching stream, barrier + synchronize on both sides, max over ranks.
+``--impl reference`` times the CPU port of the same path (oracle/, batched
+over requests, same drafter law) on a bounded sample of the workload.
 """
 
 from __future__ import annotations
@@ -24,9 +34,7 @@ import argparse
 import ctypes
 import json
 import os
-import re
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -43,6 +51,7 @@ K = 4
 METRIC = "rollout accepted tokens/sec (Qwen2.5-1.5B-shaped target, batch 256/GPU, k=4, greedy)"
 UNIT = "tokens/s"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
+CATS = ["qkv", "o", "gate_up", "down", "lm_head", "attention", "other", "attention_combine"]
 
 
 def parse():
@@ -55,6 +64,7 @@ def parse():
     ap.add_argument("--model", default=MODEL)
     ap.add_argument("--layers", type=int, default=None, help="debug only: truncate depth")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the n-gram / 7B / n-gram-kernel lines")
     ap.add_argument("--eager", action="store_true",
                     help="launch every kernel from the host instead of replaying a CUDA graph")
     ap.add_argument("--drafter", choices=["synthetic", "ngram"], default="synthetic",
@@ -63,6 +73,8 @@ def parse():
     ap.add_argument("--accept-method", default="draft-0.5b",
                     help="reference drafting method whose latent acceptance/keyed draws drive the "
                          "synthetic drafter (scenarios.METHODS)")
+    ap.add_argument("--ref-batch", type=int, default=16, help="--impl reference: requests in the CPU sample")
+    ap.add_argument("--ref-prompt-cap", type=int, default=128, help="--impl reference: prompt tokens kept")
     return ap.parse_args()
 
 
@@ -88,80 +100,114 @@ def workload(rank: int, batch: int, steps_total: int, vocab: int, world: int = 1
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled every 5 ms through
+    NVML while the timed region runs (nvidia-smi's fields, faster)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20), ("hw_thermal_slowdown", 0x40),
+               ("hw_power_brake_slowdown", 0x80), ("sw_power_cap", 0x4))
 
     def __init__(self, index: int):
         self.index = index
-        self.rows: list[list[str]] = []
+        self.rows: list[tuple[int, int, int]] = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._armed = threading.Event()
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            import pynvml
 
-    def __enter__(self):
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            return
+        while not self._stop.is_set():
+            if self._armed.is_set():
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    reasons = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((sm, reasons, time.perf_counter_ns()))
+                except Exception:
+                    pass
+            self._stop.wait(0.005)
+
+    def start(self):
         self._t.start()
         return self
 
-    def __exit__(self, *a):
+    def arm(self, on: bool):
+        (self._armed.set if on else self._armed.clear)()
+
+    def stop(self):
         self._stop.set()
         self._t.join(timeout=10)
 
     def summary(self) -> dict:
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({n for r in self.rows for n, bit in self.REASONS if r[1] & bit})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": getattr(self, "max_mhz", None),
+                "reasons": reasons, "samples": len(self.rows), "source": "NVML every 5 ms during the timed regions"}
 
 
-# -- our arm -------------------------------------------------------------------------
-
-
-def traffic_bytes():
-    f = ROOT / "profiles" / "r01" / "ncu_step_layer0.json"
-    try:
-        for d in json.loads(f.read_text()):
-            m = re.search(r"gemm_\w*kernel<(\d+), (\d+)", d["kernel"])
-            if m and m.group(2) == "2":  # epilogue 2 = SwiGLU: the gate_up GEMM
-                return d["dram_read_bytes"] + d["dram_write_bytes"]
-    except Exception:
-        return None
-    return None
+# -- helpers -----------------------------------------------------------------------------
 
 
 def peaks():
     if PEAKS.exists():
         d = json.loads(PEAKS.read_text())
-        return d["bf16_tflops"], d["bf16_tflops_sustained"], d["hbm_gbs"], "measured"
-    return 1590.0, 1400.0, 6650.0, "fallback"
+        return d["bf16_tflops"], d["bf16_tflops_sustained"], d["hbm_gbs"], "measured (MEASURED_PEAKS.json)"
+    return 1590.0, 1400.0, 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """DRAM read+write bytes per launch of gate_up (epilogue 2 = SwiGLU, the
+    largest verify GEMM) from the newest committed ncu --set full capture of
+    the step (profiles/rNN/ncu_step_layer0.json)."""
+    import re
+
+    for rnd in ("r02", "r01"):
+        f = ROOT / "profiles" / rnd / "ncu_step_layer0.json"
+        if not f.exists():
+            continue
+        try:
+            for d in json.loads(f.read_text()):
+                m = re.search(r"gemm_\w*kernel<(\d+), (\d+)", d["kernel"])
+                if m and m.group(2) == "2":
+                    return rnd, d["dram_read_bytes"] + d["dram_write_bytes"]
+        except Exception:
+            pass
+    return None, None
+
+
+def timed(fn, reps: int, stream=None) -> float:
+    """Mean ms per call of ``fn`` (device work enqueued on the current
+    stream), CUDA events around ``reps`` back-to-back calls."""
+    import torch
+
+    st = stream or torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(reps):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
 
 
 def workload_config(args, s, world):
-    """The bench's workload description, shared by both arms."""
     B = args.batch
     return {"workload": f"configs[1]: {args.model}-shaped target, batch {B}/GPU, k={K}, "
                         f"single {args.drafter} drafter, greedy exact match, bonus token",
             "model": args.model, "layers": s.layers, "batch_per_gpu": B, "global_batch": B * world,
             "k": K, "verify_rows_per_step": B * (K + 1), "prompt_len": "U[128,1024] (default_trace_spec)",
             "parallelism": f"prompt-sharded x{world} (no data-path collective)",
-            "l2": "inputs larger than L2 (3.1 GB weights + paged KV per step)",
+            "l2": "inputs larger than L2 (3.1 GB weights + ~8 GB paged KV read per step)",
             "cuda_graph": not args.eager}
+
+
+# -- our arm -------------------------------------------------------------------------
 
 
 def run_ours(args, rank, world, dist):
@@ -171,7 +217,8 @@ def run_ours(args, rank, world, dist):
     from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine, SyntheticDrafter
     from paper_2511_16193_b200.model import DeviceModel, init_weights, shape
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
     lib = _native.lib()
     s = shape(args.model, args.layers)
     steps_total = args.warmup + 3 * args.steps + 12
@@ -190,18 +237,14 @@ def run_ours(args, rank, world, dist):
     plain.prefill()
     plain.run()
     truth = plain.outputs()
-    ngram_probe = None
-    if args.drafter == "synthetic":
-        drafter = SyntheticDrafter(truth, trace, args.accept_method, seed=0)
-        ngram_probe = probe_ngram(RolloutEngine, NgramDrafter, model, prompts, budget, truth)
-    else:
-        drafter = NgramDrafter(1, 3)
     del plain
+    drafter = (SyntheticDrafter(truth, trace, args.accept_method, seed=0) if args.drafter == "synthetic"
+               else NgramDrafter(1, 3))
     eng = RolloutEngine(model, prompts, budget, k=K, drafters=(drafter,), bonus_token=True, history=1)
     eng.prefill()
     if not args.eager:
         eng.capture()
-    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", 0))).__enter__()
+    clocks = ClockSampler(local).start()
     for _ in range(args.warmup):
         eng.step()
     torch.cuda.synchronize()
@@ -213,41 +256,44 @@ def run_ours(args, rank, world, dist):
 
     # ---- timed region: K device-resident steps (inputs already in HBM)
     hist = torch.zeros((args.steps, B, 4), dtype=torch.int32, device="cuda")
+    ctx_sum = int(eng.seq_len.sum().item())
     gen0 = eng.gen_len.sum()
     launches0 = lib.sr_launch_count()
-    lib.sr_model_profile(model.handle, 1 if args.eager else 0, None, None)
     st = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    clocks.arm(True)
     ev0.record(st)
     for i in range(args.steps):
         eng.step()
         hist[i].copy_(eng.history[0])
     ev1.record(st)
     barrier()
-    clocks.__exit__(None, None, None)
+    clocks.arm(False)
     launches = lib.sr_launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
     committed = int((eng.gen_len.sum() - gen0).item())
+    ctx_sum_end = int(eng.seq_len.sum().item())
+
+    # ---- per-kernel durations: a second graph of the same step with CUDA
+    # event nodes bracketing every forward launch (on the launching stream),
+    # replayed after the timed region; K3 and the drafter timed alone
     cat_ms = (ctypes.c_float * 8)()
     cat_n = (ctypes.c_int32 * 8)()
-    lib.sr_model_profile(model.handle, 0, cat_ms, cat_n)
+    lib.sr_model_profile(model.handle, 0, None, None)
     if not args.eager:
-        # kernel durations: a second graph of the same step with CUDA event
-        # nodes bracketing every launch (captured on the launching stream);
-        # replayed after the timed region, read back from its last replay
         lib.sr_model_profile(model.handle, 1, None, None)
         l0 = lib.sr_launch_count()
         prof_graph = eng.capture(install=False)
-        per_step_launches = lib.sr_launch_count() - l0
+        launches = int((lib.sr_launch_count() - l0) * args.steps)   # every replay launches them once
         for _ in range(3):
             prof_graph.replay()
         torch.cuda.synchronize()
+        # durations of the last replay's launches (one step)
         _native.check(lib.sr_model_profile(model.handle, 0, cat_ms, cat_n), "sr_model_profile")
-        launches = int(per_step_launches * args.steps)  # every replay launches them once
-        for i in range(8):
-            cat_ms[i] *= args.steps
         del prof_graph
+    per_kernel = {c: cat_ms[i] for i, c in enumerate(CATS)}
+    k3_ms, draft_ms = time_step_pieces(eng, lib, _native)
     outs_ok = all(o == t[: len(o)] for o, t in zip(eng.outputs(), truth))
     h = hist.cpu().numpy().reshape(-1, 4)
     live = h[h[:, 0] + h[:, 2] > 0]
@@ -258,12 +304,11 @@ def run_ours(args, rank, world, dist):
     # ---- e2e: same steps through the public API with host buffers each step
     budget_h = torch.tensor(budget, dtype=torch.int32).pin_memory()
     out_h = torch.empty((B, 4 + K + 2), dtype=torch.int32).pin_memory()
-    e2e_in = budget_h.numel() * 4
-    e2e_out = out_h.numel() * 4
-    lib.sr_model_profile(model.handle, 0, None, None)
+    e2e_in, e2e_out = budget_h.numel() * 4, out_h.numel() * 4
     gen1 = eng.gen_len.sum()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.arm(True)
     if args.eager:
         e0.record(st)
         for _ in range(args.steps):
@@ -295,35 +340,31 @@ def run_ours(args, rank, world, dist):
         check_sum += int(out2[(args.steps - 1) % 2][0, 2])
         e1.record(st)
     barrier()
+    clocks.arm(False)
     e2e_ms = e0.elapsed_time(e1)
     e2e_committed = int((eng.gen_len.sum() - gen1).item())
-    # drift check: the e2e steps run on contexts ~(K + 3) * tokens/window
-    # longer than the device-timed ones; the same device replay after them
-    # separates that from the host-facing overhead
-    gen2 = eng.gen_len.sum()
-    barrier()
-    ev0.record(st)
-    for _ in range(args.steps):
-        eng.step()
-    ev1.record(st)
-    barrier()
-    after_ms = ev0.elapsed_time(ev1)
-    after_committed = int((eng.gen_len.sum() - gen2).item())
 
     # ---- cross-rank reduction: max time, summed tokens
     from paper_2511_16193_b200.dist import reduce_step_stats
 
-    (ms_max, e2e_max, after_max), (tot_committed, tot_e2e, tot_after) = reduce_step_stats(
-        [ms, e2e_ms, after_ms], [committed, e2e_committed, after_committed], dist, device="cuda")
+    (ms_max, e2e_max), (tot_committed, tot_e2e) = reduce_step_stats(
+        [ms, e2e_ms], [committed, e2e_committed], dist, device="cuda")
 
-    # ---- roofline of the dominant kernel family: the verify GEMMs (tensor-bound)
-    gemm_ms = sum(cat_ms[i] for i in range(5))
+    # ---- rooflines
+    burst, sustained, hbm, src = peaks()
+    step_ms = ms / args.steps
     rows = B * (K + 1)
     flops_step = 2.0 * rows * s.linear_params()
-    burst, sustained, hbm, src = peaks()
-    achieved = flops_step * args.steps / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
-    attn_ms = cat_ms[5] + cat_ms[7]
-    step_ms = ms / args.steps
+    gemm_ms = sum(per_kernel[c] for c in CATS[:5])
+    attn_ms = per_kernel["attention"] + per_kernel["attention_combine"]
+    bracket_sum = sum(per_kernel.values()) + k3_ms + draft_ms
+    achieved = flops_step / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    # attention reads every committed key of every verified request once per
+    # layer: mean context over the timed steps x KV bytes/token, + q and out
+    ctx_mean = 0.5 * (ctx_sum + ctx_sum_end)
+    attn_bytes = ctx_mean * s.kv_bytes_per_token() + 2 * rows * s.layers * s.q_heads * s.head_dim * 2
+    k3_bytes = rows * 8 + B * (4 + 16 + (K + 2) * 4)   # ids + targets in; lengths, outcome rows, tokens
+    ncu_round, gate_up_traffic = ncu_traffic()
     result = {
         "metric": METRIC, "value": tot_committed / (ms_max * 1e-3), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -336,81 +377,259 @@ def run_ours(args, rank, world, dist):
                     f"accept_draw u < latent_accept['{args.accept_method}'] (sim.py:322-336)"
                     if args.drafter == "synthetic" else "n-gram (vLLM prompt lookup, min_n=1, max_n=3)"),
         "outputs_equal_plain_greedy": outs_ok,
-        "ngram_probe": ngram_probe,
         "mean_proposed": proposed_mean,
         "tokens_per_window": committed_per_window,
-        "roofline": {"bound": "tensor", "kernel": "verify GEMMs (qkv, o, gate_up+SwiGLU, down, lm_head+argmax)",
-                     "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
-                     "frac": (achieved / sustained) if achieved else None,
-                     "peak_source": f"{src} bf16_tflops_sustained (kernels timed inside the step)",
-                     "traffic": traffic_bytes(),
-                     "traffic_note": "DRAM read+write bytes per launch of the largest verify GEMM (gate_up "
-                                     "+SwiGLU) from profiles/r01/ncu_step_layer0.json (ncu --set full); "
-                                     "algorithmic = 55.0 MB weights + 3.9 MB activations in + 22.9 MB "
-                                     "SwiGLU output (written to L2, consumed there by down: DRAM sees "
-                                     "weights + activations + a partial write-back)",
-                     "algorithmic_flops_per_step": flops_step,
-                     "gemm_ms_per_step": gemm_ms / args.steps,
-                     "gemm_share_of_step": (gemm_ms / args.steps) / step_ms,
-                     "attention_ms_per_step": attn_ms / args.steps,
-                     "attention_combine_ms_per_step": cat_ms[7] / args.steps,
-                     "other_ms_per_step": cat_ms[6] / args.steps,
-                     "per_gemm_ms_per_step": {n: cat_ms[i] / args.steps for i, n in
-                                              enumerate(["qkv", "o", "gate_up", "down", "lm_head"])}},
+        "roofline": {
+            "bound": "tensor", "kernel": "verify GEMMs (qkv+RoPE, o+residual+norm, gate_up+SwiGLU, down, "
+                                        "lm_head+argmax)",
+            "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
+            "frac": (achieved / burst) if achieved else None,
+            "frac_of_sustained": (achieved / sustained) if achieved else None,
+            "peak_source": f"{src} bf16_tflops (burst: clocks are sampled unthrottled in the step; "
+                           f"frac_of_sustained divides by bf16_tflops_sustained)",
+            "traffic": gate_up_traffic,
+            "traffic_note": (f"DRAM read+write bytes per launch of gate_up (the largest verify GEMM; algorithmic: "
+                             f"55.0 MB weights + 3.9 MB activations in + 22.9 MB SwiGLU out) from ncu --set full, "
+                             f"profiles/{ncu_round}/ncu_step_layer0.json") if gate_up_traffic else "no ncu capture",
+            "algorithmic_flops_per_step": flops_step,
+            "gemm_ms_per_step": gemm_ms,
+            "per_kernel_ms_per_step": {c: per_kernel[c] for c in CATS},
+            "per_kernel_note": "event-bracketed durations of each launch (a profiling graph of one step, "
+                               "its third replay); "
+                               "brackets break the programmatic-dependent-launch overlap, so their sum "
+                               "(bracket_sum_ms) exceeds ms_per_step; shares_of_step scale them to the step",
+            "bracket_sum_ms": bracket_sum,
+            "shares_of_step": {**{c: per_kernel[c] / bracket_sum for c in CATS},
+                               "accept_k3": k3_ms / bracket_sum, "drafter": draft_ms / bracket_sum},
+            "families": {
+                "verify_gemms": {"bound": "tensor", "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
+                                 "frac": (achieved / burst) if achieved else None},
+                "attention": {"bound": "hbm", "unit": "GB/s", "peak": hbm,
+                              "algorithmic_bytes_per_step": attn_bytes,
+                              "achieved": attn_bytes / (attn_ms * 1e-3) / 1e9 if attn_ms > 0 else None,
+                              "frac": attn_bytes / (attn_ms * 1e-3) / 1e9 / hbm if attn_ms > 0 else None,
+                              "ms_per_step": attn_ms},
+                "accept_k3": {"bound": "latency", "unit": "GB/s", "peak": hbm,
+                              "algorithmic_bytes_per_step": k3_bytes, "ms_per_step": k3_ms,
+                              "achieved": k3_bytes / (k3_ms * 1e-3) / 1e9 if k3_ms > 0 else None,
+                              "note": "argmax is fused into the lm_head epilogue, so K3 moves ~20 KB: "
+                                      "launch-latency bound (timed alone, graph of 20 launches)"},
+                "drafter": {"ms_per_step": draft_ms, "kind": args.drafter},
+            }},
         "e2e": {"value": tot_e2e / (e2e_max * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": e2e_in, "d2h_bytes_per_step": e2e_out,
-                "device_value_after": tot_after / (after_max * 1e-3),
-                "note": "device_value_after = the device-resident replay of the same number of steps run "
-                        "right after the e2e steps (longer contexts): e2e vs it is the host-facing cost"},
+                "path": "RolloutEngine.capture_io/step_io: pinned H2D budgets, step, D2H outcome rows + tokens"},
         "gpu_launches": int(launches),
-        "clocks": clocks.summary(),
     }
-    return result, (s, model, prompts)
+    return result, (s, model, prompts, trace, truth), clocks
 
 
-def probe_ngram(RolloutEngine, NgramDrafter, model, prompts, budget, truth, steps=8):
-    """Measured acceptance of the real n-gram drafter on this workload (not timed)."""
+def time_step_pieces(eng, lib, _native):
+    """K3 (fused accept + commit) and the drafter kernel timed alone: a graph
+    of 20 launches on scratch copies of the engine state, CUDA events."""
     import torch
 
-    eng = RolloutEngine(model, prompts, budget, k=K, drafters=(NgramDrafter(1, 3),), bonus_token=True,
-                        history=steps)
+    seq_len, gen_len, tokens = eng.seq_len.clone(), eng.gen_len.clone(), eng.tokens.clone()
+    out = torch.zeros_like(eng.history[0])
+    bon = torch.zeros_like(eng.bon)
+
+    def k3():
+        st = _native.stream_handle()       # the capturing stream
+        _native.check(lib.sr_accept_commit(
+            eng.m.handle, eng.B, eng.N, eng.seqs.data_ptr(), eng.token_ids.data_ptr(), eng.target_ids.data_ptr(),
+            tokens.data_ptr(), eng.stride, seq_len.data_ptr(), gen_len.data_ptr(), eng.max_new.data_ptr(),
+            eng.bonus, out.data_ptr(), bon.data_ptr(), st), "sr_accept_commit")
+
+    d = eng.drafters[0]
+    drafts, nd = torch.empty_like(eng.drafts[0]), torch.empty_like(eng.ndraft[0])
+
+    def draft():
+        st = _native.stream_handle()
+        if hasattr(d, "truth"):
+            _native.check(lib.sr_synthetic_draft(
+                eng.B, eng.k, d.truth.data_ptr(), d.stride, d.truth_len.data_ptr(), d.uniforms.data_ptr(),
+                d.stride, d.p.data_ptr(), gen_len.data_ptr(), d.vocab or eng.m.s.vocab, drafts.data_ptr(),
+                nd.data_ptr(), st), "sr_synthetic_draft")
+        else:
+            _native.check(lib.sr_ngram_propose(
+                eng.B, tokens.data_ptr(), eng.stride, seq_len.data_ptr(), d.min_n, d.max_n, eng.k,
+                drafts.data_ptr(), nd.data_ptr(), eng.ngram_scratch.data_ptr(), st), "sr_ngram_propose")
+
+    res = []
+    for fn in (k3, draft):
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            g.capture_begin()
+            for _ in range(20):
+                fn()
+            g.capture_end()
+        torch.cuda.current_stream().wait_stream(s)
+        g.replay()
+        res.append(timed(g.replay, 5) / 20)
+    return res
+
+
+# -- variants (one GPU, rank 0): the real n-gram drafter, configs[2], K4 alone ------------
+
+
+def variant_ngram(args, s, model, prompts, truth, steps=20, warmup=3):
+    """The headline config with the real n-gram drafter (vLLM prompt lookup)
+    in place of the reference-acceptance drafter: steady state, CUDA graph."""
+    import torch
+
+    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine
+
+    budget = [8 + (K + 1) * (steps + warmup + 4)] * len(prompts)
+    eng = RolloutEngine(model, prompts, budget, k=K, drafters=(NgramDrafter(1, 3),), bonus_token=True, history=1)
     eng.prefill()
-    for _ in range(steps):
+    eng.capture()
+    for _ in range(warmup):
         eng.step()
-    torch.cuda.synchronize()
-    h = eng.outcome_rows().reshape(-1, 4)
+    hist = torch.zeros((steps, eng.B, 4), dtype=torch.int32, device="cuda")
+    gen0 = int(eng.gen_len.sum())
+
+    def run():
+        for i in range(steps):
+            eng.step()
+            hist[i].copy_(eng.history[0])
+    ms = timed(run, 1)
+    committed = int(eng.gen_len.sum()) - gen0
+    h = hist.cpu().numpy().reshape(-1, 4)
     live = h[h[:, 0] + h[:, 2] > 0]
     same = all(o == t[: len(o)] for o, t in zip(eng.outputs(), truth))
-    return {"steps": steps, "mean_proposed": float(live[:, 0].mean()), "mean_accepted": float(live[:, 1].mean()),
-            "tokens_per_window": float(live[:, 2].mean()), "outputs_equal_plain_greedy": same}
+    return {"value": committed / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
+            "mean_proposed": float(live[:, 0].mean()), "mean_accepted_length": float(live[:, 1].mean()),
+            "tokens_per_window": float(live[:, 2].mean()), "outputs_equal_plain_greedy": same,
+            "note": "random-init weights and random prompts: the target's outputs rarely repeat a context "
+                    "n-gram, so windows are mostly empty (1 committed token per request per step)"}
 
 
-# -- CPU baseline (oracle port of the same path) ----------------------------------------
-
-
-def cpu_baseline(s, model, prompts, requests=8, prompt_cap=128, windows=24):
-    """Bounded sample of the same workload through the CPU oracle port."""
+def variant_ngram_kernel(lib, _native, B=1024, L=20480, reps=20):
+    """K4 alone at SURVEY §8(d)'s large shape: 1024 requests x 20K context."""
     import torch
 
-    from oracle.qwen2_oracle import CachedRollout, Qwen2Oracle
+    g = torch.Generator(device="cuda").manual_seed(0)
+    stride = L + 64
+    tokens = torch.randint(0, 1000, (B, stride), generator=g, device="cuda", dtype=torch.int32)
+    lens = torch.full((B,), L, dtype=torch.int32, device="cuda")
+    drafts = torch.empty((B, K), dtype=torch.int32, device="cuda")
+    nd = torch.empty(B, dtype=torch.int32, device="cuda")
+    scratch = torch.zeros(2 * B, dtype=torch.int64, device="cuda")
+    st = _native.stream_handle()
+
+    def go():
+        _native.check(lib.sr_ngram_propose(B, tokens.data_ptr(), stride, lens.data_ptr(), 1, 3, K,
+                                           drafts.data_ptr(), nd.data_ptr(), scratch.data_ptr(), st), "ngram")
+    for _ in range(3):
+        go()
+    ms = timed(go, reps)
+    nbytes = B * L * 4
+    _, _, hbm, _ = peaks()
+    return {"shape": f"{B} requests x {L} context tokens (int32), min_n=1, max_n=3, k={K}",
+            "us_per_launch": ms * 1e3, "algorithmic_bytes": nbytes,
+            "achieved_gbs": nbytes / (ms * 1e-3) / 1e9, "frac_of_hbm": nbytes / (ms * 1e-3) / 1e9 / hbm}
+
+
+def variant_configs2(steps=10, warmup=2, batch=64, graph=True):
+    """configs[2] on one GPU: Qwen2.5-7B-shaped target, the per-GPU share of
+    batch 512 over 8 GPUs (64 prompts), Best-of-N with N = 3 drafters
+    (n-gram + 0.5B- and 1.5B-shaped random-init model drafters), k = 4."""
+    import torch
+
+    from paper_2511_16193_b200.engine import ModelDrafter, NgramDrafter, RolloutEngine
+    from paper_2511_16193_b200.model import DeviceModel, init_weights, shape
+
+    s = shape("qwen2.5-7b")
+    trace, prompts, budget = workload(0, batch, steps + warmup + 4, s.vocab)
+    max_len = max(len(p) for p in prompts) + budget[0] + K + 8
+    N = 3
+    w = init_weights(s, seed=0, device="cuda")
+    m = DeviceModel(s, w, dtype="bf16", max_requests=batch, max_len=max_len, max_tokens=batch * N * (K + 1),
+                    max_seqs=batch * N, branches=batch * (N - 1))
+    del w
+    drafters = [NgramDrafter(1, 3)]
+    for name in ("qwen2.5-0.5b", "qwen2.5-1.5b"):
+        ds = shape(name)
+        dw = init_weights(ds, seed=1, device="cuda")
+        dm = DeviceModel(ds, dw, dtype="bf16", max_requests=batch, max_len=max_len, max_tokens=batch * (K + 2),
+                         max_seqs=batch)
+        del dw
+        drafters.append(ModelDrafter(dm, name=name))
+    torch.cuda.empty_cache()
+    eng = RolloutEngine(m, prompts, budget, k=K, drafters=tuple(drafters), bonus_token=True, history=1)
+    eng.prefill()
+    if graph:
+        eng.capture()
+    for _ in range(warmup):
+        eng.step()
+    gen0 = int(eng.gen_len.sum())
+    ms = timed(lambda: [eng.step() for _ in range(steps)], 1)
+    committed = int(eng.gen_len.sum()) - gen0
+    out = {"value": committed / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
+           "config": f"configs[2] per-GPU share: qwen2.5-7b-shaped target, {batch} prompts, k={K}, Best-of-N "
+                     f"N=3 (n-gram + 0.5B + 1.5B-shaped model drafters), greedy",
+           "note": "random-init drafters are rarely accepted: ~1 token per request per step; the step is "
+                   "dominated by the two model drafters' k+1 small-M forwards and the M=960 verify"}
+    del eng, m, drafters
+    torch.cuda.empty_cache()
+    return out
+
+
+# -- CPU baselines (ports of the same path; test infrastructure, oracle/) --------------------
+
+
+def cpu_port_sample(s, weights, prompts, trace, batch, prompt_cap, windows, warmup=1, method="draft-0.5b"):
+    """Bounded sample of the benched step on the host: ``batch`` requests
+    (prompts capped at ``prompt_cap`` tokens), the same reference-acceptance
+    drafter over the port's own greedy continuation, k = 4, bonus on; each
+    window is one batched forward (oracle/qwen2_oracle.py BatchedRollout)."""
+    import torch
+
+    from oracle.qwen2_oracle import BatchedRollout, Qwen2Oracle
+    from oracle.rollout_oracle import accept_uniforms
 
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
-    w = weights_to_cpu(s, model)
-    runner = CachedRollout(Qwen2Oracle(s, w, "bf16"))
-    ps = [p[:prompt_cap].tolist() for p in prompts[:requests]]
-    seqs = runner.prefill(ps)
+    ps = [p[:prompt_cap].tolist() for p in prompts[:batch]]
+    reqs = trace[:batch]
+    port = BatchedRollout(Qwen2Oracle(s, weights, "bf16"), rows=len(ps) * (K + 1))
     t0 = time.perf_counter()
-    committed = 0
-    for _ in range(windows):
-        for r in range(requests):
-            c, _, _ = runner.step(r, seqs[r], K)
-            committed += c
-    dt = time.perf_counter() - t0
-    return {"value": committed / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{requests} requests x {windows} windows (k={K}, n-gram) of the full "
-                      f"{s.layers}-layer {s.name} model on CPU (oracle/qwen2_oracle.py CachedRollout, "
-                      f"bf16-emulated torch, prompts truncated to {prompt_cap} tokens), {dt:.1f} s"}
+    port.prefill(ps)
+    # the continuation the drafter proposes from (drafts past its end: none)
+    tl = 4 * (windows + warmup) + 8
+    truth = port.greedy(ps, tl)
+    setup = time.perf_counter() - t0
+    vocab = s.vocab
+    us = [accept_uniforms(0, r.id, method, tl + K) for r in reqs]
+    pr = [r.latent_accept[method] for r in reqs]
+    seqs = [list(p) for p in ps]
+    gen = [0] * len(ps)
+
+    def drafts():
+        out = []
+        for r in range(len(ps)):
+            g = gen[r]
+            out.append([truth[r][g + j] if us[r][g + j] < pr[r] else (truth[r][g + j] + 1) % vocab
+                        for j in range(K) if g + j < tl])
+        return out
+
+    times, committed, acc = [], 0, []
+    for i in range(warmup + windows):
+        t = time.perf_counter()
+        res = port.window(seqs, drafts())
+        dt = time.perf_counter() - t
+        for r, (n, a, c) in enumerate(res):
+            gen[r] += c
+        if i >= warmup:
+            times.append(dt)
+            committed += sum(c for _, _, c in res)
+            acc += [a for _, a, _ in res]
+    # committed output == the port's greedy continuation (as far as it was computed)
+    ok = all(seqs[r][len(ps[r]):][:tl] == truth[r][: min(gen[r], tl)] for r in range(len(ps)))
+    return {"committed": committed, "seconds": sum(times), "times": times, "threads": threads, "setup_s": setup,
+            "mean_accepted_length": float(np.mean(acc)) if acc else 0.0, "outputs_equal_port_greedy": ok}
 
 
 def weights_to_cpu(s, model):
@@ -419,6 +638,7 @@ def weights_to_cpu(s, model):
     w = {"embed": model.embed.float().cpu(), "final_norm": model.final_norm.cpu(), "layers": []}
     w["lm_head"] = w["embed"] if s.tied else model.lm_head.float().cpu()
     nq, nkv, hd, I = s.q_heads * s.head_dim, s.kv_heads * s.head_dim, s.head_dim, s.intermediate
+
     def unpair(x, heads):
         return pair_deinterleave_heads(x, heads, hd) if model.fused_rope else x
 
@@ -434,43 +654,78 @@ def weights_to_cpu(s, model):
     return w
 
 
+def cpu_baseline(s, model, prompts, trace, truth, batch=16, prompt_cap=128, windows=6):
+    r = cpu_port_sample(s, weights_to_cpu(s, model), prompts, trace, batch, prompt_cap, windows)
+    return {"value": r["committed"] / r["seconds"], "unit": UNIT, "cores": r["threads"], "kind": "port",
+            "sample": f"{batch} requests (prompts capped at {prompt_cap} tokens) x {windows} windows of the "
+                      f"benched step (k={K}, same reference-acceptance drafter law over the port's own greedy "
+                      f"continuation, bonus on) through the full {s.layers}-layer {s.name} model on the host, "
+                      f"one batched forward per window (oracle/qwen2_oracle.py BatchedRollout, bf16-emulated "
+                      f"torch), {r['seconds']:.1f} s timed",
+            "mean_accepted_length": r["mean_accepted_length"]}
+
+
+def cpu_baseline_simulator(batch=256):
+    """SURVEY §8(d) CPU baseline (i): the reference's own rollout path -- the
+    virtual-time simulator -- at the config's batch, one core.  The
+    reference tree is not on the GPU box, so this times its restatement
+    (paper_2511_16193_b200/sim.py, vendored) with the CPU oracle verifier
+    (oracle/rollout_oracle.py): decoupled policy, default trace."""
+    from oracle.rollout_oracle import OracleVerifier
+    from paper_2511_16193_b200 import scenarios
+    from paper_2511_16193_b200.sim import SimConfig, simulate
+    from paper_2511_16193_b200.workload import gen_trace
+
+    cfg = SimConfig(trace=gen_trace(scenarios.default_trace_spec(batch=batch, seed=0)),
+                    model=scenarios.default_cost_model(), policy="decoupled", method=scenarios.DEFAULT_METHOD,
+                    seed=0, scale_cost=scenarios.default_scale_cost(), estimator_priors=scenarios.estimator_priors())
+    t0 = time.perf_counter()
+    m = simulate(cfg, verifier_factory=OracleVerifier)
+    dt = time.perf_counter() - t0
+    return {"value": m.total_committed / dt, "unit": "committed tokens/s (host wall time)", "cores": 1,
+            "kind": "port",
+            "sample": f"reference simulate() restatement, decoupled policy, batch {batch}, default trace, "
+                      f"{m.total_committed} committed tokens in {dt:.1f} s; the reference prices the model "
+                      f"in virtual time (no arithmetic), so this is its rollout bookkeeping rate"}
+
+
+# -- reference arm ------------------------------------------------------------------------
+
+
 def run_reference(args):
-    """The reference arm: the CPU implementation of the path (oracle port;
-    the reference itself is a Python simulator with no model arithmetic)."""
+    """The reference arm: the CPU implementation of the benched path (the
+    reference itself is a Python simulator with no model arithmetic, so the
+    oracle port of the same step runs), batched over requests, same drafter
+    law, on a bounded sample of the workload: each step is one window for
+    ``--ref-batch`` requests with prompts capped at ``--ref-prompt-cap``."""
     import torch
 
     from paper_2511_16193_b200.model import init_weights, shape
 
     s = shape(args.model, args.layers)
-    torch.set_num_threads(os.cpu_count() or 1)
-    _, prompts, _ = workload(0, args.batch, 1, s.vocab)
-    from oracle.qwen2_oracle import CachedRollout, Qwen2Oracle
-
+    trace, prompts, _ = workload(0, args.batch, 1, s.vocab)
     w = init_weights(s, seed=0, device="cpu")
-    runner = CachedRollout(Qwen2Oracle(s, w, "bf16"))
+    r = cpu_port_sample(s, w, prompts, trace, args.ref_batch, args.ref_prompt_cap, args.steps,
+                        warmup=max(args.warmup, 1), method=args.accept_method)
     del w
-    reqs = 2
-    seqs = runner.prefill([p[:128].tolist() for p in prompts[:reqs]])
-    for _ in range(max(args.warmup, 1)):
-        for r in range(reqs):
-            runner.step(r, seqs[r], K)
-    times, committed = [], 0
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        for r in range(reqs):
-            c, _, _ = runner.step(r, seqs[r], K)
-            committed += c
-        times.append(time.perf_counter() - t0)
-    total = sum(times)
-    value = committed / total
-    sample = (f"{reqs} requests x {args.steps} windows (k={K}, n-gram) through the full {s.layers}-layer "
-              f"{s.name} model, oracle port (torch CPU, bf16-emulated), prompts truncated to 128 tokens")
+    value = r["committed"] / r["seconds"]
+    sample = (f"{args.ref_batch} requests (prompts capped at {args.ref_prompt_cap} tokens) x {args.steps} "
+              f"timed windows (after {max(args.warmup, 1)} warm-up) of the benched step: k={K}, reference-"
+              f"acceptance drafter law over the port's own greedy continuation, bonus on, full {s.layers}-layer "
+              f"{s.name} model, one batched forward per window (oracle/qwen2_oracle.py BatchedRollout, "
+              f"bf16-emulated torch, {r['threads']} threads)")
+    cfg = {"workload": f"bounded CPU sample of configs[1]: {args.model}-shaped target, batch {args.ref_batch} "
+                       f"(of {args.batch}/GPU), prompts capped at {args.ref_prompt_cap}, k={K}, single synthetic "
+                       f"drafter (same law), greedy exact match, bonus token",
+           "model": args.model, "layers": s.layers, "batch_per_gpu": args.ref_batch, "global_batch": args.ref_batch,
+           "k": K, "verify_rows_per_step": args.ref_batch * (K + 1),
+           "prompt_len": f"U[128,1024] capped at {args.ref_prompt_cap}", "parallelism": "host threads"}
     return {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic", "config": workload_config(args, s, args.gpus),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-                             "sample": sample},
+            "data": "synthetic", "config": cfg, "mean_accepted_length": r["mean_accepted_length"],
+            "outputs_equal_port_greedy": r["outputs_equal_port_greedy"],
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["threads"], "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -490,14 +745,27 @@ def main():
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         tdist.init_process_group("nccl")
         dist = tdist
-    result, ctx = run_ours(args, rank, world, dist)
+    result, ctx, clocks = run_ours(args, rank, world, dist)
     if rank == 0:
+        from paper_2511_16193_b200 import _native
         from paper_2511_16193_b200.model import shape
-        # the CPU sample of a >10B model would need its fp32 weights in host RAM
-        if world == 1 and not args.no_cpu_baseline and shape(args.model).linear_params() <= 10e9:
-            result["cpu_baseline"] = cpu_baseline(*ctx)
-        else:
-            result["cpu_baseline"] = None
+
+        s, model, prompts, trace, truth = ctx
+        if world == 1 and not args.no_variants and args.layers is None and args.model == MODEL:
+            lib = _native.lib()
+            result["variants"] = {"ngram": variant_ngram(args, s, model, prompts, truth),
+                                  "ngram_kernel": variant_ngram_kernel(lib, _native)}
+        cpu_ok = world == 1 and not args.no_cpu_baseline and shape(args.model).linear_params() <= 10e9
+        result["cpu_baseline"] = cpu_baseline(s, model, prompts, trace, truth) if cpu_ok else None
+        result["cpu_baseline_simulator"] = cpu_baseline_simulator() if cpu_ok else None
+        if "variants" in result:
+            del model, ctx
+            import torch
+            torch.cuda.empty_cache()
+            result["variants"]["configs2_7b"] = variant_configs2()
+    clocks.stop()
+    result["clocks"] = clocks.summary()
+    if rank == 0:
         print(json.dumps(result), flush=True)
     if dist is not None:
         dist.barrier()

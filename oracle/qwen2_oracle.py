@@ -308,3 +308,120 @@ class CachedRollout:
         c = (len(d) + (1 if bonus else 0)) if a == len(d) and d else (a + 1)
         seq += y[:c]
         return c, len(d), a
+
+
+class BatchedRollout:
+    """Batched, KV-cached CPU port of the benched rollout step (bench.py's
+    ``--impl reference`` arm and ``cpu_baseline``): every window of the batch
+    goes through ONE forward -- the projections and MLP as GEMMs over all
+    window rows, attention per request over its cache -- with the oracle's
+    arithmetic, then exact-match acceptance with the reference's commit rule
+    (sim.py:983-1042, bonus token on as in the bench).
+
+    Drafts follow the bench's reference-acceptance law: the
+    draft at output position g is the target's own greedy token ``truth[g]``
+    (from this port's plain decode) when the reference's keyed acceptance
+    uniform ``u[g] < p`` (sim.py:322-336), else a wrong token.
+
+    Like the GPU path, the port must compute a position's token identically
+    in a plain-decode step and in a speculation window, or its own greedy
+    continuation would not verify: host BLAS results depend on the GEMM's row
+    count (thread partitioning), so decode steps and windows run the same
+    padded row count ``rows``, and window attention runs query row by query
+    row (a batched einsum's result depends on the window length)."""
+
+    def __init__(self, oracle: Qwen2Oracle, rows: int | None = None):
+        self.o = oracle
+        self.rows = rows
+        self.kc: list[list[torch.Tensor]] = []
+        self.vc: list[list[torch.Tensor]] = []
+
+    @torch.no_grad()
+    def forward(self, windows, prefill: bool = False) -> list[torch.Tensor]:
+        """``windows`` = [(request, tokens, start)]; positions [start, start +
+        len) of each request, keys [0, start) from its cache.  Returns the
+        logits of each window's rows."""
+        o, s = self.o, self.o.s
+        nq, nkv, hd = s.q_heads, s.kv_heads, s.head_dim
+        G = nq // nkv
+        toks = [t for _, ts, _ in windows for t in ts]
+        lens = [len(ts) for _, ts, _ in windows]
+        n_real = len(toks)
+        if not prefill and self.rows:
+            if n_real > self.rows:
+                raise ValueError("window rows exceed the port's fixed row count")
+            toks += [0] * (self.rows - n_real)
+        x = o.embed[torch.as_tensor(toks, dtype=torch.long)].to(o.acc)
+        scale = float(np.sqrt(hd))
+        for li, L in enumerate(o.layers):
+            qkv = o._normed_proj(x, L["ln1"], L["wqkv"]) + L["bqkv"]
+            outs, r0 = [], 0
+            for (req, ts, start), T in zip(windows, lens):
+                pos = torch.arange(start, start + T)
+                blk = qkv[r0:r0 + T]
+                r0 += T
+                q = o._rope(blk[:, : nq * hd].view(T, nq, hd), pos)
+                k = o._rope(blk[:, nq * hd: (nq + nkv) * hd].view(T, nkv, hd), pos)
+                v = o._r(blk[:, (nq + nkv) * hd:].view(T, nkv, hd))
+                kc = torch.cat([self.kc[req][li][:start], k]) if start else k
+                vc = torch.cat([self.vc[req][li][:start], v]) if start else v
+                self.kc[req][li], self.vc[req][li] = kc, vc
+                kk, vv = kc.repeat_interleave(G, 1), vc.repeat_interleave(G, 1)
+                if prefill:
+                    sc = torch.einsum("qhd,khd->hqk", q, kk) / scale
+                    sc = sc.masked_fill(torch.ones(T, start + T, dtype=torch.bool).triu(start + 1), float("-inf"))
+                    p = torch.exp(sc - sc.amax(-1, keepdim=True))
+                    l = p.sum(-1, keepdim=True)
+                    outs.append(torch.einsum("hqk,khd->qhd", o._r(p), vv) / l.permute(1, 0, 2))
+                    continue
+                for i in range(T):   # one query row at a time: window-length invariant
+                    n = start + i + 1
+                    sc = torch.einsum("hd,khd->hk", q[i], kk[:n]) / scale
+                    p = torch.exp(sc - sc.amax(-1, keepdim=True))
+                    l = p.sum(-1, keepdim=True)
+                    outs.append((torch.einsum("hk,khd->hd", o._r(p), vv[:n]) / l)[None])
+            att = torch.cat(outs).reshape(-1, nq * hd)
+            if att.shape[0] < x.shape[0]:
+                att = torch.cat([att, att.new_zeros(x.shape[0] - att.shape[0], nq * hd)])
+            x = x + o._r(att) @ L["wo"].t()
+            g = o._normed_proj(x, L["ln2"], L["wg"])
+            u = o._normed_proj(x, L["ln2"], L["wu"])
+            x = x + o._r(g / (1.0 + torch.exp(-g)) * u) @ L["wd"].t()
+        lg = o._normed_proj(x[:n_real], o.final_norm, o.lm_head)
+        return list(torch.split(lg, lens))
+
+    def prefill(self, prompts) -> None:
+        """Cache every prompt token but the last (the first window starts from it)."""
+        for p in prompts:
+            self.kc.append([None] * len(self.o.layers))
+            self.vc.append([None] * len(self.o.layers))
+        self.forward([(r, list(p[:-1]), 0) for r, p in enumerate(prompts) if len(p) > 1], prefill=True)
+
+    def greedy(self, prompts, steps: int) -> list[list[int]]:
+        """Plain batched greedy decode of ``steps`` tokens per request (the
+        target continuation the reference-acceptance drafter proposes)."""
+        seqs = [list(p) for p in prompts]
+        out = [[] for _ in prompts]
+        for _ in range(steps):
+            lg = self.forward([(r, [s[-1]], len(s) - 1) for r, s in enumerate(seqs)])
+            for r, l in enumerate(lg):
+                t = int(torch.argmax(l[-1]))
+                out[r].append(t)
+                seqs[r].append(t)
+        return out
+
+    def window(self, seqs, drafts, bonus: bool = True) -> list[tuple[int, int, int]]:
+        """One speculation window for every request: verify ``drafts[r]``
+        after ``seqs[r]`` (committed tokens, extended in place).  Returns
+        per-request (proposed, accepted, committed)."""
+        lg = self.forward([(r, [s[-1]] + list(d), len(s) - 1) for r, (s, d) in enumerate(zip(seqs, drafts))])
+        res = []
+        for r, (s, d) in enumerate(zip(seqs, drafts)):
+            y = [int(t) for t in torch.argmax(lg[r], -1)]
+            a = 0
+            while a < len(d) and d[a] == y[a]:
+                a += 1
+            c = (len(d) + (1 if bonus else 0)) if (a == len(d) and d) else a + 1
+            s += y[:c]
+            res.append((len(d), a, c))
+        return res

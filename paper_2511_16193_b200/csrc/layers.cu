@@ -15,11 +15,16 @@ template <> __device__ __forceinline__ float from_f<float>(float v) { return v; 
 template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
 template <typename T>
-__global__ void embed_kernel(const T* __restrict__ table, const int32_t* __restrict__ ids, int H,
+__global__ void embed_kernel(const T* __restrict__ table, const int32_t* __restrict__ ids, int H, int vocab,
                              float* __restrict__ x) {
   grid_dep_sync();
   const int row = blockIdx.x;
-  const T* src = table + (int64_t)ids[row] * H;
+  // an id outside this model's vocabulary (a drafter whose vocabulary is
+  // smaller than the target's padded one, e.g. Qwen2.5-0.5B 151936 vs 7B
+  // 152064) embeds as token 0: drafts stay proposals, never out-of-bounds reads
+  int id = ids[row];
+  if (id < 0 || id >= vocab) id = 0;
+  const T* src = table + (int64_t)id * H;
   float* dst = x + (int64_t)row * H;
   for (int i = threadIdx.x; i < H; i += blockDim.x) dst[i] = to_f(src[i]);
 }
@@ -398,9 +403,9 @@ int norm_prep_rows(const float* x, const float* w, int M, int H, int parts, __nv
 }
 
 template <typename T>
-int embed_rows(const T* table, const int32_t* ids, int M, int H, float* x, cudaStream_t s) {
+int embed_rows(const T* table, const int32_t* ids, int M, int H, int vocab, float* x, cudaStream_t s) {
   if (M == 0) return SR_OK;
-  sr::launch_k(embed_kernel<T>, M, 256, 0, s, table, ids, H, x);
+  sr::launch_k(embed_kernel<T>, M, 256, 0, s, table, ids, H, vocab, x);
   return check_launch("embed_kernel");
 }
 
@@ -434,8 +439,8 @@ int argmax_rows(const float* logits, int M, int V, int ld, int32_t* ids, float* 
   return check_launch("argmax_rows_kernel");
 }
 
-template int embed_rows<float>(const float*, const int32_t*, int, int, float*, cudaStream_t);
-template int embed_rows<__nv_bfloat16>(const __nv_bfloat16*, const int32_t*, int, int, float*, cudaStream_t);
+template int embed_rows<float>(const float*, const int32_t*, int, int, int, float*, cudaStream_t);
+template int embed_rows<__nv_bfloat16>(const __nv_bfloat16*, const int32_t*, int, int, int, float*, cudaStream_t);
 template int rmsnorm_rows<float>(const float*, const float*, int, int, float, float*, cudaStream_t);
 template int rmsnorm_rows<__nv_bfloat16>(const float*, const float*, int, int, float, __nv_bfloat16*, cudaStream_t);
 template int rope_scatter<float>(const float*, const int32_t*, const SeqInfo*, int, int, const float*,

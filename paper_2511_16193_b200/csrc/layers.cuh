@@ -49,7 +49,7 @@ __host__ __device__ __forceinline__ int kv_phys(int slot, int d) {
 }
 
 template <typename T>
-int embed_rows(const T* table, const int32_t* ids, int M, int H, float* x, cudaStream_t s);
+int embed_rows(const T* table, const int32_t* ids, int M, int H, int vocab, float* x, cudaStream_t s);
 
 int norm_prep_rows(const float* x, const float* w, int M, int H, int parts, __nv_bfloat16* h, float* ssq,
                    cudaStream_t s);

@@ -350,7 +350,7 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
   if (a->output == 2) SR_TRY(sr::row_keys(seqs, S, a->positions, a->logit_rows, R, m->key_req, m->key_pos, st));
   if (d.dtype == 1) {
     using bf = __nv_bfloat16;
-    SR_TRY(sr::embed_rows<bf>((const bf*)d.embed, a->token_ids, M, H, m->x, st));
+    SR_TRY(sr::embed_rows<bf>((const bf*)d.embed, a->token_ids, M, H, d.vocab, m->x, st));
     // input norm of layer 0; every later norm is fused into the o / down GEMMs
     SR_TRY(sr::norm_prep_rows(m->x, (const float*)m->layer_ptrs[0], M, H, m->prep_parts, (bf*)m->h, m->ssq, st));
     // KV destination of every row, shared by all layers' qkv + RoPE epilogues
@@ -404,7 +404,7 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
       m->prof.end(st);
     }
   } else {
-    SR_TRY(sr::embed_rows<float>((const float*)d.embed, a->token_ids, M, H, m->x, st));
+    SR_TRY(sr::embed_rows<float>((const float*)d.embed, a->token_ids, M, H, d.vocab, m->x, st));
     for (int l = 0; l < d.layers; ++l) {
       const void* const* w = m->layer_ptrs.data() + (size_t)l * sr::kLayerPtrs;
       float* h = (float*)m->h;

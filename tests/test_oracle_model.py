@@ -96,3 +96,30 @@ def test_shapes_and_roofline_params():
     assert abs(SHAPES["qwen2.5-32b"].linear_params() / 31.98e9 - 1) < 0.01
     assert SHAPES["qwen2.5-1.5b"].kv_bytes_per_token() == 28672
     assert SHAPES["qwen2.5-7b"].kv_bytes_per_token() == 57344
+
+
+def test_batched_rollout_port_matches_oracle():
+    """The batched CPU port timed by bench.py's reference arm: its greedy
+    continuation equals the oracle's, and speculation windows with wrong
+    drafts still commit exactly that continuation."""
+    import numpy as np
+
+    from oracle.qwen2_oracle import BatchedRollout, Qwen2Oracle
+    from paper_2511_16193_b200.model import init_weights, shape
+
+    s = shape("tiny")
+    o = Qwen2Oracle(s, init_weights(s, seed=0), "bf16")
+    rng = np.random.default_rng(1)
+    ps = [rng.integers(0, s.vocab, int(rng.integers(5, 30))).tolist() for _ in range(3)]
+    port = BatchedRollout(o, rows=3 * 4)
+    port.prefill(ps)
+    g = port.greedy(ps, 10)
+    assert g == [o.greedy(p, 10) for p in ps]
+    seqs, gen = [list(p) for p in ps], [0, 0, 0]
+    while min(gen) < 10:
+        d = [[g[r][gen[r] + j] if j != 2 else (g[r][gen[r] + j] + 1) % s.vocab
+              for j in range(3) if gen[r] + j < 10] for r in range(3)]
+        for r, (n, a, c) in enumerate(port.window(seqs, d)):
+            assert a == min(n, 2)
+            gen[r] += c
+    assert all(seqs[r][len(ps[r]):][:10] == g[r] for r in range(3))
