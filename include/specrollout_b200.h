@@ -203,6 +203,10 @@ typedef struct sr_forward_args {
   float* out_val;           /* optional max logit per row (argmax output) */
   float temperature;        /* output 2: T > 0 */
   uint32_t seed;            /* output 2: sampling stream seed */
+  const int32_t* live_rows; /* optional device int: the batch's rows [0, *live_rows) are live
+                               (sr_build_verify_batch compaction); the bf16 GEMMs skip the rest.
+                               Must be written >= 2 kernel launches before the forward on its
+                               stream (the GEMMs read it before their dependency wait). */
 } sr_forward_args;
 
 /* Keyed Gumbel-max sampling of fp32 logit rows:
@@ -304,8 +308,9 @@ int sr_synthetic_draft(int num_requests, int k, const int32_t* truth, int64_t tr
                        int32_t* ndraft, sr_stream_t stream);
 
 /* K5 small-model drafter batches (drafting methods `draft-0.5b`/`draft-1.5b`,
- * scenarios.py:25-29, priced per token at sim.py:883-892).  Rows [b*(k+2),
- * +k+2) belong to request b.  step 0: catch-up of the committed tokens the
+ * scenarios.py:25-29, priced per token at sim.py:883-892).  Step 0: rows
+ * [b*(k+2), +k+2) belong to request b; steps >= 1: row b (run the forward
+ * over the first B rows).  step 0: catch-up of the committed tokens the
  * drafter has not cached, [dkv_len, seq_len) (advances dkv_len), logits at
  * the last one; step j in [1, k): decode the previous draft; step k: file the
  * last output and write ndraft.  prev_out [B] is the previous forward's
@@ -328,13 +333,18 @@ int sr_draft_model_batch(int num_requests, int k, int step, const int32_t* token
  * max_new_cap [B] (optional): max_new is clamped to it IN PLACE first --
  * the token row and KV pages of request b hold max_new_cap[b] outputs, and a
  * retired request (cap = gen_len) stays retired whatever budget the host
- * copies in. */
+ * copies in.
+ * live_rows (optional, device int): COMPACT the batch instead -- sequence
+ * s = b*N+n keeps its SeqInfo slot but its rows are packed back to back
+ * (q_start = exclusive prefix sum of q_len over s), so finished requests and
+ * unproposed draft slots take no rows; *live_rows = rows used.  Pass it on to
+ * sr_forward_args.live_rows and the GEMMs skip the dead tiles. */
 int sr_build_verify_batch(int num_requests, int num_drafters, int k, const int32_t* tokens,
                           int64_t tok_stride, const int32_t* seq_len, const int32_t* gen_len,
                           int32_t* max_new, const int32_t* max_new_cap, const int32_t* drafts,
                           const int32_t* ndraft,
                           const int32_t* window, int32_t* token_ids, int32_t* positions, void* seqs,
-                          sr_stream_t stream);
+                          int32_t* live_rows, sr_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -49,7 +49,7 @@ SIGNATURES: dict[str, list] = {
                             _vp, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp],
     "sr_pack_results": [_i32, _i32, _vp, _vp, _i64, _vp, _vp, _vp],
     "sr_build_verify_batch": [_i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                              _vp, _vp, _vp],
+                              _vp, _vp, _vp, _vp],
 }
 _RESTYPES = {"sr_last_error": ctypes.c_char_p, "sr_model_workspace_bytes": ctypes.c_uint64,
              "sr_launch_count": ctypes.c_longlong}
@@ -83,7 +83,7 @@ class ForwardArgs(ctypes.Structure):
                 ("num_tokens", "num_seqs", "max_q_len", "max_key", "output", "num_logit_rows")] + [
         (n, ctypes.c_void_p) for n in
         ("token_ids", "positions", "seqs", "logit_rows", "out", "out_val")] + [
-        ("temperature", ctypes.c_float), ("seed", ctypes.c_uint32)]
+        ("temperature", ctypes.c_float), ("seed", ctypes.c_uint32), ("live_rows", ctypes.c_void_p)]
     __slots__ = ()  # typos in field names raise instead of silently adding attributes
 
 _lib = None

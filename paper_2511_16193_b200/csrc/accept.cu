@@ -177,6 +177,93 @@ __global__ void build_verify_kernel(int B, int N, int k, const int32_t* __restri
   }
 }
 
+// Compacting variant (one CTA): sequences keep their index s = b*N + n, but
+// their rows are packed back to back -- q_start = exclusive prefix sum of
+// q_len in s order -- so finished requests, gap rounds and unproposed draft
+// slots occupy no rows; *live_rows = the packed row count, which the
+// forward's GEMMs read to skip dead tiles.  q_start stays non-decreasing in s
+// (an empty sequence takes the next live one's start), which the row ->
+// sequence binary searches of the forward rely on.
+constexpr int kCompactThreads = 1024;
+
+__global__ void __launch_bounds__(kCompactThreads)
+build_verify_compact_kernel(int B, int N, int k, const int32_t* __restrict__ tokens, int64_t tok_stride,
+                            const int32_t* __restrict__ seq_len, const int32_t* __restrict__ gen_len,
+                            int32_t* __restrict__ max_new, const int32_t* __restrict__ max_new_cap,
+                            const int32_t* __restrict__ drafts, const int32_t* __restrict__ ndraft,
+                            const int32_t* __restrict__ window, int32_t* __restrict__ token_ids,
+                            int32_t* __restrict__ positions, SeqInfo* __restrict__ seqs,
+                            int32_t* __restrict__ live_rows) {
+  grid_dep_sync();
+  __shared__ int warp_sum[kCompactThreads / 32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  const int S = B * N;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int s0 = 0; s0 < S; s0 += kCompactThreads) {
+    const int s = s0 + threadIdx.x;
+    int q_len = 0, nd = 0, b = 0, n = 0, L = 0;
+    if (s < S) {
+      b = s / N;
+      n = s % N;
+      int mn = max_new[b];
+      if (max_new_cap != nullptr) {
+        mn = min(mn, max_new_cap[b]);
+        if (n == 0) max_new[b] = mn;
+      }
+      const int remaining = mn - gen_len[b];
+      L = seq_len[b];
+      bool active = remaining > 0;
+      if (active) {
+        nd = drafts != nullptr ? ndraft[n * B + b] : 0;
+        active = nd >= 0;  // ndraft < 0: no window this round (decoupled gap round)
+        nd = max(0, min(nd, min(k, remaining)));
+        if (window != nullptr) nd = min(nd, max(0, window[b]));
+      }
+      q_len = active ? nd + 1 : 0;
+    }
+    // block-wide exclusive scan of q_len in s order
+    int x = q_len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int w = warp_sum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_sum[lane] = w;  // inclusive totals of warps 0..lane
+    }
+    __syncthreads();
+    const int start = carry + (wid ? warp_sum[wid - 1] : 0) + x - q_len;
+    if (s < S) {
+      SeqInfo sq;
+      sq.q_start = start;
+      sq.q_len = q_len;
+      sq.request = b;
+      sq.ctx_len = L - 1;
+      sq.branch = n == 0 ? -1 : b * (N - 1) + (n - 1);
+      sq.pad0 = sq.pad1 = sq.pad2 = 0;
+      seqs[s] = sq;
+      for (int j = 0; j < q_len; ++j) {
+        token_ids[start + j] =
+            j == 0 ? tokens[(int64_t)b * tok_stride + L - 1] : drafts[((int64_t)n * B + b) * k + j - 1];
+        positions[start + j] = L - 1 + j;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += warp_sum[kCompactThreads / 32 - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *live_rows = carry;
+}
+
 // Reference-acceptance drafter: proposes the target's own continuation
 // truth[g] for output position g when the reference's keyed acceptance draw
 // u[g] < p (sim.py:322-336), else a deterministic wrong token, so the
@@ -207,7 +294,8 @@ __global__ void synthetic_draft_kernel(int B, int k, const int32_t* __restrict__
 
 // Draft-model batches (K5).  step 0 = catch-up: the committed tokens the
 // drafter has not cached yet, [dkv_len, seq_len), with logits taken at the
-// last one; step j >= 1 = one decode step on the previous draft token.
+// last one (rows [b*(k+2), +k+2)); step j >= 1 = one decode step on the
+// previous draft token (row b: forward over the first B rows only).
 // The output of step j-1 (prev_out [B]) is filed as draft j-1.
 __global__ void draft_batch_kernel(int B, int k, int step, const int32_t* __restrict__ tokens, int64_t tok_stride,
                                    const int32_t* __restrict__ seq_len, const int32_t* __restrict__ gen_len,
@@ -247,12 +335,15 @@ __global__ void draft_batch_kernel(int B, int k, int step, const int32_t* __rest
     if (key_pos != nullptr) key_pos[b] = L;  // the draft's output position
     if (q > 0) dkv_len[b] = L;
   } else {
+    // decode steps: one row per request, packed at row b (the forward runs
+    // over B rows, not B * (k + 2))
     const int p = L - 1 + step;
+    sq.q_start = b;
     sq.q_len = step < want ? 1 : 0;
     sq.ctx_len = p;
-    token_ids[b * rows] = prev_out[b];
-    positions[b * rows] = p;
-    logit_rows[b] = b * rows;
+    token_ids[b] = prev_out[b];
+    positions[b] = p;
+    logit_rows[b] = b;
     if (key_pos != nullptr) key_pos[b] = p + 1;
   }
   seqs[b] = sq;
@@ -357,12 +448,18 @@ extern "C" int sr_build_verify_batch(int num_requests, int num_drafters, int k, 
                                      int32_t* max_new, const int32_t* max_new_cap, const int32_t* drafts,
                                      const int32_t* ndraft,
                                      const int32_t* window, int32_t* token_ids, int32_t* positions,
-                                     void* seqs, sr_stream_t stream) {
+                                     void* seqs, int32_t* live_rows, sr_stream_t stream) {
   SR_REQUIRE(num_requests >= 0 && num_drafters >= 1 && k >= 0, "bad batch shape");
   if (num_requests == 0) return SR_OK;
   SR_REQUIRE(tokens && seq_len && gen_len && max_new && token_ids && positions && seqs, "null pointer");
   SR_REQUIRE(drafts == nullptr || ndraft != nullptr, "drafts without ndraft");
   const int S = num_requests * num_drafters;
+  if (live_rows != nullptr) {
+    sr::launch_k(sr::build_verify_compact_kernel, 1, sr::kCompactThreads, 0, (cudaStream_t)stream, num_requests,
+                 num_drafters, k, tokens, tok_stride, seq_len, gen_len, max_new, max_new_cap, drafts, ndraft, window,
+                 token_ids, positions, reinterpret_cast<sr::SeqInfo*>(seqs), live_rows);
+    return sr::check_launch("build_verify_compact_kernel");
+  }
   sr::launch_k(sr::build_verify_kernel, sr::ceil_div(S, 128), 128, 0, (cudaStream_t)stream, 
       num_requests, num_drafters, k, tokens, tok_stride, seq_len, gen_len, max_new, max_new_cap, drafts, ndraft,
       window,

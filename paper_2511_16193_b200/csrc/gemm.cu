@@ -329,12 +329,28 @@ __device__ __forceinline__ void scale_chunk(uint32_t* v, float r) {
   for (int i = 0; i < W; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * r);
 }
 
+// Live-row count of a compacted verify batch (sr_build_verify_batch writes
+// it): tiles are walked over min(capacity, live) rows, so the rows of
+// finished requests and unproposed draft slots cost nothing.  Read before
+// griddepcontrol.wait, bypassing L1: the value is written by a kernel at
+// least two launches earlier in the stream, which has completed (and
+// flushed) before the immediately preceding kernel passes its own wait --
+// and this grid cannot start before that.  The tile schedule (and so every
+// row's accumulation order) does not depend on it: only the tile count does.
+__device__ __forceinline__ int live_rows(int cap, const int32_t* m_live) {
+  if (m_live == nullptr) return cap;
+  const int v = __ldcg(m_live);
+  return v < cap ? (v > 0 ? v : 0) : cap;
+}
+
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    int M, int N, int K, void* C, int ldc, const float* __restrict__ bias,
-                    int32_t* __restrict__ aux, SampleArgs sa, NormArgs na, RopeArgs ra) {
+                    int M_cap, const int32_t* __restrict__ m_live, int N, int K, void* C, int ldc,
+                    const float* __restrict__ bias, int32_t* __restrict__ aux, SampleArgs sa, NormArgs na,
+                    RopeArgs ra) {
   using Cfg = GemmCfg<BN>;
+  const int M = live_rows(M_cap, m_live);
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -522,9 +538,11 @@ constexpr bool kStagedEpi = (EPI == kEpiResidualF32 || EPI == kEpiResidualNorm) 
 template <int BN, int EPI, int MC, int KC>
 __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 int M, int N, int K, void* C, int ldc, const float* __restrict__ bias,
-                 int32_t* __restrict__ aux, SampleArgs sa, NormArgs na, RopeArgs ra) {
+                 int M_cap, const int32_t* __restrict__ m_live, int N, int K, void* C, int ldc,
+                 const float* __restrict__ bias, int32_t* __restrict__ aux, SampleArgs sa, NormArgs na,
+                 RopeArgs ra) {
   static_assert(MC == 1 || KC == 1 || KC == MC, "A multicast splits rows (KC 1) or k chunks (KC == MC)");
+  const int M = live_rows(M_cap, m_live);
   using Cfg = PairCfg<BN, KC>;
   constexpr int S = Cfg::kStages;
   constexpr int CW = Cfg::kChunk;
@@ -958,8 +976,8 @@ int launch_typed(const GemmPlan& p, int M, cudaStream_t stream) {
   }
   const int tiles = ((M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  sr::launch_k(kern, grid, kThreads, Cfg::kSmem, stream, p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux, p.sample,
-               p.norm, p.rope);
+  sr::launch_k(kern, grid, kThreads, Cfg::kSmem, stream, p.a, p.b, M, p.m_live, p.N, p.K, p.c, p.ldc, p.bias, p.aux,
+               p.sample, p.norm, p.rope);
   return check_launch("gemm_tcgen05_kernel");
 }
 
@@ -992,8 +1010,8 @@ int launch_pair_mc(const GemmPlan& p, int M, cudaStream_t stream) {
   const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * (((p.N + BN - 1) / BN + MC - 1) / MC);
   const int slots = num_sms() / (2 * MC);
   const int clusters = tiles < slots ? tiles : slots;
-  sr::launch_k(kern, 2 * MC * clusters, kThreads, smem, stream, p.a, p.b, M, p.N, p.K, p.c, p.ldc, p.bias, p.aux,
-               p.sample, p.norm, p.rope);
+  sr::launch_k(kern, 2 * MC * clusters, kThreads, smem, stream, p.a, p.b, M, p.m_live, p.N, p.K, p.c, p.ldc,
+               p.bias, p.aux, p.sample, p.norm, p.rope);
   return check_launch("gemm_pair_kernel");
 }
 
@@ -1151,6 +1169,7 @@ int gemm_bf16_plan(GemmPlan* p, int M, int N, int K, const __nv_bfloat16* A, int
   p->mc = mc;
   p->kc = (pair && K % kBK == 0 && g_pair_kc == 2) ? 2 : 1;
   p->sample = SampleArgs{nullptr, nullptr, 0u, 0.0f};
+  p->m_live = nullptr;
   const int mrows = M > 0 ? M : 1;
   if (p->kc > 1) {
     int rc = mc == 2 ? make_tmap_bf16(&p->a, A, (uint64_t)K, (uint64_t)mrows, (uint64_t)lda * 2, kBK, kBM)

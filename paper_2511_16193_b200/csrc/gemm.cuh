@@ -76,6 +76,7 @@ struct GemmPlan {
   SampleArgs sample;  // argmax epilogue: keyed Gumbel sampling when inv_temp > 0
   NormArgs norm;      // fused RMSNorm (consumer scaling / producer outputs)
   RopeArgs rope;      // fused RoPE + KV scatter (kEpiQkvRope)
+  const int32_t* m_live = nullptr;  // device live-row count (compacted batch); nullptr = M
 };
 
 // Build a plan (tensor maps) once; launch many times (graph-capturable).

@@ -359,6 +359,7 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
       auto& P = m->prof;
       P.begin(sr::kProfQkv, st);
       m->p_qkv[l].rope.pos = a->positions;
+      m->p_qkv[l].m_live = a->live_rows;
       SR_TRY(sr::gemm_bf16_launch(m->p_qkv[l], st, M));
       P.end(st);
       P.begin(sr::kProfAttn, st);
@@ -370,12 +371,15 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
                                 m->attn_part, m->partial_floats, (bf*)m->attn, st, 1, false));
       P.end(st);
       P.begin(sr::kProfO, st);
+      m->p_o[l].m_live = a->live_rows;
       SR_TRY(sr::gemm_bf16_launch(m->p_o[l], st, M));
       P.end(st);
       P.begin(sr::kProfGateUp, st);
+      m->p_gu[l].m_live = a->live_rows;
       SR_TRY(sr::gemm_bf16_launch(m->p_gu[l], st, M));
       P.end(st);
       P.begin(sr::kProfDown, st);
+      m->p_down[l].m_live = a->live_rows;
       SR_TRY(sr::gemm_bf16_launch(m->p_down[l], st, M));
       P.end(st);
     }
@@ -389,7 +393,9 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
       SR_TRY(sr::check_launch("gather_rows_kernel"));
     }
     if (a->output == 1) {
-      SR_TRY(sr::gemm_bf16_launch(sel ? m->p_lm_logits_sel : m->p_lm_logits, st, R));
+      sr::GemmPlan& lmp = sel ? m->p_lm_logits_sel : m->p_lm_logits;
+      lmp.m_live = sel ? nullptr : a->live_rows;
+      SR_TRY(sr::gemm_bf16_launch(lmp, st, R));
       const size_t vpad = (size_t)(d.vocab + 7) / 8 * 8;
       SR_CHECK_CUDA(cudaMemcpy2DAsync(a->out, (size_t)d.vocab * 4, m->logits, vpad * 4, (size_t)d.vocab * 4, R,
                                       cudaMemcpyDeviceToDevice, st));
@@ -397,6 +403,7 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
       m->prof.begin(sr::kProfLmHead, st);
       sr::GemmPlan& lm = sel ? m->p_lm_argmax_sel : m->p_lm_argmax;
       lm.sample = sample;
+      lm.m_live = sel ? nullptr : a->live_rows;
       SR_TRY(sr::gemm_bf16_launch(lm, st, R));
       m->prof.end(st);
       m->prof.begin(sr::kProfOther, st);

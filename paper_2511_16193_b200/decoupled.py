@@ -164,10 +164,13 @@ class DraftSide:
                 self.drafts.data_ptr(), self.nd.data_ptr(), self.m_token_ids.data_ptr(),
                 self.m_positions.data_ptr(), self.m_seqs.data_ptr(), self.m_logit_rows.data_ptr(), None, st),
                 "sr_draft_model_batch")
-            if step < self.k:
+            if step == 0:
                 m.forward(self.m_token_ids, self.m_positions, self.m_seqs, num_seqs=self.B,
                           max_q_len=self.k + 2, max_key=self.max_key, out=self.m_out,
                           logit_rows=self.m_logit_rows)
+            elif step < self.k:   # decode steps: one row per request, rows [0, B)
+                m.forward(self.m_token_ids[:self.B], self.m_positions[:self.B], self.m_seqs, num_seqs=self.B,
+                          max_q_len=1, max_key=self.max_key, out=self.m_out)
 
     def _draft(self) -> None:
         st = _native.stream_handle()
@@ -286,9 +289,9 @@ class VerifySide:
             e.B, 1, e.k, e.tokens.data_ptr(), e.stride, e.seq_len.data_ptr(), e.gen_len.data_ptr(),
             e.max_new.data_ptr(), e.max_new_cap.data_ptr(), e.drafts.data_ptr(), e.ndraft.data_ptr(), None,
             e.token_ids.data_ptr(),
-            e.positions.data_ptr(), e.seqs.data_ptr(), st), "sr_build_verify_batch")
+            e.positions.data_ptr(), e.seqs.data_ptr(), e.live_rows.data_ptr(), st), "sr_build_verify_batch")
         e.m.forward(e.token_ids, e.positions, e.seqs, num_seqs=e.B, max_q_len=e.k + 1, max_key=e.max_key,
-                    out=e.target_ids)
+                    out=e.target_ids, live_rows=e.live_rows)
         out = e.history[0]
         _native.check(lib.sr_accept_commit(
             e.m.handle, e.B, 1, e.seqs.data_ptr(), e.token_ids.data_ptr(), e.target_ids.data_ptr(), e.tokens.data_ptr(),

@@ -146,21 +146,23 @@ class ModelDrafter:
                 "sr_draft_model_batch")
             if step == e.k:
                 break
+            # step 0: catch-up rows [b*(k+2), +k+2), logits at each request's
+            # last one; steps >= 1: one decode row per request, rows [0, B)
+            rows = (self.token_ids, self.positions, self.logit_rows, e.k + 2) if step == 0 else \
+                (self.token_ids[:e.B], self.positions[:e.B], None, 1)
             if rejection:
                 # the drafter samples its window from q = softmax(logits / T)
                 # with its own keyed noise, and keeps q's rows for K3
                 q = self.q_logits[step]
-                self.m.forward(self.token_ids, self.positions, self.seqs, num_seqs=e.B,
-                               max_q_len=e.k + 2, max_key=e.max_key, out=q, logit_rows=self.logit_rows,
-                               output=1)
+                self.m.forward(rows[0], rows[1], self.seqs, num_seqs=e.B, max_q_len=rows[3],
+                               max_key=e.max_key, out=q, logit_rows=rows[2], output=1)
                 _native.check(lib.sr_sample_rows(
                     q.data_ptr(), e.B, q.shape[1], q.shape[1], self.key_req.data_ptr(), self.key_pos.data_ptr(),
                     (e.seed ^ DRAFT_SEED_SALT) & 0xFFFFFFFF, e.temperature, self.out.data_ptr(), st),
                     "sr_sample_rows")
             else:
-                self.m.forward(self.token_ids, self.positions, self.seqs, num_seqs=e.B,
-                               max_q_len=e.k + 2, max_key=e.max_key, out=self.out,
-                               logit_rows=self.logit_rows, output=e._out_mode,
+                self.m.forward(rows[0], rows[1], self.seqs, num_seqs=e.B, max_q_len=rows[3],
+                               max_key=e.max_key, out=self.out, logit_rows=rows[2], output=e._out_mode,
                                temperature=e.temperature, seed=e.seed)
 
 
@@ -205,7 +207,7 @@ class RolloutEngine:
 
     def __init__(self, target: DeviceModel, prompts: list[np.ndarray], max_new: list[int], *, k: int = 4,
                  drafters: tuple = (NgramDrafter(),), bonus_token: bool = False, history: int = 0,
-                 temperature: float = 0.0, seed: int = 0, acceptance: str = "exact"):
+                 temperature: float = 0.0, seed: int = 0, acceptance: str = "exact", compact: bool = True):
         if not prompts:
             raise ConfigError("empty batch")
         if len(prompts) != len(max_new):
@@ -274,6 +276,11 @@ class RolloutEngine:
         # planner.reconfigure / sim.py:445-510): one batch mixes windows
         # 0..k; rows beyond a request's window are simply not verified
         self.window = torch.full((self.B,), k, dtype=torch.int32, device=dev)
+        # live-row compaction: each step packs only live rows (finished
+        # requests, gap rounds and unproposed draft slots take none) and the
+        # forward's GEMMs skip the dead tiles (sr_build_verify_batch live_rows)
+        self.compact = bool(compact)
+        self.live_rows = torch.zeros(1, dtype=torch.int32, device=dev)
         if acceptance == "rejection":
             self.p_logits = torch.empty((R, target.s.vocab), dtype=torch.float32, device=dev)
             self.rs_stats = torch.zeros((R, 4), dtype=torch.float32, device=dev)
@@ -320,13 +327,14 @@ class RolloutEngine:
             self.B, self.N, self.k, self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(),
             self.gen_len.data_ptr(), self.max_new.data_ptr(), self.max_new_cap.data_ptr(), drafts_ptr, nd_ptr,
             self.window.data_ptr(),
-            self.token_ids.data_ptr(), self.positions.data_ptr(), self.seqs.data_ptr(), st),
+            self.token_ids.data_ptr(), self.positions.data_ptr(), self.seqs.data_ptr(),
+            self.live_rows.data_ptr() if self.compact else None, st),
             "sr_build_verify_batch")
         out = self.history[slot]
         if self.acceptance == "rejection":
             d = self.drafters[0]
             self.m.forward(self.token_ids, self.positions, self.seqs, num_seqs=self.B, max_q_len=self.k + 1,
-                           max_key=self.max_key, out=self.p_logits, output=1)
+                           max_key=self.max_key, out=self.p_logits, output=1, live_rows=self._live())
             V = self.p_logits.shape[1]
             _native.check(lib.sr_accept_rejection(
                 self.B, self.k, self.seqs.data_ptr(), self.token_ids.data_ptr(), self.p_logits.data_ptr(), V,
@@ -337,12 +345,16 @@ class RolloutEngine:
             return
         self.m.forward(self.token_ids, self.positions, self.seqs, num_seqs=self.B * self.N,
                        max_q_len=self.k + 1, max_key=self.max_key, out=self.target_ids,
-                       output=self._out_mode, temperature=self.temperature, seed=self.seed)
+                       output=self._out_mode, temperature=self.temperature, seed=self.seed,
+                       live_rows=self._live())
         _native.check(lib.sr_accept_commit(
             self.m.handle, self.B, self.N, self.seqs.data_ptr(), self.token_ids.data_ptr(),
             self.target_ids.data_ptr(), self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(),
             self.gen_len.data_ptr(), self.max_new.data_ptr(), self.bonus, out.data_ptr(), self.bon.data_ptr(), st),
             "sr_accept_commit")
+
+    def _live(self):
+        return self.live_rows if self.compact else None
 
     def step(self) -> None:
         slot = self.steps % self.history.shape[0]

@@ -245,7 +245,7 @@ class DeviceModel:
 
     def forward(self, token_ids, positions, seqs, *, num_seqs: int, max_q_len: int, max_key: int,
                 out, output: int = 0, logit_rows=None, out_val=None, stream=None,
-                temperature: float = 0.0, seed: int = 0) -> None:
+                temperature: float = 0.0, seed: int = 0, live_rows=None) -> None:
         """Enqueue one forward (``output`` 0 = argmax ids, 1 = fp32 logits,
         2 = keyed Gumbel-max sample at ``temperature``)."""
         a = _native.ForwardArgs()
@@ -258,6 +258,7 @@ class DeviceModel:
         a.out = out.data_ptr()
         a.out_val = out_val.data_ptr() if out_val is not None else None
         a.temperature, a.seed = float(temperature), int(seed) & 0xFFFFFFFF
+        a.live_rows = live_rows.data_ptr() if live_rows is not None else None
         _native.check(self.lib.sr_model_forward(self.handle, ctypes.byref(a),
                                                 _native.stream_handle(stream)), "sr_model_forward")
 

@@ -713,3 +713,34 @@ def test_edge_cases_spec_equals_plain(k):
     spec.prefill()
     spec.run()
     assert spec.outputs() == ref
+
+
+@pytest.mark.parametrize("N", [1, 3])
+def test_compacted_batch_equals_fixed_layout(N):
+    """Live-row compaction (sr_build_verify_batch live_rows): finished
+    requests and unproposed draft slots take no rows and the GEMMs skip the
+    dead tiles; outputs, outcome rows and the per-step live-row count equal
+    the fixed-layout batch's."""
+    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine
+
+    B, k = 6, 4
+    s, w, m = make("tiny", "bf16", B=B, branches=B * (N - 1), max_len=256)
+    prompts = prompts_for(s.vocab, B, 31, alphabet=8)
+    max_new = [3, 40, 17, 29, 1, 35]          # requests finish at different steps
+    drafters = tuple(NgramDrafter(1 + i, 3 + i) for i in range(N))
+    res = []
+    for compact in (False, True):
+        eng = RolloutEngine(m, prompts, max_new, k=k, drafters=drafters, history=256, compact=compact)
+        eng.prefill()
+        live, steps = [], 0
+        while not eng.done():
+            eng.step()
+            steps += 1
+            sq = eng.seqs.cpu().numpy()
+            live.append((int(eng.live_rows.item()), int(sq[:, 1].sum())))
+        res.append((eng.outputs(), eng.outcome_rows(steps), live))
+    assert res[0][0] == res[1][0]
+    assert np.array_equal(res[0][1], res[1][1])
+    for got, total in res[1][2]:
+        assert got == total                    # packed rows == sum of window lengths
+    assert res[1][2][-1][0] < B * N * (k + 1)  # the tail ran on fewer rows
