@@ -290,11 +290,13 @@ int sr_accept_rejection(int num_requests, int k, const void* seqs, const int32_t
                         int32_t* seq_len, int32_t* gen_len, const int32_t* max_new, int bonus_token,
                         float* stats, int32_t* outcome, int32_t* bon, sr_stream_t stream);
 
-/* Host-facing step result (RolloutEngine.capture_io): out [B, 4 + width] =
- * outcome row b (first 4 ints) then tokens[b, seq_before[b] + j] for
- * j < width (clamped to the row) -- the committed window of the step. */
-int sr_pack_results(int num_requests, int width, const int32_t* outcome, const int32_t* tokens,
-                    int64_t tok_stride, const int32_t* seq_before, int32_t* out, sr_stream_t stream);
+/* Host-facing step result (RolloutEngine.capture_io): out [B, 4N + width] =
+ * the N drafters' outcome rows of request b (4N ints) then
+ * tokens[b, seq_before[b] + j] for j < width (clamped to the row) -- the
+ * committed window of the step. */
+int sr_pack_results(int num_requests, int num_drafters, int width, const int32_t* outcome,
+                    const int32_t* tokens, int64_t tok_stride, const int32_t* seq_before, int32_t* out,
+                    sr_stream_t stream);
 
 /* Reference-acceptance drafter: for output position
  * g = gen_len[b] + j propose truth[b, g] (the target's own greedy token) when
@@ -334,6 +336,9 @@ int sr_draft_model_batch(int num_requests, int k, int step, const int32_t* token
  * the token row and KV pages of request b hold max_new_cap[b] outputs, and a
  * retired request (cap = gen_len) stays retired whatever budget the host
  * copies in.
+ * active [N, B] (optional): drafter n proposes for request b only where
+ * active[n*B + b] != 0 (Best-of-N drafters assigned to tail requests on
+ * drain, bon.py:79-139); NULL = every drafter for every request.
  * live_rows (optional, device int): COMPACT the batch instead -- sequence
  * s = b*N+n keeps its SeqInfo slot but its rows are packed back to back
  * (q_start = exclusive prefix sum of q_len over s), so finished requests and
@@ -343,8 +348,8 @@ int sr_build_verify_batch(int num_requests, int num_drafters, int k, const int32
                           int64_t tok_stride, const int32_t* seq_len, const int32_t* gen_len,
                           int32_t* max_new, const int32_t* max_new_cap, const int32_t* drafts,
                           const int32_t* ndraft,
-                          const int32_t* window, int32_t* token_ids, int32_t* positions, void* seqs,
-                          int32_t* live_rows, sr_stream_t stream);
+                          const int32_t* window, const int32_t* active, int32_t* token_ids,
+                          int32_t* positions, void* seqs, int32_t* live_rows, sr_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -134,8 +134,8 @@ __global__ void build_verify_kernel(int B, int N, int k, const int32_t* __restri
                                     int32_t* __restrict__ max_new, const int32_t* __restrict__ max_new_cap,
                                     const int32_t* __restrict__ drafts,
                                     const int32_t* __restrict__ ndraft, const int32_t* __restrict__ window,
-                                    int32_t* __restrict__ token_ids, int32_t* __restrict__ positions,
-                                    SeqInfo* __restrict__ seqs) {
+                                    const int32_t* __restrict__ active_mask, int32_t* __restrict__ token_ids,
+                                    int32_t* __restrict__ positions, SeqInfo* __restrict__ seqs) {
   grid_dep_sync();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= B * N) return;
@@ -155,6 +155,7 @@ __global__ void build_verify_kernel(int B, int N, int k, const int32_t* __restri
   if (active) {
     nd = drafts != nullptr ? ndraft[n * B + b] : 0;
     active = nd >= 0;  // ndraft < 0: no window this round (decoupled gap round)
+    if (active_mask != nullptr && active_mask[n * B + b] == 0) active = false;  // drafter off for b
     nd = max(0, min(nd, min(k, remaining)));
     if (window != nullptr) nd = min(nd, max(0, window[b]));  // per-request window (reconfiguration)
   }
@@ -191,9 +192,9 @@ build_verify_compact_kernel(int B, int N, int k, const int32_t* __restrict__ tok
                             const int32_t* __restrict__ seq_len, const int32_t* __restrict__ gen_len,
                             int32_t* __restrict__ max_new, const int32_t* __restrict__ max_new_cap,
                             const int32_t* __restrict__ drafts, const int32_t* __restrict__ ndraft,
-                            const int32_t* __restrict__ window, int32_t* __restrict__ token_ids,
-                            int32_t* __restrict__ positions, SeqInfo* __restrict__ seqs,
-                            int32_t* __restrict__ live_rows) {
+                            const int32_t* __restrict__ window, const int32_t* __restrict__ active_mask,
+                            int32_t* __restrict__ token_ids, int32_t* __restrict__ positions,
+                            SeqInfo* __restrict__ seqs, int32_t* __restrict__ live_rows) {
   grid_dep_sync();
   __shared__ int warp_sum[kCompactThreads / 32];
   __shared__ int carry;
@@ -217,6 +218,7 @@ build_verify_compact_kernel(int B, int N, int k, const int32_t* __restrict__ tok
       if (active) {
         nd = drafts != nullptr ? ndraft[n * B + b] : 0;
         active = nd >= 0;  // ndraft < 0: no window this round (decoupled gap round)
+        if (active_mask != nullptr && active_mask[n * B + b] == 0) active = false;  // drafter off for b
         nd = max(0, min(nd, min(k, remaining)));
         if (window != nullptr) nd = min(nd, max(0, window[b]));
       }
@@ -353,19 +355,19 @@ __global__ void draft_batch_kernel(int B, int k, int step, const int32_t* __rest
 
 // Host-facing step result: per request its outcome row then the token
 // slots [seq_before, seq_before + w) (clamped to the row), one thread per cell.
-__global__ void pack_results_kernel(int B, int w, const int32_t* __restrict__ outcome,
+__global__ void pack_results_kernel(int B, int N, int w, const int32_t* __restrict__ outcome,
                                     const int32_t* __restrict__ tokens, int64_t tok_stride,
                                     const int32_t* __restrict__ seq_before, int32_t* __restrict__ out) {
   grid_dep_sync();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  const int cols = 4 + w;
+  const int cols = 4 * N + w;
   if (e >= B * cols) return;
   const int b = e / cols, c = e % cols;
   int v;
-  if (c < 4) {
-    v = outcome[(int64_t)b * 4 + c];
+  if (c < 4 * N) {
+    v = outcome[(int64_t)b * 4 * N + c];   // drafter c / 4's outcome row
   } else {
-    const int64_t pos = min((int64_t)seq_before[b] + (c - 4), tok_stride - 1);
+    const int64_t pos = min((int64_t)seq_before[b] + (c - 4 * N), tok_stride - 1);
     v = tokens[(int64_t)b * tok_stride + pos];
   }
   out[e] = v;
@@ -373,14 +375,15 @@ __global__ void pack_results_kernel(int B, int w, const int32_t* __restrict__ ou
 
 }  // namespace sr
 
-extern "C" int sr_pack_results(int num_requests, int width, const int32_t* outcome, const int32_t* tokens,
-                               int64_t tok_stride, const int32_t* seq_before, int32_t* out, sr_stream_t stream) {
-  SR_REQUIRE(num_requests >= 0 && width >= 0 && tok_stride > 0, "bad result shape");
+extern "C" int sr_pack_results(int num_requests, int num_drafters, int width, const int32_t* outcome,
+                               const int32_t* tokens, int64_t tok_stride, const int32_t* seq_before, int32_t* out,
+                               sr_stream_t stream) {
+  SR_REQUIRE(num_requests >= 0 && num_drafters >= 1 && width >= 0 && tok_stride > 0, "bad result shape");
   if (num_requests == 0) return SR_OK;
   SR_REQUIRE(outcome && tokens && seq_before && out, "null pointer");
-  const int n = num_requests * (4 + width);
-  sr::launch_k(sr::pack_results_kernel, sr::ceil_div(n, 256), 256, 0, (cudaStream_t)stream, num_requests, width,
-               outcome, tokens, tok_stride, seq_before, out);
+  const int n = num_requests * (4 * num_drafters + width);
+  sr::launch_k(sr::pack_results_kernel, sr::ceil_div(n, 256), 256, 0, (cudaStream_t)stream, num_requests,
+               num_drafters, width, outcome, tokens, tok_stride, seq_before, out);
   return sr::check_launch("pack_results_kernel");
 }
 
@@ -447,8 +450,8 @@ extern "C" int sr_build_verify_batch(int num_requests, int num_drafters, int k, 
                                      int64_t tok_stride, const int32_t* seq_len, const int32_t* gen_len,
                                      int32_t* max_new, const int32_t* max_new_cap, const int32_t* drafts,
                                      const int32_t* ndraft,
-                                     const int32_t* window, int32_t* token_ids, int32_t* positions,
-                                     void* seqs, int32_t* live_rows, sr_stream_t stream) {
+                                     const int32_t* window, const int32_t* active, int32_t* token_ids,
+                                     int32_t* positions, void* seqs, int32_t* live_rows, sr_stream_t stream) {
   SR_REQUIRE(num_requests >= 0 && num_drafters >= 1 && k >= 0, "bad batch shape");
   if (num_requests == 0) return SR_OK;
   SR_REQUIRE(tokens && seq_len && gen_len && max_new && token_ids && positions && seqs, "null pointer");
@@ -457,12 +460,11 @@ extern "C" int sr_build_verify_batch(int num_requests, int num_drafters, int k, 
   if (live_rows != nullptr) {
     sr::launch_k(sr::build_verify_compact_kernel, 1, sr::kCompactThreads, 0, (cudaStream_t)stream, num_requests,
                  num_drafters, k, tokens, tok_stride, seq_len, gen_len, max_new, max_new_cap, drafts, ndraft, window,
-                 token_ids, positions, reinterpret_cast<sr::SeqInfo*>(seqs), live_rows);
+                 active, token_ids, positions, reinterpret_cast<sr::SeqInfo*>(seqs), live_rows);
     return sr::check_launch("build_verify_compact_kernel");
   }
   sr::launch_k(sr::build_verify_kernel, sr::ceil_div(S, 128), 128, 0, (cudaStream_t)stream, 
       num_requests, num_drafters, k, tokens, tok_stride, seq_len, gen_len, max_new, max_new_cap, drafts, ndraft,
-      window,
-      token_ids, positions, reinterpret_cast<sr::SeqInfo*>(seqs));
+      window, active, token_ids, positions, reinterpret_cast<sr::SeqInfo*>(seqs));
   return sr::check_launch("build_verify_kernel");
 }

@@ -287,7 +287,7 @@ class VerifySide:
         self.seq_before.copy_(e.seq_len)
         _native.check(lib.sr_build_verify_batch(
             e.B, 1, e.k, e.tokens.data_ptr(), e.stride, e.seq_len.data_ptr(), e.gen_len.data_ptr(),
-            e.max_new.data_ptr(), e.max_new_cap.data_ptr(), e.drafts.data_ptr(), e.ndraft.data_ptr(), None,
+            e.max_new.data_ptr(), e.max_new_cap.data_ptr(), e.drafts.data_ptr(), e.ndraft.data_ptr(), None, None,
             e.token_ids.data_ptr(),
             e.positions.data_ptr(), e.seqs.data_ptr(), e.live_rows.data_ptr(), st), "sr_build_verify_batch")
         e.m.forward(e.token_ids, e.positions, e.seqs, num_seqs=e.B, max_q_len=e.k + 1, max_key=e.max_key,

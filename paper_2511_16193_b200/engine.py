@@ -280,6 +280,10 @@ class RolloutEngine:
         # requests, gap rounds and unproposed draft slots take none) and the
         # forward's GEMMs skip the dead tiles (sr_build_verify_batch live_rows)
         self.compact = bool(compact)
+        # Best-of-N drafter assignment: drafter n proposes for request b only
+        # where active[n, b] != 0 (all on by default; policy.RolloutDriver
+        # turns extra drafters on for tail requests when the batch drains)
+        self.active = torch.ones((self.N, self.B), dtype=torch.int32, device=dev)
         self.live_rows = torch.zeros(1, dtype=torch.int32, device=dev)
         if acceptance == "rejection":
             self.p_logits = torch.empty((R, target.s.vocab), dtype=torch.float32, device=dev)
@@ -326,7 +330,7 @@ class RolloutEngine:
         _native.check(lib.sr_build_verify_batch(
             self.B, self.N, self.k, self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(),
             self.gen_len.data_ptr(), self.max_new.data_ptr(), self.max_new_cap.data_ptr(), drafts_ptr, nd_ptr,
-            self.window.data_ptr(),
+            self.window.data_ptr(), self.active.data_ptr() if self.N > 1 else None,
             self.token_ids.data_ptr(), self.positions.data_ptr(), self.seqs.data_ptr(),
             self.live_rows.data_ptr() if self.compact else None, st),
             "sr_build_verify_batch")
@@ -385,8 +389,8 @@ class RolloutEngine:
     def capture_io(self, budget_host: torch.Tensor, result_host: torch.Tensor):
         """Host-facing step as one CUDA graph: H2D of the per-request budgets
         (``budget_host``, pinned int32 [B]), the speculation step, and D2H of
-        each request's outcome row and its next k+2 token slots
-        (``result_host``, pinned int32 [B, 4 + k + 2]).  Budgets are clamped
+        each request's N drafter outcome rows and its next k+2 token slots
+        (``result_host``, pinned int32 [B, 4 * N + k + 2]).  Budgets are clamped
         on device to the constructor's ``max_new`` (:attr:`max_new_cap`): a
         larger host budget cannot grow a request past its slot.  :meth:`step_io`
         replays the latest one (or pass the returned graph); the caller waits
@@ -396,10 +400,11 @@ class RolloutEngine:
         if self.history.shape[0] != 1:
             raise ConfigError("graph capture needs history=0/1 (the graph writes slot 0)")
         w = self.k + 2
-        if tuple(result_host.shape) != (self.B, 4 + w) or budget_host.numel() != self.B:
-            raise ConfigError("result_host must be [B, 4 + k + 2] and budget_host [B]")
+        cols = 4 * self.N + w
+        if tuple(result_host.shape) != (self.B, cols) or budget_host.numel() != self.B:
+            raise ConfigError("result_host must be [B, 4 * N + k + 2] and budget_host [B]")
         seq_before = torch.empty_like(self.seq_len)
-        res = torch.empty((self.B, 4 + w), dtype=torch.int32, device=self.dev)
+        res = torch.empty((self.B, cols), dtype=torch.int32, device=self.dev)
         if not hasattr(self, "_io_keep"):
             self._io_keep = []
         self._io_keep.append((seq_before, res))   # buffers the graph reads/writes stay alive
@@ -413,7 +418,7 @@ class RolloutEngine:
             seq_before.copy_(self.seq_len)
             self._enqueue_step(0)
             _native.check(self.lib.sr_pack_results(
-                self.B, w, self.history[0].data_ptr(), self.tokens.data_ptr(), self.stride,
+                self.B, self.N, w, self.history[0].data_ptr(), self.tokens.data_ptr(), self.stride,
                 seq_before.data_ptr(), res.data_ptr(), _native.stream_handle()), "sr_pack_results")
             result_host.copy_(res, non_blocking=True)
             g.capture_end()
@@ -424,6 +429,17 @@ class RolloutEngine:
     def step_io(self, graph=None) -> None:
         (graph or self.graph_io).replay()
         self.steps += 1
+
+    def set_active(self, mask) -> None:
+        """Best-of-N drafter assignment: ``mask`` [N, B] (nonzero = drafter n
+        proposes for request b).  Drafter 0 (the incumbent) stays on.  In
+        place, so captured step graphs pick it up."""
+        a = torch.as_tensor(mask, dtype=torch.int32)
+        if a.shape != (self.N, self.B):
+            raise ConfigError(f"active mask must be [{self.N}, {self.B}]")
+        a = a.clone()
+        a[0] = 1
+        self.active.copy_(a.to(self.dev))
 
     def retire(self, b: int) -> None:
         """Stop request ``b`` where it is (its slot was migrated away): budget
