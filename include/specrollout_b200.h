@@ -351,6 +351,36 @@ int sr_build_verify_batch(int num_requests, int num_drafters, int k, const int32
                           const int32_t* window, const int32_t* active, int32_t* token_ids,
                           int32_t* positions, void* seqs, int32_t* live_rows, sr_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * a6  Decoupled speculation round bookkeeping (pipeline depth 2; replaces the
+ * decoupled branch of `_Executor.begin_round` sim.py:860-917 and
+ * `_end_decoupled` sim.py:1051-1092 for the per-request state), one thread
+ * per request.  Drafter side: prep (successor's first output position g0
+ * and context length ctx behind the in-flight window), post (cap the drafted
+ * window at the remaining budget, append it to the token mirror, stage it
+ * for the verifier), apply (fold the verifier's decision: accepted prefix +
+ * corrected token, advance, roll a model drafter's KV length back, the new
+ * in-flight count).  Verifier side: post (after K3: the decision rows and the
+ * k+1 committed-token slots to send back), receive (admit the drafter's new
+ * windows as pending, or drop them and charge their size as depth-2 waste
+ * when the predecessor was rejected).  dkv_len may be NULL.
+ * ------------------------------------------------------------------------- */
+int sr_decoupled_draft_prep(int B, const int32_t* seq_len, const int32_t* gen_len, const int32_t* inflight,
+                            int32_t* g0, int32_t* ctx, sr_stream_t stream);
+int sr_decoupled_draft_post(int B, int k, int64_t stride, const int32_t* max_new, const int32_t* g0,
+                            const int32_t* ctx, const int32_t* drafts, int32_t* nd, int32_t* tokens,
+                            int32_t* out_drafts, int32_t* out_nd, sr_stream_t stream);
+int sr_decoupled_draft_apply(int B, int k, int64_t stride, const int32_t* in_verified, const int32_t* in_accepted,
+                             const int32_t* in_committed, const int32_t* in_ctoks, const int32_t* out_nd,
+                             int32_t* inflight, int32_t* tokens, int32_t* seq_len, int32_t* gen_len,
+                             int32_t* dkv_len, sr_stream_t stream);
+int sr_decoupled_verify_post(int B, int k, int64_t stride, const int32_t* outcome, const int32_t* bon,
+                             const int32_t* tokens, const int32_t* seq_before, int32_t* rows, int32_t* out_verified,
+                             int32_t* out_accepted, int32_t* out_committed, int32_t* out_ctoks, sr_stream_t stream);
+int sr_decoupled_verify_receive(int B, int k, const int32_t* out_verified, const int32_t* out_accepted,
+                                const int32_t* out_committed, const int32_t* in_drafts, const int32_t* in_nd,
+                                int32_t* rows, int32_t* pending, int32_t* pending_nd, sr_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

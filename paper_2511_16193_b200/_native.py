@@ -47,6 +47,11 @@ SIGNATURES: dict[str, list] = {
                              _vp, _vp, _vp, _vp],
     "sr_accept_rejection": [_i32, _i32, _vp, _vp, _vp, _i64, _vp, _i64, _i32, ctypes.c_float, ctypes.c_uint32,
                             _vp, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp],
+    "sr_decoupled_draft_prep": [_i32, _vp, _vp, _vp, _vp, _vp, _vp],
+    "sr_decoupled_draft_post": [_i32, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "sr_decoupled_draft_apply": [_i32, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "sr_decoupled_verify_post": [_i32, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "sr_decoupled_verify_receive": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "sr_pack_results": [_i32, _i32, _i32, _vp, _vp, _i64, _vp, _vp, _vp],
     "sr_build_verify_batch": [_i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               _vp, _vp, _vp, _vp, _vp],

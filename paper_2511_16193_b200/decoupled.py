@@ -99,9 +99,11 @@ class DraftSide:
     are static-buffer device work, replayed from CUDA graphs after the first
     round (``graphs=True``)."""
 
-    def __init__(self, prompts, max_new, k: int, drafter, device="cuda", graphs: bool = True):
+    def __init__(self, prompts, max_new, k: int, drafter, device="cuda", graphs: bool = True, vocab: int = 0):
         if isinstance(drafter, (SyntheticDrafter, NgramDrafter, ModelDrafter)):
             self.drafter = drafter
+            # wrong-token id space of the synthetic drafter
+            self.vocab = (drafter.vocab or vocab) if isinstance(drafter, SyntheticDrafter) else vocab
         else:
             raise ConfigError("decoupled mode supports the n-gram, small-model and reference-acceptance drafters")
         self.lib = _native.lib()
@@ -124,7 +126,6 @@ class DraftSide:
         self.g0 = torch.zeros(B, dtype=torch.int32, device=d)
         self.ctx = torch.zeros(B, dtype=torch.int32, device=d)
         self.scratch = torch.zeros(2 * B, dtype=torch.int64, device=d)
-        self.ar = torch.arange(k, device=d)
         # round I/O (static: graph-replayable, NCCL-sendable)
         self.out_drafts = torch.full((B, k), -1, dtype=torch.int32, device=d)
         self.out_nd = torch.zeros(B, dtype=torch.int32, device=d)
@@ -173,51 +174,36 @@ class DraftSide:
                           max_q_len=1, max_key=self.max_key, out=self.m_out)
 
     def _draft(self) -> None:
-        st = _native.stream_handle()
-        self.g0.copy_(self.gen_len + self.inflight)             # first drafted output position
-        self.ctx.copy_(self.seq_len + self.inflight)            # context incl. in-flight drafts
-        room = (self.max_new - self.g0).clamp(min=0)
+        st, lib = _native.stream_handle(), self.lib
+        _native.check(lib.sr_decoupled_draft_prep(self.B, self.seq_len.data_ptr(), self.gen_len.data_ptr(),
+                                                  self.inflight.data_ptr(), self.g0.data_ptr(), self.ctx.data_ptr(),
+                                                  st), "sr_decoupled_draft_prep")
         if isinstance(self.drafter, SyntheticDrafter):
             d = self.drafter
-            _native.check(self.lib.sr_synthetic_draft(
+            _native.check(lib.sr_synthetic_draft(
                 self.B, self.k, d.truth.data_ptr(), d.stride, self.max_new.data_ptr(), d.uniforms.data_ptr(),
-                d.stride, d.p.data_ptr(), self.g0.data_ptr(), self._vocab, self.drafts.data_ptr(),
+                d.stride, d.p.data_ptr(), self.g0.data_ptr(), self.vocab, self.drafts.data_ptr(),
                 self.nd.data_ptr(), st), "sr_synthetic_draft")
         elif isinstance(self.drafter, ModelDrafter):
             self._draft_model(st)
         else:
             d = self.drafter
-            _native.check(self.lib.sr_ngram_propose(
+            _native.check(lib.sr_ngram_propose(
                 self.B, self.tokens.data_ptr(), self.stride, self.ctx.data_ptr(), d.min_n, d.max_n, self.k,
                 self.drafts.data_ptr(), self.nd.data_ptr(), self.scratch.data_ptr(), st), "sr_ngram_propose")
-        self.nd.copy_(torch.minimum(self.nd, room.to(torch.int32)))
-        # append the new window after the in-flight one (context of the next successor)
-        cols = (self.ctx[:, None] + self.ar[None, :]).clamp(max=self.stride - 1).long()
-        keep = self.ar[None, :] < self.nd[:, None]
-        self.tokens.scatter_(1, cols, torch.where(keep, self.drafts, self.tokens.gather(1, cols)))
-        self.out_drafts.copy_(self.drafts)
-        self.out_nd.copy_(self.nd)
+        # cap at the budget, append behind the in-flight window, stage for the verifier
+        _native.check(lib.sr_decoupled_draft_post(
+            self.B, self.k, self.stride, self.max_new.data_ptr(), self.g0.data_ptr(), self.ctx.data_ptr(),
+            self.drafts.data_ptr(), self.nd.data_ptr(), self.tokens.data_ptr(), self.out_drafts.data_ptr(),
+            self.out_nd.data_ptr(), st), "sr_decoupled_draft_post")
 
     def _apply(self) -> None:
-        verified = self.in_verified > 0
-        accepted, committed, ctoks = self.in_accepted, self.in_committed, self.in_ctoks
-        # an empty window (nothing proposed) that committed the target's token
-        # leaves its successor misaligned by one: treat it as rejected
-        full = verified & (accepted == self.inflight) & ((self.inflight > 0) | (committed == 0))
-        part = verified & ~full
-        # partial: accepted prefix + corrected token
-        pos = (self.seq_len + accepted).clamp(max=self.stride - 1).long()
-        corr = ctoks.gather(1, accepted.clamp(max=self.k).long()[:, None])[:, 0]
-        self.tokens.scatter_(1, pos[:, None], torch.where(part, corr, self.tokens.gather(1, pos[:, None])[:, 0])[:, None])
-        adv = torch.where(verified, committed, torch.zeros_like(committed))
-        self.seq_len += adv
-        self.gen_len += adv
-        if isinstance(self.drafter, ModelDrafter):
-            # the drafter's KV from the corrected token on was computed on
-            # rejected tokens: recompute from there next window
-            self.dkv_len.copy_(torch.where(part, torch.minimum(self.dkv_len, self.seq_len - 1), self.dkv_len))
-        # in flight next round: the window just drafted, unless its predecessor was rejected
-        self.inflight.copy_(torch.where(~part, self.out_nd, torch.zeros_like(self.out_nd)))
+        dkv = self.dkv_len.data_ptr() if isinstance(self.drafter, ModelDrafter) else None
+        _native.check(self.lib.sr_decoupled_draft_apply(
+            self.B, self.k, self.stride, self.in_verified.data_ptr(), self.in_accepted.data_ptr(),
+            self.in_committed.data_ptr(), self.in_ctoks.data_ptr(), self.out_nd.data_ptr(), self.inflight.data_ptr(),
+            self.tokens.data_ptr(), self.seq_len.data_ptr(), self.gen_len.data_ptr(), dkv, _native.stream_handle()),
+            "sr_decoupled_draft_apply")
 
     def draft(self) -> tuple[torch.Tensor, torch.Tensor]:
         """Next window of every request: successor of the in-flight one, or
@@ -242,7 +228,6 @@ class DraftSide:
         else:
             self._g_apply.replay()
 
-    _vocab = 0
 
 
 class VerifySide:
@@ -262,10 +247,12 @@ class VerifySide:
         self.k, self.B = k, len(prompts)
         d = self.eng.dev
         B = self.B
-        self.pending = torch.full((B, k), -1, dtype=torch.int32, device=d)
-        self.pending_nd = torch.full((B,), -1, dtype=torch.int32, device=d)  # -1: no window
+        # pending windows = the engine's drafter-0 draft slots (no copies)
+        self.pending = self.eng.drafts[0]
+        self.pending_nd = self.eng.ndraft[0]
+        self.pending.fill_(-1)
+        self.pending_nd.fill_(-1)                                   # -1: no window
         self.seq_before = torch.zeros(B, dtype=torch.int32, device=d)
-        self.slots = torch.arange(k + 1, device=d)
         self.out_verified = torch.zeros(B, dtype=torch.int32, device=d)
         self.out_accepted = torch.zeros(B, dtype=torch.int32, device=d)
         self.out_committed = torch.zeros(B, dtype=torch.int32, device=d)
@@ -282,14 +269,13 @@ class VerifySide:
     def _verify(self) -> None:
         e = self.eng
         lib, st = e.lib, _native.stream_handle()
-        e.drafts[0].copy_(self.pending)
-        e.ndraft[0].copy_(self.pending_nd)
         self.seq_before.copy_(e.seq_len)
+        # the pending windows live in the engine's drafter-0 slots (receive writes them there)
         _native.check(lib.sr_build_verify_batch(
             e.B, 1, e.k, e.tokens.data_ptr(), e.stride, e.seq_len.data_ptr(), e.gen_len.data_ptr(),
             e.max_new.data_ptr(), e.max_new_cap.data_ptr(), e.drafts.data_ptr(), e.ndraft.data_ptr(), None, None,
-            e.token_ids.data_ptr(),
-            e.positions.data_ptr(), e.seqs.data_ptr(), e.live_rows.data_ptr(), st), "sr_build_verify_batch")
+            e.token_ids.data_ptr(), e.positions.data_ptr(), e.seqs.data_ptr(), e.live_rows.data_ptr(), st),
+            "sr_build_verify_batch")
         e.m.forward(e.token_ids, e.positions, e.seqs, num_seqs=e.B, max_q_len=e.k + 1, max_key=e.max_key,
                     out=e.target_ids, live_rows=e.live_rows)
         out = e.history[0]
@@ -297,24 +283,17 @@ class VerifySide:
             e.m.handle, e.B, 1, e.seqs.data_ptr(), e.token_ids.data_ptr(), e.target_ids.data_ptr(), e.tokens.data_ptr(),
             e.stride, e.seq_len.data_ptr(), e.gen_len.data_ptr(), e.max_new.data_ptr(), 0, out.data_ptr(),
             e.bon.data_ptr(), st), "sr_accept_commit")
-        self.rows.copy_(out[: self.B])
-        self.out_verified.copy_((e.bon >= 0).to(torch.int32))
-        self.out_accepted.copy_(self.rows[:, 1])
-        self.out_committed.copy_(self.rows[:, 2])
-        cols = (self.seq_before[:, None] + self.slots[None, :]).clamp(max=e.stride - 1)
-        self.out_ctoks.copy_(e.tokens.gather(1, cols.long()))
+        _native.check(lib.sr_decoupled_verify_post(
+            e.B, e.k, e.stride, out.data_ptr(), e.bon.data_ptr(), e.tokens.data_ptr(), self.seq_before.data_ptr(),
+            self.rows.data_ptr(), self.out_verified.data_ptr(), self.out_accepted.data_ptr(),
+            self.out_committed.data_ptr(), self.out_ctoks.data_ptr(), st), "sr_decoupled_verify_post")
 
     def _receive(self) -> None:
-        verified = self.out_verified > 0
-        nd = self.in_nd
-        full = verified & (self.out_accepted == self.rows[:, 0]) & ((self.rows[:, 0] > 0) | (self.out_committed == 0))
-        part = verified & ~full
-        # nd == 0 (the drafter proposed nothing) is still a window: verifying
-        # it commits the target's next token, as a plain decode step would
-        ok = (~verified | full) & (nd >= 0)
-        self.pending.copy_(self.in_drafts)
-        self.pending_nd.copy_(torch.where(ok, nd, torch.full_like(nd, -1)))
-        self.rows[:, 3] += torch.where(part, nd, torch.zeros_like(nd))
+        e = self.eng
+        _native.check(e.lib.sr_decoupled_verify_receive(
+            self.B, self.k, self.out_verified.data_ptr(), self.out_accepted.data_ptr(), self.out_committed.data_ptr(),
+            self.in_drafts.data_ptr(), self.in_nd.data_ptr(), self.rows.data_ptr(), self.pending.data_ptr(),
+            self.pending_nd.data_ptr(), _native.stream_handle()), "sr_decoupled_verify_receive")
 
     def verify(self) -> None:
         """Verify the pending windows into the ``out_*`` buffers and ``rows``."""
@@ -346,9 +325,7 @@ class VerifySide:
 def run_local(model: DeviceModel, prompts, max_new, k: int, drafter, max_rounds: int = 100000,
               graphs: bool = True):
     """Both roles on one GPU (tests): returns (outputs, outcome rows per round)."""
-    if isinstance(drafter, SyntheticDrafter):
-        DraftSide._vocab = drafter.vocab or model.s.vocab
-    D = DraftSide(prompts, max_new, k, drafter, device=model.dev, graphs=graphs)
+    D = DraftSide(prompts, max_new, k, drafter, device=model.dev, graphs=graphs, vocab=model.s.vocab)
     V = VerifySide(model, prompts, max_new, k, graphs=graphs)
     V.prefill()
     history = []
@@ -408,8 +385,6 @@ def run_ranks(dist, rank: int, world: int, drafters: int, shards: dict, k: int, 
         for v in mine:
             prompts, max_new = shards[v]
             drafter = make_drafter(v)
-            if isinstance(drafter, SyntheticDrafter):
-                DraftSide._vocab = drafter.vocab
             sides[v] = DraftSide(prompts, max_new, k, drafter, device=dev, graphs=graphs)
             done[v] = torch.zeros(1, dtype=torch.int32, device=dev)
         live = set(mine)
