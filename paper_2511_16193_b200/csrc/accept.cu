@@ -77,6 +77,7 @@ accept_commit_kernel(int B, int N, const SeqInfo* __restrict__ seqs, const int32
       committed = min(committed, remaining);
     }
     const int base = seq_len[b];
+    SR_DCHECK(base + committed <= tok_stride);
     for (int i = lane; i < committed; i += 32) tokens[(int64_t)b * tok_stride + base + i] = target[win_q + i];
     if (lane < N) {
       int4 o;
@@ -117,7 +118,9 @@ accept_commit_kernel(int B, int N, const SeqInfo* __restrict__ seqs, const int32
     const int sel = r & 1;
     const int layer = r >> 1;
     const int pos = s_ctx + j;
+    SR_DCHECK(pos / kv.page < kv.max_pages && j < kv.window_max && s_branch < kv.branches);
     const int page = btab[pos / kv.page];
+    SR_DCHECK(page >= 0 && page < kv.num_pages);
     const int slot = pos % kv.page;
     const T* src = reinterpret_cast<const T*>(kv.window) + layer * kv.window_layer_elems() +
                    ((((int64_t)s_branch * 2 + sel) * nkv + h) * kv.window_max + j) * hd + kv_phys<T>(j, c * kVec);
@@ -159,6 +162,7 @@ __global__ void build_verify_kernel(int B, int N, int k, const int32_t* __restri
     nd = max(0, min(nd, min(k, remaining)));
     if (window != nullptr) nd = min(nd, max(0, window[b]));  // per-request window (reconfiguration)
   }
+  SR_DCHECK(!active || (L >= 1 && L + nd <= tok_stride));
   SeqInfo sq;
   sq.q_start = s * (k + 1);
   sq.q_len = active ? nd + 1 : 0;
@@ -253,6 +257,7 @@ build_verify_compact_kernel(int B, int N, int k, const int32_t* __restrict__ tok
       sq.branch = n == 0 ? -1 : b * (N - 1) + (n - 1);
       sq.pad0 = sq.pad1 = sq.pad2 = 0;
       seqs[s] = sq;
+      SR_DCHECK(L >= 1 && L - 1 + q_len <= tok_stride);
       for (int j = 0; j < q_len; ++j) {
         token_ids[start + j] =
             j == 0 ? tokens[(int64_t)b * tok_stride + L - 1] : drafts[((int64_t)n * B + b) * k + j - 1];

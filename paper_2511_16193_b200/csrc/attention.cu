@@ -173,6 +173,7 @@ attn_bf16_kernel(AttnArgs A) {
                              (int64_t)A.layer * A.kv.window_layer_elems();
   const int32_t* btab = A.kv.block_table + (int64_t)sq.request * A.kv.max_pages;
   const int psz = A.kv.page;
+  SR_DCHECK(max_key / psz < A.kv.max_pages || sq.branch >= 0);
 
   for (int e = tid; e < kRows * CH; e += kAttnThreads) {
     const int r = e / CH, c = e % CH;
@@ -565,6 +566,7 @@ __global__ void attn_f32_kernel(const float* __restrict__ q, const SeqInfo* __re
     int64_t vstep;
     if (sq.branch < 0 || kp < sq.ctx_len) {
       const int page = btab[kp / psz];
+      SR_DCHECK(kp / psz < kv.max_pages && page >= 0 && page < kv.num_pages);
       k = cache + (((int64_t)page * 2 * nkv + h) * psz + kp % psz) * hd;
       vstep = (int64_t)nkv * psz * hd;
     } else {

@@ -11,6 +11,18 @@
 
 #include "../../include/specrollout_b200.h"
 
+// Debug build (SR_EXTRA_NVCC_FLAGS=-DSR_DEBUG_CHECKS python -m
+// paper_2511_16193_b200.build): device-side bounds asserts on every index the
+// hot path computes from device state (token rows, KV pages, branch slots).
+// compute-sanitizer is not available on the GPU pool, so the test suite runs
+// against this build instead (scripts/debug_checks.sh).
+#ifdef SR_DEBUG_CHECKS
+#include <cassert>
+#define SR_DCHECK(cond) assert(cond)
+#else
+#define SR_DCHECK(cond) ((void)0)
+#endif
+
 namespace sr {
 
 void set_error(const char* fmt, ...);

@@ -105,7 +105,9 @@ __global__ void rope_scatter_kernel(const T* __restrict__ qkv, const int32_t* __
   int64_t head_stride;  // elements between consecutive kv heads at this slot
   int slot_id;          // swizzle key of the destination row
   if (sq.branch < 0) {
+    SR_DCHECK(pos >= 0 && pos / kv.page < kv.max_pages);
     const int page = kv.block_table[(int64_t)sq.request * kv.max_pages + pos / kv.page];
+    SR_DCHECK(page >= 0 && page < kv.num_pages);
     const int slot = pos % kv.page;
     T* base = reinterpret_cast<T*>(kv.cache) + layer * kv.cache_layer_elems() +
               (int64_t)page * 2 * nkv * kv.page * hd;
@@ -339,7 +341,9 @@ __global__ void kv_rows_kernel(const SeqInfo* __restrict__ seqs, int S, const in
   const int hd = kv.head_dim, nkv = kv.kv_heads;
   if (sq.branch < 0) {
     const int pos = positions[t];
+    SR_DCHECK(pos >= 0 && pos / kv.page < kv.max_pages);
     const int page = kv.block_table[(int64_t)sq.request * kv.max_pages + pos / kv.page];
+    SR_DCHECK(page >= 0 && page < kv.num_pages);
     dst[t] = (int64_t)page * 2 * nkv * kv.page * hd;
     info[t] = pos % kv.page;
   } else {

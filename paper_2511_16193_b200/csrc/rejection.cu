@@ -232,6 +232,7 @@ rs_commit_kernel(int B, const SeqInfo* __restrict__ seqs, const int32_t* __restr
   }
   if (threadIdx.x == 0) {
     const int base = seq_len[b];
+    SR_DCHECK(base + committed <= tok_stride);
     int32_t* trow = tokens + (int64_t)b * tok_stride + base;
     const int keep = min(a, committed);
     for (int i = 0; i < keep; ++i) trow[i] = token_ids[q0 + 1 + i];
