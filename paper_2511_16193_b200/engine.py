@@ -307,13 +307,33 @@ class RolloutEngine:
 
     # -- one speculation window ------------------------------------------------
 
+    def _side_stream(self, n: int):
+        if not hasattr(self, "_sides"):
+            self._sides = {}
+        if n not in self._sides:
+            self._sides[n] = torch.cuda.Stream(device=self.dev)
+        return self._sides[n]
+
     def _enqueue_step(self, slot: int) -> None:
         lib, st = self.lib, _native.stream_handle()
         drafts_ptr, nd_ptr = None, None
         if self.k > 0:
+            # several small-model drafters (Best-of-N) are independent small-M
+            # forwards that each fill a fraction of the GPU: run them on their
+            # own streams (graph branches) and join before the verify batch
+            cur = torch.cuda.current_stream()
+            parallel = sum(isinstance(d, ModelDrafter) for d in self.drafters) > 1
+            forks = []
             for n, d in enumerate(self.drafters):
                 if isinstance(d, ModelDrafter):
-                    d.enqueue(self.drafts[n], self.ndraft[n])
+                    if parallel:
+                        side = self._side_stream(n)
+                        side.wait_stream(cur)
+                        with torch.cuda.stream(side):
+                            d.enqueue(self.drafts[n], self.ndraft[n])
+                        forks.append(side)
+                    else:
+                        d.enqueue(self.drafts[n], self.ndraft[n])
                     continue
                 if isinstance(d, SyntheticDrafter):
                     _native.check(lib.sr_synthetic_draft(
@@ -326,6 +346,8 @@ class RolloutEngine:
                     self.B, self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(), d.min_n, d.max_n,
                     self.k, self.drafts[n].data_ptr(), self.ndraft[n].data_ptr(),
                     self.ngram_scratch.data_ptr(), st), "sr_ngram_propose")
+            for side in forks:
+                cur.wait_stream(side)
             drafts_ptr, nd_ptr = self.drafts.data_ptr(), self.ndraft.data_ptr()
         _native.check(lib.sr_build_verify_batch(
             self.B, self.N, self.k, self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(),
