@@ -567,6 +567,12 @@ def variant_configs2(steps=10, warmup=2, batch=64, graph=True):
     gen0 = int(eng.gen_len.sum())
     ms = timed(lambda: [eng.step() for _ in range(steps)], 1)
     committed = int(eng.gen_len.sum()) - gen0
+    if os.environ.get("SR_PROFILE_STEP"):       # one step inside a profiler range (ncu --profile-from-start off)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        eng.step()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
     out = {"value": committed / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
            "config": f"configs[2] per-GPU share: qwen2.5-7b-shaped target, {batch} prompts, k={K}, Best-of-N "
                      f"N=3 (n-gram + 0.5B + 1.5B-shaped model drafters), greedy",
