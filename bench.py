@@ -16,8 +16,10 @@ target's own greedy continuation, accepted by the reference's keyed
 n-gram drafter ~0 acceptance, so it is reported beside it (``variants.ngram``),
 together with the configs[2] shape on one GPU (``variants.configs2_7b``: 7B
 target, 64 prompts = the per-GPU share of 512 over 8 GPUs, Best-of-N with
-n-gram + 0.5B + 1.5B-shaped model drafters) and the n-gram kernel alone at
-1024 x 20K context (``variants.ngram_kernel``).
+n-gram + 0.5B + 1.5B-shaped model drafters), the configs[4] shape on one GPU
+(``variants.configs4_32b``: 32B target, 64 prompts, T = 1 keyed sampling,
+Best-of-N N = 4) and the n-gram kernel alone at 1024 x 20K context
+(``variants.ngram_kernel``).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
@@ -583,6 +585,50 @@ def variant_configs2(steps=10, warmup=2, batch=64, graph=True):
     return out
 
 
+def variant_configs4(steps=6, warmup=2, batch=64, graph=True):
+    """configs[4] on one GPU: Qwen2.5-32B-shaped target (weights built layer
+    by layer), 64 prompts (the paper's per-GPU share), T = 1.0 keyed sampling,
+    Best-of-N with N = 4 drafters (n-gram at four (min_n, max_n) settings: the
+    paper has three methods, SURVEY §8(d) C5 leaves the fourth to the
+    builder), k = 4.  Exact-match verification against the target's keyed
+    sample keeps the committed tokens equal to plain sampled decoding."""
+    import torch
+
+    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine
+    from paper_2511_16193_b200.model import DeviceModel, init_weights, shape
+
+    s = shape("qwen2.5-32b")
+    trace, prompts, budget = workload(0, batch, steps + warmup + 4, s.vocab)
+    max_len = max(len(p) for p in prompts) + budget[0] + K + 8
+    N = 4
+    w = init_weights(s, seed=0, device="cuda", lazy=True)
+    m = DeviceModel(s, w, dtype="bf16", max_requests=batch, max_len=max_len, max_tokens=batch * N * (K + 1),
+                    max_seqs=batch * N, branches=batch * (N - 1))
+    del w
+    torch.cuda.empty_cache()
+    drafters = (NgramDrafter(1, 3), NgramDrafter(2, 2), NgramDrafter(1, 1), NgramDrafter(3, 4))
+    eng = RolloutEngine(m, prompts, budget, k=K, drafters=drafters, bonus_token=True, history=1,
+                        temperature=1.0, seed=7)
+    eng.prefill()
+    if graph:
+        eng.capture()
+    for _ in range(warmup):
+        eng.step()
+    gen0 = int(eng.gen_len.sum())
+    ms = timed(lambda: [eng.step() for _ in range(steps)], 1)
+    committed = int(eng.gen_len.sum()) - gen0
+    rows = eng.live_rows.item()
+    out = {"value": committed / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
+           "verify_rows_last_step": int(rows),
+           "config": f"configs[4] per-GPU share: qwen2.5-32b-shaped target, {batch} prompts, k={K}, T=1.0 keyed "
+                     f"sampling, Best-of-N N=4 (n-gram (1,3) (2,2) (1,1) (3,4))",
+           "note": "random-init target + random prompts: n-gram drafts rarely exist, so compacted verify "
+                   "batches are ~1 row per request and the step is the 32B weight stream (64 GB bf16)"}
+    del eng, m
+    torch.cuda.empty_cache()
+    return out
+
+
 # -- CPU baselines (ports of the same path; test infrastructure, oracle/) --------------------
 
 
@@ -769,6 +815,7 @@ def main():
             import torch
             torch.cuda.empty_cache()
             result["variants"]["configs2_7b"] = variant_configs2()
+            result["variants"]["configs4_32b"] = variant_configs4()
     clocks.stop()
     result["clocks"] = clocks.summary()
     if rank == 0:

@@ -161,6 +161,9 @@ __global__ void build_verify_kernel(int B, int N, int k, const int32_t* __restri
     if (active_mask != nullptr && active_mask[n * B + b] == 0) active = false;  // drafter off for b
     nd = max(0, min(nd, min(k, remaining)));
     if (window != nullptr) nd = min(nd, max(0, window[b]));  // per-request window (reconfiguration)
+    // a Best-of-N branch with nothing to propose cannot beat the incumbent
+    // (ties go to drafter 0): no window, its outcome row stays zero
+    if (n > 0 && nd == 0) active = false;
   }
   SR_DCHECK(!active || (L >= 1 && L + nd <= tok_stride));
   SeqInfo sq;
@@ -225,6 +228,7 @@ build_verify_compact_kernel(int B, int N, int k, const int32_t* __restrict__ tok
         if (active_mask != nullptr && active_mask[n * B + b] == 0) active = false;  // drafter off for b
         nd = max(0, min(nd, min(k, remaining)));
         if (window != nullptr) nd = min(nd, max(0, window[b]));
+        if (n > 0 && nd == 0) active = false;  // empty BoN branch: cannot beat the incumbent
       }
       q_len = active ? nd + 1 : 0;
     }

@@ -1063,14 +1063,22 @@ int launch_pair(const GemmPlan& p, int M, cudaStream_t stream) {
 // slower).  Two pairs per cluster multicasting A save ~3% when the grid is a
 // single wave with an even tile count per row block, and lose badly
 // (cluster-of-4 residency) over several waves.
+// tuning probe: cap the pair tile width (SR_PAIR_BN_MAX, default 256)
+int g_pair_bn_max = [] {
+  const char* v = getenv("SR_PAIR_BN_MAX");
+  const int b = v ? atoi(v) : 256;
+  return b >= 64 && b <= 256 ? b : 256;
+}();
+
 void choose_pair_tile(int M, int N, int K, int epi, int* bn_out, int* mc_out) {
   static const int cands[] = {256, 224, 192, 160, 128, 96, 64};
   const int num_m = (M + 255) / 256;
   const int kb = (K + 63) / 64;
   const int pairs = num_sms() / 2;
-  int best = 256;
+  int best = g_pair_bn_max;
   double best_t = 1e30;
   for (int bn : cands) {
+    if (bn > g_pair_bn_max) continue;
     if ((epi == kEpiSwiGLU || epi == kEpiQkvRope) && bn % 32 != 0) continue;
     const int tiles = num_m * ((N + bn - 1) / bn);
     const int waves = (tiles + pairs - 1) / pairs;
