@@ -130,6 +130,19 @@ int sr_gemm(int dtype, int M, int N, int K, const void* A, int lda, const void* 
             void* C, int ldc, int epilogue, const float* bias, int bn, int32_t* aux,
             sr_stream_t stream);
 
+/* K ranges the bf16 projection (N, K, epilogue) is split into: its small-M
+ * mode (live rows <= 128; weights as the 256-row UMMA side, tokens as N)
+ * spreads (weight tile, K range) units over the SMs and sums the ranges'
+ * fp32 partials in order, and the large-M mode sums one TMEM accumulator
+ * per range in the same order, so a row's bits do not depend on how many
+ * rows a launch carries.  Depends on the shape and the SM count only. */
+int sr_gemm_splits(int N, int K, int epilogue);
+
+/* Live-row threshold of the small-M mode for GEMM plans (sr_gemm, models)
+ * created afterwards: -1 = per shape (default: the weight bytes decide),
+ * 0 = off, 1..128.  Either mode gives the same bits. */
+int sr_set_gemm_swap_max_m(int max_m);
+
 /* ---------------------------------------------------------------------------
  * K1+K2+K6  Verification forward of the target model (Qwen2-style decoder:
  * RMSNorm, RoPE, GQA with QKV bias, SwiGLU, tied or untied lm_head).  The

@@ -31,6 +31,8 @@ SIGNATURES: dict[str, list] = {
     "sr_ngram_propose": [_i32, _vp, _i64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
     "sr_gemm": [_i32, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _i32, _vp, _i32,
                 _vp, _vp],
+    "sr_gemm_splits": [_i32, _i32, _i32],
+    "sr_set_gemm_swap_max_m": [_i32],
     "sr_paged_attention": [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _i32,
                            _vp, _i32, _vp, _i32, _i32, _vp, ctypes.c_uint64, _vp, _vp],
     "sr_set_attention_split": [_i32],

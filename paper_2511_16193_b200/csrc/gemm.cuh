@@ -45,17 +45,22 @@ struct RopeArgs {
 
 // Fused RMSNorm.  norm(x) W = r (x o w) W with r = rsqrt(mean(x^2) + eps) per
 // row, so the residual GEMM that produces x (kEpiResidualNorm) writes
-// bf16(x o w) as the next GEMM's A operand plus per-N-tile partial sums of
-// x^2, and the consuming GEMM scales each accumulator row by r (summing the
-// partials in tile order) before its bias / SwiGLU / argmax.  No separate
-// normalization pass touches the residual stream.
+// bf16(x o w) as the next GEMM's A operand plus partial sums of x^2 per
+// 128-column group, and the consuming GEMM scales each accumulator row by r
+// (summing the partials in column order) before its bias / SwiGLU / argmax.
+// No separate normalization pass touches the residual stream.  A group's
+// partial has one fixed form, whatever tile or GEMM mode produced it: per
+// 32-column chunk s_q = fma chain over columns 4q..4q+3 (q = 0..7), chunk =
+// ((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)); group = the chunks
+// summed in column order.  Producer tiles are 128 or 256 wide.
+constexpr int kSsqCols = 128;
 struct NormArgs {
   const float* ssq_in = nullptr;  // consumer: [M, parts_in] (nullptr: no row scaling)
   int parts_in = 0;
   float hdim = 0.0f, eps = 0.0f;
   __nv_bfloat16* h_out = nullptr;  // producer (kEpiResidualNorm): [M, ld_h]
   const float* w = nullptr;        // norm weights [N]
-  float* ssq_out = nullptr;        // [M, N tiles of this GEMM]
+  float* ssq_out = nullptr;        // [M, ceil(N / kSsqCols)]
   int ld_h = 0;
 };
 
@@ -63,8 +68,37 @@ struct NormArgs {
 int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                    uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer);
 
+// Small-M ("swap") mode of the CTA-pair kernel, taken on device when the live
+// row count is <= max_m: the pair computes C^T = W A^T -- 256 weight rows as
+// the UMMA M side (128 per CTA), the <= 128 live tokens as N -- so a launch
+// streams weights on many SMs instead of padding tokens to 256-row tiles.
+// Long-K projections split K into `splits` contiguous ranges (one pair per
+// (256-row weight tile, range)); fp32 partials go through `ws` and the last
+// pair to arrive on a tile sums them in range order.  The pair mode keeps
+// one TMEM accumulator per range and sums them in the same order, so both
+// modes produce identical bits for every row (batch invariance across
+// live-row counts).  `splits` is a function of (N, K) only.
+constexpr int kSwapRows = 128;
+// The small-M mode's tensor maps live in device memory (a 640-byte block per
+// plan, uploaded once) so the kernel parameter block stays small: launch
+// cost grows with it.
+struct SwapMaps {
+  CUtensorMap w;         // W [N, K] as (64, rows, K / 64), box (64, 128, 2)
+  CUtensorMap x[4];      // A [cap, K], box (64, 16 (g + 1), 2): token rows per CTA
+};
+struct SwapArgs {
+  const SwapMaps* maps = nullptr;  // device copy of the plan's maps
+  float* ws = nullptr;   // [splits][kSwapRows][N] fp32 partials
+  int32_t* cnt = nullptr;  // [2 ceil(N / 256)] arrival counters, zero between launches
+  int splits = 1;
+  int max_m = 0;         // 0: swap mode off
+  int flags = 1;         // bit 0: stage the first weight blocks before griddepcontrol.wait
+};
+
 struct GemmPlan {
   CUtensorMap a, b;
+  SwapArgs sw;
+  SwapMaps sw_maps;   // host copy; the owner uploads it and sets sw.maps
   int M, N, K, bn, epi;
   bool pair;          // CTA-pair (cta_group::2, 256-row tiles) kernel
   int mc;             // pairs per cluster sharing (multicasting) A: 1 | 2
@@ -92,6 +126,11 @@ int gemm_bf16_plan(GemmPlan* plan, int M, int N, int K, const __nv_bfloat16* A, 
 // beyond it are computed from stale memory and discarded).
 int gemm_bf16_launch(const GemmPlan& plan, cudaStream_t stream, int m_override = -1);
 int gemm_num_n_tiles(int N, int bn);
+// Workspace (bytes) the plan's swap mode needs: partials + counters.
+size_t gemm_swap_ws_floats(const GemmPlan& plan);
+size_t gemm_swap_cnt_ints(const GemmPlan& plan);
+// Number of K ranges a (N, K) projection is split into (see SwapArgs).
+int gemm_splits(int N, int K, int epi);
 
 // fp32 parity path (CUDA cores, fixed k order): same epilogues, f32 activations.
 int gemm_f32(int M, int N, int K, const float* A, int lda, const float* W, int ldw, void* C,

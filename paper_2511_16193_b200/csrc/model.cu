@@ -128,6 +128,10 @@ struct Model {
   int32_t* key_pos;
   float* ssq;          // fused RMSNorm partial sums of x^2 [T, parts] (bf16 path)
   float* ssq_sel;      // the same for the gathered lm_head rows
+  float* swap_ws;      // small-M GEMM mode: fp32 K-range partials
+  SwapMaps* swap_maps; // and its tensor maps (device copies, [layer][qkv, o, down])
+  int32_t* swap_cnt;   // and its arrival counters (zeroed at create, self-resetting)
+  size_t swap_cnt_ints;
   int64_t* kv_dst;     // per token row: KV destination for the fused qkv + RoPE epilogue
   int32_t* kv_info;
   int prep_parts;      // slots the embedding-side norm prep writes (= qkv[0]'s consumer count)
@@ -159,12 +163,29 @@ static size_t carve(const sr_model_desc& d, Model* m, char* base) {
   float* ap = c.take<float>(d.dtype == 1 ? pf : 0);
   int32_t* kr = c.take<int32_t>((size_t)T);
   int32_t* kp = c.take<int32_t>((size_t)T);
-  const int max_parts = (H + 63) / 64;  // residual GEMM N tiles (tile width >= 64)
+  const int max_parts = (H + kSsqCols - 1) / kSsqCols;  // RMSNorm partials per row
   float* ssq = c.take<float>(d.dtype == 1 ? (size_t)T * max_parts : 0);
   float* ssq_sel = c.take<float>(d.dtype == 1 ? (size_t)T * max_parts : 0);
   int64_t* kv_dst = c.take<int64_t>(d.dtype == 1 ? (size_t)T : 0);
   int32_t* kv_info = c.take<int32_t>(d.dtype == 1 ? (size_t)T : 0);
+  // small-M mode partials / counters of the qkv, o and down projections
+  size_t swf = 0, swc = 0;
+  if (d.dtype == 1) {
+    const int nqd = d.q_heads * d.head_dim;
+    const int shp[3][3] = {{qkv_w, H, kEpiQkvRope}, {H, nqd, kEpiResidualNorm}, {H, d.intermediate, kEpiResidualNorm}};
+    for (auto& g : shp) {
+      const int sp = gemm_splits(g[0], g[1], g[2]);
+      const size_t f = sp > 1 ? (size_t)sp * kSwapRows * g[0] : 0, cn = (size_t)2 * ((g[0] + 255) / 256);
+      swf = f > swf ? f : swf;
+      swc = cn > swc ? cn : swc;
+    }
+  }
+  float* sw_ws = c.take<float>(swf);
+  int32_t* sw_cnt = c.take<int32_t>(swc);
+  // device copies of the qkv / o / down plans' small-M tensor maps (64-byte aligned)
+  SwapMaps* sw_maps = d.dtype == 1 ? c.take<SwapMaps>((size_t)3 * d.layers) : nullptr;
   if (m != nullptr) {
+    m->swap_ws = sw_ws; m->swap_cnt = sw_cnt; m->swap_cnt_ints = swc; m->swap_maps = sw_maps;
     m->x = x; m->h = h; m->qkv = qkv; m->q = q; m->attn = attn; m->act = act; m->h_sel = h_sel;
     m->logits = logits; m->part_val = pv; m->part_idx = pi; m->attn_part = ap;
     m->key_req = kr; m->key_pos = kp;
@@ -271,6 +292,24 @@ int sr_model_create(const sr_model_desc* desc, void** handle) {
       if (!rc) rc = sr::gemm_bf16_plan(&m->p_down[l], T, H, I, (const bf*)m->act, I, (const bf*)w[6], I,
                                        m->x, H, sr::kEpiResidualNorm, nullptr, 0);
       if (rc) { delete m; return rc; }
+      int j = 0;
+      for (sr::GemmPlan* gp : {&m->p_qkv[l], &m->p_o[l], &m->p_down[l]}) {
+        gp->sw.ws = m->swap_ws;
+        gp->sw.cnt = m->swap_cnt;
+        if (sr::gemm_swap_ws_floats(*gp) > 0 && m->swap_ws == nullptr) rc = sr::config_error("swap workspace");
+        if (gp->sw.max_m > 0) {
+          sr::SwapMaps* dst = m->swap_maps + 3 * l + j;
+          if (cudaMemcpy(dst, &gp->sw_maps, sizeof(sr::SwapMaps), cudaMemcpyHostToDevice) != cudaSuccess)
+            rc = sr::config_error("cannot upload the GEMM tensor maps");
+          gp->sw.maps = dst;
+        }
+        ++j;
+      }
+      if (rc) { delete m; return rc; }
+    }
+    if (m->swap_cnt_ints > 0 && cudaMemset(m->swap_cnt, 0, m->swap_cnt_ints * sizeof(int32_t)) != cudaSuccess) {
+      delete m;
+      return sr::config_error("cannot zero the GEMM counters");
     }
     for (int sel = 0; sel < 2 && !rc; ++sel) {
       const bf* a_in = (const bf*)(sel ? m->h_sel : m->h);
@@ -282,6 +321,10 @@ int sr_model_create(const sr_model_desc* desc, void** handle) {
                                 (const bf*)d.lm_head, H, m->logits, (d.vocab + 7) / 8 * 8, sr::kEpiStoreF32,
                                 nullptr, 0);
     }
+    // the logits lm_head (parity / rejection-sampling output) keeps the
+    // large-M mode: a vocabulary-wide N already spreads over every SM
+    m->p_lm_logits.sw.max_m = 0;
+    m->p_lm_logits_sel.sw.max_m = 0;
     if (!rc) m->lm_tiles = sr::gemm_num_n_tiles(d.vocab, m->p_lm_argmax.bn);
     if (rc) { delete m; return rc; }
     // Fused RMSNorm wiring: o / down write bf16(x o w_next) + partials; qkv /
@@ -291,7 +334,7 @@ int sr_model_create(const sr_model_desc* desc, void** handle) {
       p.norm.w = wn;
       p.norm.ssq_out = m->ssq;
       p.norm.ld_h = H;
-      return sr::gemm_num_n_tiles(H, p.bn);
+      return (H + sr::kSsqCols - 1) / sr::kSsqCols;
     };
     auto consumer = [&](sr::GemmPlan& p, const float* ssq, int parts) {
       p.norm.ssq_in = ssq;
@@ -299,7 +342,7 @@ int sr_model_create(const sr_model_desc* desc, void** handle) {
       p.norm.hdim = (float)H;
       p.norm.eps = d.rms_eps;
     };
-    int parts = m->prep_parts = sr::gemm_num_n_tiles(H, m->p_down[0].bn);
+    int parts = m->prep_parts = (H + sr::kSsqCols - 1) / sr::kSsqCols;
     for (int l = 0; l < d.layers; ++l) {
       const void* const* w = m->layer_ptrs.data() + (size_t)l * sr::kLayerPtrs;
       const void* const* wn = l + 1 < d.layers ? w + sr::kLayerPtrs : nullptr;

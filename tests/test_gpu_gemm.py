@@ -182,3 +182,69 @@ def test_pair_batch_invariance(bn):
     other = torch.empty(1280, 1536, device="cuda")
     sr_gemm(A, W, other, EPI_F32, None, -128 if bn == -1152 else -1136)
     assert torch.equal(other, big)
+
+
+# Small-M ("swap") mode: live rows <= 128 run C^T = W A^T with K split into
+# ranges summed in order; the large-M pair mode sums per-range TMEM
+# accumulators in the same order.  Rows must come out bit-identical whichever
+# mode (and however many rows) a launch runs, and match torch within bf16
+# tolerance.  Shapes: 1.5B qkv/o/down, 0.5B down, ragged N and K.
+SWAP_SHAPES = [(512, 256), (1536, 1536), (2048, 1536), (1536, 8960), (896, 4864), (1000, 448), (4608, 3584)]
+
+
+@pytest.fixture
+def swap_everywhere():
+    """Small-M mode for every swap-capable plan at <= 128 live rows (the
+    default threshold depends on the weight bytes)."""
+    from paper_2511_16193_b200 import _native
+
+    lib = _native.lib()
+    _native.check(lib.sr_set_gemm_swap_max_m(128), "swap threshold")
+    yield
+    _native.check(lib.sr_set_gemm_swap_max_m(-1), "swap threshold")
+
+
+@pytest.mark.parametrize("N,K", SWAP_SHAPES)
+def test_small_m_mode_bit_identical_to_pair_mode(N, K, swap_everywhere):
+    from paper_2511_16193_b200 import _native
+
+    splits = _native.lib().sr_gemm_splits(N, K, EPI_F32)
+    assert splits >= 1
+    if (N, K) == (1536, 8960):
+        assert splits > 1  # the K-range reduction is exercised
+    g = torch.Generator(device="cuda").manual_seed(N + 3 * K)
+    big_m = 320
+    A = torch.randn(big_m, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g)
+    R0 = torch.randn(big_m, N, device="cuda", generator=g)
+    exp = ref(A, W, bias)
+    for epi in (EPI_F32, EPI_STORE, EPI_RESID):
+        out_dtype = torch.bfloat16 if epi == EPI_STORE else torch.float32
+        b = None if epi == EPI_RESID else bias
+        big = R0.clone() if epi == EPI_RESID else torch.empty(big_m, N, device="cuda", dtype=out_dtype)
+        sr_gemm(A, W, big, epi, b)
+        for m in (1, 17, 32, 64, 100, 128):
+            small = R0[:m].clone() if epi == EPI_RESID else torch.empty(m, N, device="cuda", dtype=out_dtype)
+            sr_gemm(A[:m].contiguous(), W, small, epi, b)
+            assert torch.equal(small, big[:m]), f"epi {epi} m {m}: small-M mode differs from the pair mode"
+        if epi == EPI_F32:
+            torch.testing.assert_close(big, exp, rtol=1e-4, atol=2e-3)
+        if epi == EPI_RESID:
+            torch.testing.assert_close(big, R0 + ref(A, W), rtol=1e-4, atol=2e-3)
+
+
+def test_small_m_mode_repeated_launches_reset_counters(swap_everywhere):
+    """The K-range arrival counters reset themselves: many back-to-back small-M
+    launches (different row counts) give the same bits as the first."""
+    N, K = 1536, 8960
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randn(128, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    first = torch.empty(128, N, device="cuda")
+    sr_gemm(A, W, first, EPI_F32)
+    for it in range(20):
+        m = 1 + (it * 37) % 128
+        out = torch.empty(m, N, device="cuda")
+        sr_gemm(A[:m].contiguous(), W, out, EPI_F32)
+        assert torch.equal(out, first[:m])

@@ -164,6 +164,36 @@ def test_verify_logits_equal_decode_logits_bit_exact():
         assert torch.equal(one[0], win[j]), f"slot {j}"
 
 
+@pytest.mark.parametrize("shape_name,layers", [("tiny", None), ("qwen2.5-1.5b", 2)])
+def test_small_m_window_logits_equal_large_prefill_bit_exact(shape_name, layers):
+    """Positions prefilled in one 300-row forward (large-M GEMM mode) and
+    re-verified as a 6-row window (small-M mode: weights as the UMMA M side,
+    K ranges summed in order, fused qkv-RoPE / residual-RMSNorm epilogues
+    through the transpose) give bit-identical logits."""
+    from paper_2511_16193_b200 import _native
+    from paper_2511_16193_b200.model import seq_table
+
+    lib = _native.lib()
+    _native.check(lib.sr_set_gemm_swap_max_m(128), "swap threshold")  # every projection, any size
+    try:
+        s, w, m = make(shape_name, "bf16", layers=layers, B=1, logits=512, max_len=512)
+    finally:
+        _native.check(lib.sr_set_gemm_swap_max_m(-1), "swap threshold")
+    rng = np.random.default_rng(3)
+    L = 300
+    ids = torch.from_numpy(rng.integers(0, s.vocab, L).astype(np.int32)).cuda()
+    pos = torch.arange(L, dtype=torch.int32, device="cuda")
+    full = torch.empty(L, s.vocab, device="cuda")
+    m.forward(ids, pos, seq_table([(0, L, 0, 0, -1)], "cuda"), num_seqs=1, max_q_len=L, max_key=L - 1,
+              out=full, output=1)
+    P = L - 6
+    win = torch.empty(6, s.vocab, device="cuda")
+    m.forward(ids[P:], pos[P:], seq_table([(0, 6, 0, P, -1)], "cuda"), num_seqs=1, max_q_len=6,
+              max_key=L - 1, out=win, output=1)
+    torch.cuda.synchronize()
+    assert torch.equal(win, full[P:])
+
+
 def test_accept_commit_kernel_vs_python():
     """K3 on random verify batches (N=3 drafters, budgets, bonus) vs a direct
     restatement of sim.py:983-1042 + longest-prefix Best-of-N."""
