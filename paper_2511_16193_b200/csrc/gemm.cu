@@ -157,7 +157,7 @@ int swap_max_m(int N, int K) {
 
 bool swap_epi(int epi) {
   return epi == kEpiStoreBf16 || epi == kEpiStoreF32 || epi == kEpiResidualF32 || epi == kEpiResidualNorm ||
-         epi == kEpiQkvRope;
+         epi == kEpiQkvRope || epi == kEpiSwiGLU;
 }
 
 // sr_gemm's own partials / counters (the model carves its own)
@@ -292,6 +292,10 @@ int gemm_bf16_plan(GemmPlan* p, int M, int N, int K, const __nv_bfloat16* A, int
   const int mrows = M > 0 ? M : 1;
   p->sw.splits = pair ? splits : 1;
   p->sw.max_m = (pair && p->kc == 2 && swappable) ? swap_max_m(N, K) : 0;
+  // wide-N SwiGLU plans for large batches keep the lean pair kernel (the
+  // small-M mode costs its large-M path a few percent); launches of few
+  // rows take a plan made for them (the model's narrow plans)
+  if (epi == kEpiSwiGLU && M > 256 && g_swap_max_m < 0) p->sw.max_m = 0;
   p->sw.ws = nullptr;
   p->sw.cnt = nullptr;
   p->sw.maps = nullptr;

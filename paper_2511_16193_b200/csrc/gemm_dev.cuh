@@ -622,7 +622,7 @@ __device__ __forceinline__ void add_splits(uint32_t taddr, int splits, int strid
 // Epilogues the small-M (swap) mode runs: the row-major 32-column chunk
 // epilogues, reached through a per-warp 32 x 32 transpose.
 template <int EPI>
-constexpr bool kSwapEpi = EPI == kEpiStoreBf16 || EPI == kEpiStoreF32 || EPI == kEpiResidualF32 ||
+constexpr bool kSwapEpi = EPI == kEpiStoreBf16 || EPI == kEpiStoreF32 || EPI == kEpiResidualF32 || EPI == kEpiSwiGLU ||
                           EPI == kEpiResidualNorm || EPI == kEpiQkvRope;
 
 
@@ -696,6 +696,17 @@ __device__ __forceinline__ void swap_epilogue(uint32_t (&v)[32], int row0, int c
       if (row0 + lane < M && col0 < N) na.ssq_out[(int64_t)(row0 + lane) * parts + col0 / kSsqCols] = gsum;
     }
     epi_bar_sync();
+  } else if constexpr (EPI == kEpiSwiGLU) {
+    // the warp's 32 columns are one interleave block: lanes 0-15 gate, 16-31 up
+    const bool ok = col0 + 32 <= N;  // N % 32 == 0 (plan)
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float x = __uint_as_float(v[i]);
+      const float up = __shfl_down_sync(0xffffffffu, x, 16);
+      if (lane < 16 && ok && row0 + i < M)
+        reinterpret_cast<__nv_bfloat16*>(C)[(int64_t)(row0 + i) * ldc + col0 / 2 + lane] =
+            __float2bfloat16_rn(silu(x) * up);
+    }
   } else if constexpr (EPI == kEpiQkvRope) {
     const int hd = ra.hd, half = hd >> 1;
     const int hq = ra.nq * hd, hk = ra.nkv * hd;

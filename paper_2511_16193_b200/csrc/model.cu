@@ -38,6 +38,7 @@ namespace {
 
 constexpr int kLayerPtrs = 7;  // ln1, w_qkv, b_qkv, w_o, ln2, w_gu, w_down
 constexpr int kLmBn = 64;  // smallest lm_head tile width: sizes the argmax partials
+constexpr int kNarrowRows = 256;  // launches up to this many rows use the narrow plans
 
 __global__ void gather_rows_kernel(const void* __restrict__ src, const int32_t* __restrict__ rows, int H,
                                    int esize, void* __restrict__ dst) {
@@ -129,7 +130,7 @@ struct Model {
   float* ssq;          // fused RMSNorm partial sums of x^2 [T, parts] (bf16 path)
   float* ssq_sel;      // the same for the gathered lm_head rows
   float* swap_ws;      // small-M GEMM mode: fp32 K-range partials
-  SwapMaps* swap_maps; // and its tensor maps (device copies, [layer][qkv, o, down])
+  SwapMaps* swap_maps; // and its tensor maps (device copies, [plan set][layer][qkv, o, gate_up, down])
   int32_t* swap_cnt;   // and its arrival counters (zeroed at create, self-resetting)
   size_t swap_cnt_ints;
   int64_t* kv_dst;     // per token row: KV destination for the fused qkv + RoPE epilogue
@@ -138,6 +139,12 @@ struct Model {
   int lm_parts;        // partial slots behind the lm_head rows (last down's N tiles)
   // plans (bf16); *_sel read the gathered rows (h_sel, ssq_sel)
   std::vector<GemmPlan> p_qkv, p_o, p_gu, p_down;
+  // launches of <= kNarrowRows rows (decode, drafter steps) take plans made
+  // for that size: narrower tiles over more SMs.  A row's bits do not depend
+  // on the tile width (nor on the mode), only on the K ranges, which both
+  // plans share.
+  bool narrow = false;
+  std::vector<GemmPlan> n_qkv, n_o, n_gu, n_down;
   GemmPlan p_lm_argmax, p_lm_logits, p_lm_argmax_sel, p_lm_logits_sel;
 };
 
@@ -172,7 +179,8 @@ static size_t carve(const sr_model_desc& d, Model* m, char* base) {
   size_t swf = 0, swc = 0;
   if (d.dtype == 1) {
     const int nqd = d.q_heads * d.head_dim;
-    const int shp[3][3] = {{qkv_w, H, kEpiQkvRope}, {H, nqd, kEpiResidualNorm}, {H, d.intermediate, kEpiResidualNorm}};
+    const int shp[4][3] = {{qkv_w, H, kEpiQkvRope}, {H, nqd, kEpiResidualNorm}, {2 * d.intermediate, H, kEpiSwiGLU},
+                           {H, d.intermediate, kEpiResidualNorm}};
     for (auto& g : shp) {
       const int sp = gemm_splits(g[0], g[1], g[2]);
       const size_t f = sp > 1 ? (size_t)sp * kSwapRows * g[0] : 0, cn = (size_t)2 * ((g[0] + 255) / 256);
@@ -183,7 +191,7 @@ static size_t carve(const sr_model_desc& d, Model* m, char* base) {
   float* sw_ws = c.take<float>(swf);
   int32_t* sw_cnt = c.take<int32_t>(swc);
   // device copies of the qkv / o / down plans' small-M tensor maps (64-byte aligned)
-  SwapMaps* sw_maps = d.dtype == 1 ? c.take<SwapMaps>((size_t)3 * d.layers) : nullptr;
+  SwapMaps* sw_maps = d.dtype == 1 ? c.take<SwapMaps>((size_t)8 * d.layers) : nullptr;
   if (m != nullptr) {
     m->swap_ws = sw_ws; m->swap_cnt = sw_cnt; m->swap_cnt_ints = swc; m->swap_maps = sw_maps;
     m->x = x; m->h = h; m->qkv = qkv; m->q = q; m->attn = attn; m->act = act; m->h_sel = h_sel;
@@ -293,12 +301,12 @@ int sr_model_create(const sr_model_desc* desc, void** handle) {
                                        m->x, H, sr::kEpiResidualNorm, nullptr, 0);
       if (rc) { delete m; return rc; }
       int j = 0;
-      for (sr::GemmPlan* gp : {&m->p_qkv[l], &m->p_o[l], &m->p_down[l]}) {
+      for (sr::GemmPlan* gp : {&m->p_qkv[l], &m->p_o[l], &m->p_gu[l], &m->p_down[l]}) {
         gp->sw.ws = m->swap_ws;
         gp->sw.cnt = m->swap_cnt;
         if (sr::gemm_swap_ws_floats(*gp) > 0 && m->swap_ws == nullptr) rc = sr::config_error("swap workspace");
         if (gp->sw.max_m > 0) {
-          sr::SwapMaps* dst = m->swap_maps + 3 * l + j;
+          sr::SwapMaps* dst = m->swap_maps + 4 * l + j;
           if (cudaMemcpy(dst, &gp->sw_maps, sizeof(sr::SwapMaps), cudaMemcpyHostToDevice) != cudaSuccess)
             rc = sr::config_error("cannot upload the GEMM tensor maps");
           gp->sw.maps = dst;
@@ -356,6 +364,38 @@ int sr_model_create(const sr_model_desc* desc, void** handle) {
     consumer(m->p_lm_argmax_sel, m->ssq_sel, parts);
     consumer(m->p_lm_logits_sel, m->ssq_sel, parts);
     m->lm_parts = parts;
+    // narrow plans (same operands, epilogue wiring and K ranges; tiles for <= kNarrowRows rows)
+    m->narrow = T > sr::kNarrowRows;
+    if (m->narrow) {
+      m->n_qkv = m->p_qkv; m->n_o = m->p_o; m->n_gu = m->p_gu; m->n_down = m->p_down;
+      for (int l = 0; l < d.layers && !rc; ++l) {
+        const void* const* w = m->layer_ptrs.data() + (size_t)l * sr::kLayerPtrs;
+        struct { sr::GemmPlan* big; sr::GemmPlan* nar; int N, K; const void* A; int lda; const void* W; int epi; } g[4] = {
+            {&m->p_qkv[l], &m->n_qkv[l], m->qkv_width, H, m->h, H, w[1], sr::kEpiQkvRope},
+            {&m->p_o[l], &m->n_o[l], H, nqd, m->attn, nqd, w[3], sr::kEpiResidualNorm},
+            {&m->p_gu[l], &m->n_gu[l], 2 * I, H, m->h, H, w[5], sr::kEpiSwiGLU},
+            {&m->p_down[l], &m->n_down[l], H, I, m->act, I, w[6], sr::kEpiResidualNorm}};
+        for (int j = 0; j < 4 && !rc; ++j) {
+          sr::GemmPlan np;
+          rc = sr::gemm_bf16_plan(&np, sr::kNarrowRows, g[j].N, g[j].K, (const bf*)g[j].A, g[j].lda, (const bf*)g[j].W,
+                                  g[j].K, g[j].big->c, g[j].big->ldc, g[j].epi, g[j].big->bias, 0, g[j].big->aux);
+          if (rc) break;
+          if (np.sw.splits != g[j].big->sw.splits) { rc = sr::config_error("narrow plan K ranges differ"); break; }
+          np.norm = g[j].big->norm;
+          np.rope = g[j].big->rope;
+          np.sw.ws = g[j].big->sw.ws;
+          np.sw.cnt = g[j].big->sw.cnt;
+          if (np.sw.max_m > 0) {
+            sr::SwapMaps* dst = m->swap_maps + 4 * (d.layers + l) + j;
+            if (cudaMemcpy(dst, &np.sw_maps, sizeof(sr::SwapMaps), cudaMemcpyHostToDevice) != cudaSuccess)
+              rc = sr::config_error("cannot upload the GEMM tensor maps");
+            np.sw.maps = dst;
+          }
+          *g[j].nar = np;
+        }
+      }
+      if (rc) { delete m; return rc; }
+    }
   }
   *handle = m;
   return SR_OK;
@@ -401,9 +441,14 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
     for (int l = 0; l < d.layers; ++l) {
       auto& P = m->prof;
       P.begin(sr::kProfQkv, st);
-      m->p_qkv[l].rope.pos = a->positions;
-      m->p_qkv[l].m_live = a->live_rows;
-      SR_TRY(sr::gemm_bf16_launch(m->p_qkv[l], st, M));
+      const bool nar = m->narrow && M <= sr::kNarrowRows;
+      sr::GemmPlan& pq = nar ? m->n_qkv[l] : m->p_qkv[l];
+      sr::GemmPlan& po = nar ? m->n_o[l] : m->p_o[l];
+      sr::GemmPlan& pg = nar ? m->n_gu[l] : m->p_gu[l];
+      sr::GemmPlan& pd = nar ? m->n_down[l] : m->p_down[l];
+      pq.rope.pos = a->positions;
+      pq.m_live = a->live_rows;
+      SR_TRY(sr::gemm_bf16_launch(pq, st, M));
       P.end(st);
       P.begin(sr::kProfAttn, st);
       SR_TRY(sr::attention_bf16((const bf*)m->q, seqs, S, a->max_q_len, a->max_key, m->kv, l, d.q_heads,
@@ -414,16 +459,16 @@ int sr_model_forward(void* handle, const sr_forward_args* a, sr_stream_t stream_
                                 m->attn_part, m->partial_floats, (bf*)m->attn, st, 1, false));
       P.end(st);
       P.begin(sr::kProfO, st);
-      m->p_o[l].m_live = a->live_rows;
-      SR_TRY(sr::gemm_bf16_launch(m->p_o[l], st, M));
+      po.m_live = a->live_rows;
+      SR_TRY(sr::gemm_bf16_launch(po, st, M));
       P.end(st);
       P.begin(sr::kProfGateUp, st);
-      m->p_gu[l].m_live = a->live_rows;
-      SR_TRY(sr::gemm_bf16_launch(m->p_gu[l], st, M));
+      pg.m_live = a->live_rows;
+      SR_TRY(sr::gemm_bf16_launch(pg, st, M));
       P.end(st);
       P.begin(sr::kProfDown, st);
-      m->p_down[l].m_live = a->live_rows;
-      SR_TRY(sr::gemm_bf16_launch(m->p_down[l], st, M));
+      pd.m_live = a->live_rows;
+      SR_TRY(sr::gemm_bf16_launch(pd, st, M));
       P.end(st);
     }
     // the last down GEMM left bf16(x o final_norm) in h and its partials in ssq

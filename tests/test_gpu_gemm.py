@@ -219,19 +219,24 @@ def test_small_m_mode_bit_identical_to_pair_mode(N, K, swap_everywhere):
     bias = torch.randn(N, device="cuda", generator=g)
     R0 = torch.randn(big_m, N, device="cuda", generator=g)
     exp = ref(A, W, bias)
-    for epi in (EPI_F32, EPI_STORE, EPI_RESID):
-        out_dtype = torch.bfloat16 if epi == EPI_STORE else torch.float32
-        b = None if epi == EPI_RESID else bias
-        big = R0.clone() if epi == EPI_RESID else torch.empty(big_m, N, device="cuda", dtype=out_dtype)
+    for epi in (EPI_F32, EPI_STORE, EPI_RESID, EPI_SWIGLU):
+        if epi == EPI_SWIGLU and N % 32 != 0:
+            continue
+        out_dtype = torch.bfloat16 if epi in (EPI_STORE, EPI_SWIGLU) else torch.float32
+        b = None if epi in (EPI_RESID, EPI_SWIGLU) else bias
+        ncols = N // 2 if epi == EPI_SWIGLU else N
+        big = R0.clone() if epi == EPI_RESID else torch.empty(big_m, ncols, device="cuda", dtype=out_dtype)
         sr_gemm(A, W, big, epi, b)
         for m in (1, 17, 32, 64, 100, 128):
-            small = R0[:m].clone() if epi == EPI_RESID else torch.empty(m, N, device="cuda", dtype=out_dtype)
+            small = R0[:m].clone() if epi == EPI_RESID else torch.empty(m, ncols, device="cuda", dtype=out_dtype)
             sr_gemm(A[:m].contiguous(), W, small, epi, b)
             assert torch.equal(small, big[:m]), f"epi {epi} m {m}: small-M mode differs from the pair mode"
         if epi == EPI_F32:
             torch.testing.assert_close(big, exp, rtol=1e-4, atol=2e-3)
         if epi == EPI_RESID:
             torch.testing.assert_close(big, R0 + ref(A, W), rtol=1e-4, atol=2e-3)
+        if epi == EPI_SWIGLU:
+            torch.testing.assert_close(big.float(), swiglu_ref(ref(A, W)), rtol=2e-2, atol=2e-2)
 
 
 def test_small_m_mode_repeated_launches_reset_counters(swap_everywhere):
