@@ -14,6 +14,8 @@ from pathlib import Path
 from .errors import ConfigError, DeviceError
 
 LIB_PATH = Path(__file__).resolve().parent / "libspecrollout_b200.so"
+if os.environ.get("SR_LIB_PATH"):  # measurement builds only (scripts/gemm_trace.py)
+    LIB_PATH = Path(os.environ["SR_LIB_PATH"])
 
 _i32, _i64, _u32, _dbl, _vp = (ctypes.c_int, ctypes.c_int64, ctypes.c_uint32,
                                ctypes.c_double, ctypes.c_void_p)

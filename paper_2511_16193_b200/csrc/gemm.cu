@@ -162,6 +162,7 @@ bool swap_epi(int epi) {
 
 // sr_gemm's own partials / counters (the model carves its own)
 float* g_swap_ws = nullptr;
+unsigned long long* g_trace_dev = nullptr;  // SR_GEMM_TRACE builds
 SwapMaps* g_swap_maps = nullptr;
 int32_t* g_swap_cnt = nullptr;
 size_t g_swap_ws_floats = 0, g_swap_cnt_ints = 0;
@@ -183,7 +184,11 @@ int gemm_splits(int N, int K, int epi) {
   const int pairs = num_sms() / 2;
   int best = 1;
   double best_t = 1e30;
-  for (int s = 1; s <= g_splits_max; ++s) {
+  // below 64 MB the pair mode's extra accumulator reads (large batches)
+  // outweigh more than two ranges for the small-M mode (1.5B down: the
+  // bench step +1.5% at 4 ranges)
+  const int smax = 2.0 * N * K < 64e6 && g_splits_max > 2 ? 2 : g_splits_max;
+  for (int s = 1; s <= smax; ++s) {
     if (chunks % s != 0 || (s > 1 && chunks / s < 8)) continue;
     const int waves = (tiles * s + pairs - 1) / pairs;
     const double t = waves * (chunks / s + 15.0) + (s > 1 ? 7.0 : 0.0);
@@ -292,14 +297,26 @@ int gemm_bf16_plan(GemmPlan* p, int M, int N, int K, const __nv_bfloat16* A, int
   const int mrows = M > 0 ? M : 1;
   p->sw.splits = pair ? splits : 1;
   p->sw.max_m = (pair && p->kc == 2 && swappable) ? swap_max_m(N, K) : 0;
-  // wide-N SwiGLU plans for large batches keep the lean pair kernel (the
-  // small-M mode costs its large-M path a few percent); launches of few
-  // rows take a plan made for them (the model's narrow plans)
-  if (epi == kEpiSwiGLU && M > 256 && g_swap_max_m < 0) p->sw.max_m = 0;
+  p->sw.flags = g_preissue ? 1 : 0;
+  // plans for more than 256 rows: the small-M mode only as a dual launch
+  // (pair + small-M kernel, the device picks by live rows), and only for
+  // weights >= 64 MB where small live batches (compacted verify tails,
+  // 7B / 32B targets) gain far more than the ~1-2 us of the second launch;
+  // smaller projections run their small batches through narrow plans
+  if (p->sw.max_m > 0 && M > 256) {
+    if (2.0 * N * K >= 64e6 || g_swap_max_m > 0) p->sw.flags |= 2;
+    else p->sw.max_m = 0;
+  }
   p->sw.ws = nullptr;
   p->sw.cnt = nullptr;
   p->sw.maps = nullptr;
-  p->sw.flags = g_preissue ? 1 : 0;
+#ifdef SR_GEMM_TRACE
+  if (g_trace_dev == nullptr) {
+    cudaMalloc(&g_trace_dev, 1024 * 8 * sizeof(unsigned long long));
+    cudaMemset(g_trace_dev, 0, 1024 * 8 * sizeof(unsigned long long));
+  }
+  p->sw.trace = g_trace_dev;
+#endif
   if (p->sw.max_m > 0) {
     int rc = make_tmap_bf16_3d(&p->sw_maps.w, W, (uint64_t)K, (uint64_t)N, (uint64_t)ldw * 2, 128, 2);
     for (int g = 0; g < 4 && rc == 0; ++g)
@@ -331,6 +348,15 @@ int gemm_bf16_launch(const GemmPlan& p, cudaStream_t stream, int m_override) {
   if (M == 0) return SR_OK;
   SR_REQUIRE(p.sw.max_m == 0 || (p.sw.maps != nullptr && p.sw.cnt != nullptr && (p.sw.splits == 1 || p.sw.ws != nullptr)),
              "small-M mode needs its device tensor maps, partials workspace and counters (SwapArgs)");
+  if (p.pair && p.sw.max_m > 0) {
+    // the launch's row count bounds the live rows: small-M mode alone
+    if (M <= p.sw.max_m) return launch_swap(p, M, stream);
+    // only the device knows the live rows: both kernels, each exits if not its case
+    if (p.sw.flags & 2) {
+      const int rc = launch_swap(p, M, stream);
+      if (rc) return rc;
+    }
+  }
   if (p.pair) return launch_pair(p, M, stream);
   return p.bn == 256 ? launch_bn<256>(p, M, stream) : launch_bn<128>(p, M, stream);
 }
@@ -477,9 +503,9 @@ extern "C" int sr_gemm_splits(int N, int K, int epilogue) {
 extern "C" int sr_debug_gemm_trace(unsigned long long* out, int n) {
 #ifdef SR_GEMM_TRACE
   if (n > 1024 * 8) n = 1024 * 8;
-  if (out) SR_CHECK_CUDA(cudaMemcpyFromSymbol(out, sr::g_gemm_trace, (size_t)n * 8));
-  static unsigned long long zeros[1024 * 8];
-  SR_CHECK_CUDA(cudaMemcpyToSymbol(sr::g_gemm_trace, zeros, sizeof(zeros)));  // cleared for the next launch
+  if (sr::g_trace_dev == nullptr) return sr::config_error("no traced GEMM plan yet");
+  if (out) SR_CHECK_CUDA(cudaMemcpy(out, sr::g_trace_dev, (size_t)n * 8, cudaMemcpyDeviceToHost));
+  SR_CHECK_CUDA(cudaMemset(sr::g_trace_dev, 0, 1024 * 8 * sizeof(unsigned long long)));  // cleared for the next launch
   return SR_OK;
 #else
   (void)out;

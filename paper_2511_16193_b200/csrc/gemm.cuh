@@ -93,6 +93,9 @@ struct SwapArgs {
   int splits = 1;
   int max_m = 0;         // 0: swap mode off
   int flags = 1;         // bit 0: stage the first weight blocks before griddepcontrol.wait
+#ifdef SR_GEMM_TRACE
+  unsigned long long* trace = nullptr;  // measurement builds: per-CTA phase stamps
+#endif
 };
 
 struct GemmPlan {

@@ -43,8 +43,7 @@ constexpr int kThreads = 192;
 // Measurement builds (-DSR_GEMM_TRACE): %globaltimer stamps per CTA and
 // event of the last launch, read back with sr_debug_gemm_trace.
 #ifdef SR_GEMM_TRACE
-__device__ unsigned long long g_gemm_trace[1024 * 8];
-#define GT(ev) (g_gemm_trace[blockIdx.x * 8 + (ev)] = sm100::global_timer_ns())
+#define GT(ev) (sw.trace ? (void)(sw.trace[blockIdx.x * 8 + (ev)] = sm100::global_timer_ns()) : (void)0)
 #else
 #define GT(ev) ((void)0)
 #endif
@@ -368,8 +367,18 @@ __device__ __forceinline__ void epilogue32(const uint32_t (&v)[32], int row, int
 __device__ __forceinline__ float norm_row_scale(const NormArgs& na, int row, int M) {
   if (na.ssq_in == nullptr || row >= M) return 1.0f;
   const float* p = na.ssq_in + (int64_t)row * na.parts_in;
+  const int parts = na.parts_in;
   float s = 0.0f;
-  for (int t = 0; t < na.parts_in; ++t) s += p[t];
+  int t = 0;
+  if ((parts & 3) == 0 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+    // 16-byte loads, several in flight; the sum stays sequential in t
+#pragma unroll 4
+    for (; t < parts; t += 4) {
+      const float4 q = *reinterpret_cast<const float4*>(p + t);
+      s += q.x; s += q.y; s += q.z; s += q.w;
+    }
+  }
+  for (; t < parts; ++t) s += p[t];
   return rsqrtf(s / na.hdim + na.eps);
 }
 
@@ -403,7 +412,9 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int M = live_rows(M_cap, m_live);
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KB-aligned by pointer arithmetic on the __shared__ array (an integer
+  // round trip would make every derived access generic)
+  uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
@@ -603,6 +614,19 @@ __device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, uint32_t* v) {
 // v holds K range 0's accumulator chunk (loaded, waited); add ranges
 // 1..splits-1 in order -- the same left fold swap_gemm applies to its fp32
 // partials, so both modes round identically.
+// one range per TMEM round trip (register-lean: the residual path keeps its
+// whole residual slice in registers)
+template <int CW>
+__device__ __forceinline__ void add_splits1(uint32_t taddr, int splits, int stride, uint32_t* v) {
+  for (int r = 1; r < splits; ++r) {
+    uint32_t t[CW];
+    tmem_ld_chunk<CW>(taddr + (uint32_t)(r * stride), t);
+    sm100::tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < CW; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) + __uint_as_float(t[i]));
+  }
+}
+
 template <int CW>
 __device__ __forceinline__ void add_splits(uint32_t taddr, int splits, int stride, uint32_t* v) {
   for (int r = 1; r < splits; r += 2) {  // two ranges per TMEM round trip
@@ -633,17 +657,55 @@ __device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;"
 // row's 32 consecutive columns (coalesced).  The arithmetic and rounding are
 // those of the row-major chunk epilogues (epilogue_chunk, qkv_rope_chunk,
 // the kSsqCols partial form), so both GEMM modes write identical bits.
+// Cross-lane data (a row's scale / RoPE destination, SwiGLU and RoPE
+// partners, the norm partial over the warp's 32 columns) goes through the
+// warp's shared scratch, not shuffles: swap_gemm is not inlined, and a
+// shuffle in a function the compiler cannot prove converged is wrapped in
+// a slow collective sequence.
+// One lane's token row inputs for the small-M epilogue (loaded before the
+// accumulator is ready): RMSNorm row scale, RoPE position / KV destination.
+struct SwapRow {
+  float rs = 1.0f;
+  int info = -1, pos = 0;
+  long long dst = 0;
+};
+
+template <int EPI>
+__device__ __forceinline__ SwapRow swap_row(const NormArgs& na, const RopeArgs& ra, int row, int M) {
+  SwapRow r;
+  if (na.ssq_in != nullptr) r.rs = norm_row_scale(na, row, M);
+  if constexpr (EPI == kEpiQkvRope) {
+    const RopeRow rr = rope_row(ra, row, M);
+    r.info = rr.info;
+    r.pos = rr.info >= 0 ? rr.pos : 0;  // padding rows: any valid table row
+    r.dst = rr.dst;
+  }
+  return r;
+}
+
+struct SwapScratch {
+  float t[32 * 33];      // [token][column] (+1 pad)
+  float rs[32];          // per token: RMSNorm row scale
+  int info[32], pos[32];
+  long long dst[32];
+};
+
 template <int EPI>
 __device__ __forceinline__ void swap_epilogue(uint32_t (&v)[32], int row0, int col0, int lane, int M, int N,
-                                              void* C, int ldc, const float* __restrict__ bias, const NormArgs& na,
-                                              const RopeArgs& ra, int parts, int quad, float* red) {
+                                              void* C, int ldc, const float* __restrict__ bias, const NormArgs na,
+                                              const RopeArgs ra, int parts, int quad, float* red,
+                                              SwapScratch& xs, const SwapRow& me, const float* res_pre) {
+  // (the argument structs are copies: their fields stay in registers across
+  // the global stores below instead of being reloaded behind each store)
   const int n = col0 + lane;
   const bool col_ok = n < N;
-  const int my_row = row0 + lane;  // per-row inputs are loaded by lane, broadcast per token
+  const int my_row = row0 + lane;  // per-row inputs are loaded by lane, read back per token
   if (na.ssq_in != nullptr) {
-    const float r = norm_row_scale(na, my_row, M);
+    xs.rs[lane] = me.rs;
+    __syncwarp();
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * __shfl_sync(0xffffffffu, r, i));
+    for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * xs.rs[i]);
+    __syncwarp();
   }
   const float b = (bias != nullptr && col_ok) ? bias[n] : 0.0f;
   if constexpr (EPI == kEpiStoreF32 || EPI == kEpiStoreBf16) {
@@ -661,8 +723,13 @@ __device__ __forceinline__ void swap_epilogue(uint32_t (&v)[32], int row0, int c
     float res[32];
     const int nl = col_ok ? n : N - 1;
     float* cbase = reinterpret_cast<float*>(C) + nl;
+    if (res_pre != nullptr) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) res[i] = cbase[(int64_t)(row0 + i < M ? row0 + i : M - 1) * ldc];
+      for (int i = 0; i < 32; ++i) res[i] = res_pre[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) res[i] = cbase[(int64_t)(row0 + i < M ? row0 + i : M - 1) * ldc];
+    }
     if constexpr (EPI == kEpiResidualF32) {
 #pragma unroll
       for (int i = 0; i < 32; ++i)
@@ -670,47 +737,65 @@ __device__ __forceinline__ void swap_epilogue(uint32_t (&v)[32], int row0, int c
       return;
     }
     const float wn = col_ok ? na.w[n] : 0.0f;
-    const int qb = lane & ~3;
+    __nv_bfloat16* const hbase = na.h_out + n;
+    const int64_t ld_h = na.ld_h;
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      const bool row_ok = row0 + i < M;  // warp-uniform
       float a = 0.0f;
-      if (row_ok && col_ok) {
+      if (row0 + i < M && col_ok) {
         a = res[i] + __uint_as_float(v[i]);
         cbase[(int64_t)(row0 + i) * ldc] = a;
-        na.h_out[(int64_t)(row0 + i) * na.ld_h + n] = __float2bfloat16_rn(a * wn);
+        hbase[(int64_t)(row0 + i) * ld_h] = __float2bfloat16_rn(a * wn);
       }
-      // kSsqCols partial of (row, chunk col0): quad fma chains, then the tree
-      const float a0 = __shfl_sync(0xffffffffu, a, qb), a1 = __shfl_sync(0xffffffffu, a, qb + 1);
-      const float a2 = __shfl_sync(0xffffffffu, a, qb + 2), a3 = __shfl_sync(0xffffffffu, a, qb + 3);
-      float sq = quad_ssq(make_float4(a0, a1, a2, a3));
-      sq += __shfl_xor_sync(0xffffffffu, sq, 4);
-      sq += __shfl_xor_sync(0xffffffffu, sq, 8);
-      sq += __shfl_xor_sync(0xffffffffu, sq, 16);
-      if (lane == 0) red[quad * 32 + i] = sq;  // this warp's chunk of the CTA's 128-column group
+      xs.t[i * 33 + lane] = a;
     }
+    __syncwarp();
+    // lane = token: this warp's 32-column chunk partial in the kSsqCols form
+    {
+      const float* tr = xs.t + lane * 33;
+      float sq[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sq[q] = quad_ssq(make_float4(tr[4 * q], tr[4 * q + 1], tr[4 * q + 2], tr[4 * q + 3]));
+      red[quad * 32 + lane] = tree8(sq);
+    }
+    __syncwarp();
     // the group (this CTA's 128 columns = 4 warps' chunks) in column order
     epi_bar_sync();
     if (quad == 0) {
+      float* const ssq_out = na.ssq_out;
       const float gsum = ((red[lane] + red[32 + lane]) + red[64 + lane]) + red[96 + lane];
-      if (row0 + lane < M && col0 < N) na.ssq_out[(int64_t)(row0 + lane) * parts + col0 / kSsqCols] = gsum;
+      if (row0 + lane < M && col0 < N) ssq_out[(int64_t)(row0 + lane) * parts + col0 / kSsqCols] = gsum;
     }
     epi_bar_sync();
   } else if constexpr (EPI == kEpiSwiGLU) {
     // the warp's 32 columns are one interleave block: lanes 0-15 gate, 16-31 up
     const bool ok = col0 + 32 <= N;  // N % 32 == 0 (plan)
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float x = __uint_as_float(v[i]);
-      const float up = __shfl_down_sync(0xffffffffu, x, 16);
-      if (lane < 16 && ok && row0 + i < M)
-        reinterpret_cast<__nv_bfloat16*>(C)[(int64_t)(row0 + i) * ldc + col0 / 2 + lane] =
-            __float2bfloat16_rn(silu(x) * up);
+    for (int i = 0; i < 32; ++i) xs.t[i * 33 + lane] = __uint_as_float(v[i]);
+    __syncwarp();
+    if (lane < 16 && ok) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (row0 + i < M)
+          reinterpret_cast<__nv_bfloat16*>(C)[(int64_t)(row0 + i) * ldc + col0 / 2 + lane] =
+              __float2bfloat16_rn(silu(__uint_as_float(v[i])) * xs.t[i * 33 + lane + 16]);
     }
+    __syncwarp();
   } else if constexpr (EPI == kEpiQkvRope) {
     const int hd = ra.hd, half = hd >> 1;
-    const int hq = ra.nq * hd, hk = ra.nkv * hd;
-    RopeRow rr = rope_row(ra, my_row, M);
+    const int nq = ra.nq, nkv = ra.nkv, page = ra.page, window_max = ra.window_max;
+    const int hq = nq * hd, hk = nkv * hd;
+    __nv_bfloat16* const q_out = ra.q_out;
+    __nv_bfloat16* const cache = ra.cache;
+    __nv_bfloat16* const window = ra.window;
+    const float* const cos_t = ra.cos;
+    const float* const sin_t = ra.sin;
+    xs.info[lane] = me.info;
+    xs.pos[lane] = me.pos;
+    xs.dst[lane] = me.dst;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) xs.t[i * 33 + lane] = __uint_as_float(v[i]) + b;
+    __syncwarp();
     const int pidx = (col0 % hd) / 2 + (lane >> 1);  // rotation pair of this column (q / k)
     const bool odd = lane & 1;
     const bool rot = col0 < hq + hk;
@@ -719,40 +804,37 @@ __device__ __forceinline__ void swap_epilogue(uint32_t (&v)[32], int row0, int c
     if (rot) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const int info = __shfl_sync(0xffffffffu, rr.info, i);
-        const int pos = info >= 0 ? __shfl_sync(0xffffffffu, rr.pos, i) : 0;  // padding rows: any valid row
-        cs[i] = ra.cos[(int64_t)pos * half + pidx];
-        sn_[i] = ra.sin[(int64_t)pos * half + pidx];
+        cs[i] = cos_t[(int64_t)xs.pos[i] * half + pidx];
+        sn_[i] = sin_t[(int64_t)xs.pos[i] * half + pidx];
       }
     }
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      const int info = __shfl_sync(0xffffffffu, rr.info, i);
-      const long long dst = __shfl_sync(0xffffffffu, (long long)rr.dst, i);
-      const float x = __uint_as_float(v[i]) + b;
-      const float xp = __shfl_xor_sync(0xffffffffu, x, 1);  // the pair partner
-      if (info < 0 || row0 + i >= M || !col_ok) continue;    // padding row of the verify batch
+      const int info = xs.info[i];
+      if (info < 0 || row0 + i >= M || !col_ok) continue;  // padding row of the verify batch
+      const float x = xs.t[i * 33 + lane];
       const bool win = (info >> 16) & 1;
       const int slot = info & 0xFFFF;
-      const int rows = win ? ra.window_max : ra.page;
-      __nv_bfloat16* kbase = (win ? ra.window : ra.cache) + dst;
+      const int rows = win ? window_max : page;
+      __nv_bfloat16* kbase = (win ? window : cache) + xs.dst[i];
       if (rot) {
-        const float c = cs[i], sn = sn_[i];
+        const float xp = xs.t[i * 33 + (lane ^ 1)];  // the pair partner
         const float x1 = odd ? xp : x, x2 = odd ? x : xp;
-        const float y = odd ? rope_y2(x1, x2, c, sn) : rope_y1(x1, x2, c, sn);
+        const float y = odd ? rope_y2(x1, x2, cs[i], sn_[i]) : rope_y1(x1, x2, cs[i], sn_[i]);
         const int dim = pidx + (odd ? half : 0);
         if (col0 < hq) {
-          ra.q_out[((int64_t)(row0 + i) * ra.nq + col0 / hd) * hd + dim] = __float2bfloat16_rn(y);
+          q_out[((int64_t)(row0 + i) * nq + col0 / hd) * hd + dim] = __float2bfloat16_rn(y);
         } else {
           __nv_bfloat16* k = kbase + (int64_t)((col0 - hq) / hd) * rows * hd;
           k[kv_elem(slot, dim, hd)] = __float2bfloat16_rn(y);
         }
       } else {
         const int vc = n - hq - hk;
-        __nv_bfloat16* vb = kbase + (int64_t)ra.nkv * rows * hd + (int64_t)(vc / hd) * rows * hd;
+        __nv_bfloat16* vb = kbase + (int64_t)nkv * rows * hd + (int64_t)(vc / hd) * rows * hd;
         vb[kv_elem(slot, vc % hd, hd)] = __float2bfloat16_rn(x);
       }
     }
+    __syncwarp();
   }
 }
 
@@ -767,9 +849,11 @@ __device__ __forceinline__ void swap_epilogue(uint32_t (&v)[32], int row0, int c
 // pair mode.  With splits > 1 each unit stores its fp32 partial; the last
 // of a tile's `splits` units (arrival counter) sums them in range order.
 template <int EPI>
-__device__ __noinline__ void swap_gemm(uint8_t* smem, uint32_t ring_bytes, const SwapArgs& sw, int M, int N, int K,
-                                       void* C, int ldc, const float* __restrict__ bias, const NormArgs& na,
-                                       const RopeArgs& ra) {
+__device__ __forceinline__ void swap_gemm(uint32_t ring_bytes, const SwapArgs sw, int M, int N, int K, void* C,
+                                          int ldc, const float* __restrict__ bias, const NormArgs na,
+                                          const RopeArgs ra) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int KC = 2;
   constexpr int kMaxStages = 12;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -789,8 +873,12 @@ __device__ __noinline__ void swap_gemm(uint8_t* smem, uint32_t ring_bytes, const
   const CUtensorMap* xmap = &sw.maps->x[(nth >> 4) - 1];
   const uint32_t wbytes = KC * 16384u, xbytes = KC * (uint32_t)nth * 128u, stage_bytes = wbytes + xbytes;
   // the last KB of the ring: the norm-group reduction scratch [4 warps][32 rows]
-  float* red = reinterpret_cast<float*>(smem + ring_bytes - 1024);
-  int nst = (int)((ring_bytes - 1024) / stage_bytes);
+  // ring tail: the norm-group scratch [4 warps][32 rows] and the epilogue
+  // warps' exchange scratch
+  constexpr uint32_t kScratch = (1024 + 4 * sizeof(SwapScratch) + 1023) & ~1023u;
+  float* red = reinterpret_cast<float*>(smem + ring_bytes - kScratch);
+  SwapScratch* xsc = reinterpret_cast<SwapScratch*>(smem + ring_bytes - kScratch + 1024);
+  int nst = (int)((ring_bytes - kScratch) / stage_bytes);
   nst = nst < kMaxStages ? nst : kMaxStages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ring_bytes);
   uint64_t* empty = full + kMaxStages;
@@ -896,14 +984,28 @@ __device__ __noinline__ void swap_gemm(uint8_t* smem, uint32_t ring_bytes, const
     const int groups = NT >> 5;
     int acc = 0;
     uint32_t acc_phase = 0;
+    SwapRow rows[4];       // this lane's token in each 32-token group
+    float res0[32];        // residual epilogues: group 0's residual rows
+    bool have_res0 = false;
     auto finish = [&](uint32_t (&v)[32], int g, int col0) {
-      swap_epilogue<EPI>(v, g * 32, col0, lane, M, N, C, ldc, bias, na, ra, parts, quad, red);
+      swap_epilogue<EPI>(v, g * 32, col0, lane, M, N, C, ldc, bias, na, ra, parts, quad, red, xsc[quad],
+                         rows[g], g == 0 && have_res0 ? res0 : nullptr);
     };
     for (int u = pair; u < units; u += npairs) {
       const int tile = u / splits, range = u - tile * splits;
       const int col0 = tile * 256 + (int)rank * 128 + quad * 32;  // this warp's 32 output columns
       const int n = col0 + lane;                                   // this lane's column
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * 128;
+      // row inputs and group 0's residual while the mainloop runs
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        if (g < groups) rows[g] = swap_row<EPI>(na, ra, g * 32 + lane, M);
+      if constexpr (EPI == kEpiResidualF32 || EPI == kEpiResidualNorm) {
+        const float* cb = reinterpret_cast<const float*>(C) + (n < N ? n : N - 1);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) res0[i] = cb[(int64_t)(i < M ? i : M - 1) * ldc];
+        have_res0 = true;
+      }
       sm100::mbar_wait(&tfull[acc], acc_phase);
       sm100::tc_fence_after();
       if (warp == 2 && lane == 0 && u == pair) GT(3);
@@ -1005,8 +1107,8 @@ __device__ __noinline__ void swap_gemm(uint8_t* smem, uint32_t ring_bytes, const
 // traffic halves, the bound of the small-N verify GEMMs (o, down, qkv).  A
 // stage is reusable only when both pairs' MMAs have drained it, so the
 // leaders' commits are multicast to all four CTAs' empty barriers (count 2).
-// XM: the plan splits K into ranges and/or may run the small-M mode; plain
-// pair plans (XM false) compile neither path (fewer registers, leaner loops).
+// XM: the plan splits K into ranges (one TMEM accumulator per range, summed
+// in order); plain plans (XM false) compile none of it.
 template <int BN, int EPI, int MC, int KC, bool XM>
 __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -1019,10 +1121,14 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   constexpr int S = Cfg::kStages;
   constexpr int CW = Cfg::kChunk;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  if constexpr (XM && kSwapEpi<EPI> && KC == 2) {
-    if (sw.max_m > 0 && M >= 1 && M <= sw.max_m) {  // grid-uniform: small-M mode
-      swap_gemm<EPI>(smem, (uint32_t)(S * Cfg::kStageBytes), sw, M, N, K, C, ldc, bias, na, ra);
+  // 1 KB-aligned by pointer arithmetic on the __shared__ array (an integer
+  // round trip would make every derived access generic)
+  uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
+  if constexpr (kSwapEpi<EPI>) {
+    // dual launch (SwapArgs flags bit 1): the small-M kernel launched beside
+    // this one computes live row counts <= max_m; exit after the wait
+    if ((sw.flags & 2) && M >= 1 && M <= sw.max_m) {
+      grid_dep_sync();
       return;
     }
   }
@@ -1214,7 +1320,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           uint32_t v[CW];
           tmem_ld_chunk<CW>(taddr + c * CW, v);
           sm100::tmem_ld_wait();
-          if constexpr (XM) add_splits<CW>(taddr + c * CW, n_split, BN, v);
+          if constexpr (XM) add_splits1<CW>(taddr + c * CW, n_split, BN, v);
           const int col = n_blk * BN + c * CW;
           if constexpr (kStagedEpi<BN, EPI, KC>) {
             if (n_blk * BN + BN <= N) {  // warp-uniform: full-width tile
@@ -1467,6 +1573,41 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   }
 }
 
+// Small-M mode as its own kernel (SwapArgs): launched alone when the host
+// knows the launch carries <= max_m rows, or beside the pair kernel (dual
+// launch) when only the device knows the live row count; each exits after
+// griddepcontrol.wait when the other one owns the launch.
+constexpr uint32_t kSwapRing = 200 * 1024;
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+gemm_swap_kernel(int M_cap, const int32_t* __restrict__ m_live, int N, int K, void* C, int ldc,
+                 const float* __restrict__ bias, NormArgs na, RopeArgs ra, SwapArgs sw) {
+  const int M = live_rows(M_cap, m_live);
+  if (!(M >= 1 && M <= sw.max_m)) {
+    grid_dep_sync();
+    return;
+  }
+  swap_gemm<EPI>(kSwapRing, sw, M, N, K, C, ldc, bias, na, ra);
+}
+
+template <int EPI>
+int launch_swap_typed(const GemmPlan& p, int M, cudaStream_t stream) {
+  auto kern = gemm_swap_kernel<EPI>;
+  constexpr size_t smem = 1024 + kSwapRing + 256;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SR_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  const int units = ((p.N + 255) / 256) * p.sw.splits;
+  const int slots = num_sms() / 2;
+  const int pairs = units < slots ? units : slots;
+  sr::launch_k(kern, 2 * pairs, kThreads, smem, stream, M, p.m_live, p.N, p.K, p.c, p.ldc, p.bias, p.norm, p.rope,
+               p.sw);
+  return check_launch("gemm_swap_kernel");
+}
+
 template <int BN, int EPI, int MC, int KC, bool XM>
 int launch_pair_mc(const GemmPlan& p, int M, cudaStream_t stream) {
   using Cfg = PairCfg<BN, KC>;
@@ -1480,13 +1621,7 @@ int launch_pair_mc(const GemmPlan& p, int M, cudaStream_t stream) {
   }
   const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * (((p.N + BN - 1) / BN + MC - 1) / MC);
   const int slots = num_sms() / (2 * MC);
-  int clusters = tiles < slots ? tiles : slots;
-  if (p.sw.max_m > 0) {  // the same launch may run in small-M mode: cover its units too
-    const int units = ((p.N + 255) / 256) * p.sw.splits;
-    const int cl_sw = (units + MC - 1) / MC;
-    const int want = cl_sw < slots ? cl_sw : slots;
-    if (want > clusters) clusters = want;
-  }
+  const int clusters = tiles < slots ? tiles : slots;
   sr::launch_k(kern, 2 * MC * clusters, kThreads, smem, stream, p.a, p.b, M, p.m_live, p.N, p.K, p.c, p.ldc,
                p.bias, p.aux, p.sample, p.norm, p.rope, p.sw);
   return check_launch("gemm_pair_kernel");
@@ -1494,7 +1629,7 @@ int launch_pair_mc(const GemmPlan& p, int M, cudaStream_t stream) {
 
 template <int BN, int EPI>
 int launch_pair_typed(const GemmPlan& p, int M, cudaStream_t stream) {
-  const bool xm = p.sw.splits > 1 || p.sw.max_m > 0;
+  const bool xm = p.sw.splits > 1;
   if constexpr (kSwapEpi<EPI>) {
     if (xm) {  // K ranges / small-M mode: KC 2 only (gemm_bf16_plan)
       if (p.kc != 2) return config_error("K-range / small-M GEMM plans need 128-k stages");
@@ -1533,7 +1668,8 @@ int launch_pair_bn(const GemmPlan& p, int M, cudaStream_t stream) {
 
 }  // namespace
 
-// one per tile width (gemm_pair_bn<BN>.cu)
+// one per tile width (gemm_pair_bn<BN>.cu); the small-M kernels (gemm_swap.cu)
+int launch_swap(const GemmPlan& p, int M, cudaStream_t stream);
 int launch_pair_bn64(const GemmPlan& p, int M, cudaStream_t stream);
 int launch_pair_bn96(const GemmPlan& p, int M, cudaStream_t stream);
 int launch_pair_bn112(const GemmPlan& p, int M, cudaStream_t stream);

@@ -105,3 +105,24 @@ if __name__ == "__main__":
         B = int(sys.argv[3]) if len(sys.argv) > 3 else 32
         step, keep = decode_graph(name, B)
         timeline(step)
+    if what == "trace":  # SR_LIB_PATH=scripts/_trace/libspecrollout_b200_trace.so: last small-M GEMM of a decode step
+        import ctypes
+
+        from paper_2511_16193_b200 import _native
+
+        name = sys.argv[2] if len(sys.argv) > 2 else "qwen2.5-1.5b"
+        B = int(sys.argv[3]) if len(sys.argv) > 3 else 32
+        step, keep = decode_graph(name, B)
+        lib = _native.lib()
+        step()
+        torch.cuda.synchronize()
+        lib.sr_debug_gemm_trace(None, 0)
+        step()
+        torch.cuda.synchronize()
+        buf = (ctypes.c_ulonglong * (1024 * 8))()
+        lib.sr_debug_gemm_trace(buf, 1024 * 8)
+        names = ["entry", "wait", "stage0", "acc", "counter", "epi", "exit", "g0"]
+        rows = [(b, [buf[b * 8 + e] for e in range(8)]) for b in range(1024) if buf[b * 8]]
+        t0 = min(ev[0] for _, ev in rows)
+        for b, ev in rows[:64]:
+            print(f"cta {b:4d} " + " ".join(f"{n}={(x - t0) / 1e3:6.2f}" if x else f"{n}=   -  " for n, x in zip(names, ev)))
