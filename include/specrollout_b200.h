@@ -245,6 +245,11 @@ int sr_paged_attention(int dtype, const void* q, const void* seqs, int num_seqs,
  * keep it fixed for a model so verify and decode stay bit-identical. */
 int sr_set_attention_split(int tiles);
 
+/* K2 kernel for head_dim 128: 0 = mma.sync (default), 1 = tcgen05/TMEM
+ * (attn_tc_kernel).  Part of the numerics like the split size: set it once
+ * per process, before any forward. */
+int sr_set_attention_tc(int on);
+
 uint64_t sr_model_workspace_bytes(const sr_model_desc* desc);
 int sr_model_create(const sr_model_desc* desc, void** handle);
 int sr_model_destroy(void* handle);

@@ -38,6 +38,7 @@ SIGNATURES: dict[str, list] = {
     "sr_paged_attention": [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _i32,
                            _vp, _i32, _vp, _i32, _i32, _vp, ctypes.c_uint64, _vp, _vp],
     "sr_set_attention_split": [_i32],
+    "sr_set_attention_tc": [_i32],
     "sr_sample_rows": [_vp, _i32, _i32, _i32, _vp, _vp, ctypes.c_uint32, ctypes.c_float, _vp, _vp],
     "sr_model_workspace_bytes": [_vp],
     "sr_model_create": [_vp, _vp],

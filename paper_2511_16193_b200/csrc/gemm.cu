@@ -249,6 +249,32 @@ int make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t K, uint64_t r
   return SR_OK;
 }
 
+// bf16 paged KV cache [blocks][64 slots][128 head dims] (blocks = layers x
+// pages x K/V x kv heads; rows already XOR-swizzled by slot in HBM) viewed as
+// (64 dims, slot in group, head-dim half, 8-slot group, block): one box
+// (64, 8, 2, 8, 1) is a whole page landing as [group][half][8 slots][128 B]
+// -- 1 KB SWIZZLE_128B atoms, K chunk (half) stride 1 KB, 8-row group stride
+// 2 KB -- so the copy itself must not swizzle again.
+int make_tmap_kv_pages(CUtensorMap* map, const void* cache, uint64_t blocks) {
+  auto enc = tmap_encoder();
+  if (enc == nullptr) {
+    set_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
+    return SR_ERR_RUNTIME;
+  }
+  cuuint64_t dims[5] = {64, 8, 2, 8, blocks};
+  cuuint64_t strides[4] = {256, 128, 8 * 256, 64 * 256};
+  cuuint32_t box[5] = {64, 8, 2, 8, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(cache), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (kv pages) failed (%d): blocks=%llu", (int)r, (unsigned long long)blocks);
+    return SR_ERR_CONFIG;
+  }
+  return SR_OK;
+}
+
 int gemm_bf16_plan(GemmPlan* p, int M, int N, int K, const __nv_bfloat16* A, int lda,
                    const __nv_bfloat16* W, int ldw, void* C, int ldc, int epi,
                    const float* bias, int bn, int32_t* aux) {

@@ -65,6 +65,7 @@ struct NormArgs {
 };
 
 // Host: encode a 2D bf16 tensor map (inner dim contiguous) with 128B swizzle.
+int make_tmap_kv_pages(CUtensorMap* map, const void* cache, uint64_t blocks);
 int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                    uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer);
 

@@ -83,6 +83,19 @@ def reference(case, ctx, q_len, nq, nkv, hd, dtype):
     return torch.cat(outs)
 
 
+@pytest.fixture(params=["mma_sync", "tcgen05"], autouse=True)
+def attention_kernel(request):
+    """Every case runs on both head_dim-128 kernels (mma.sync default and
+    the tcgen05/TMEM kernel); SR_ATTN_TC_GRID (set by the harness) caps the
+    tcgen05 grid so CTAs chain several items."""
+    from paper_2511_16193_b200 import _native
+
+    lib = _native.lib()
+    _native.check(lib.sr_set_attention_tc(1 if request.param == "tcgen05" else 0), "kernel")
+    yield request.param
+    _native.check(lib.sr_set_attention_tc(0), "kernel")
+
+
 def run_gpu(case, ctx, q_len, nq, nkv, hd, dtype, branches=None, split=32):
     from paper_2511_16193_b200 import _native
 
@@ -117,6 +130,9 @@ CASES = [
     ([0, 5, 63, 64, 65, 200], [1, 2, 5, 5, 3, 4], 12, 2, 128),     # page edges, short
     ([2040, 2047, 2048, 4100, 9000], [5, 1, 5, 3, 2], 12, 2, 128),  # 1..5 KV splits -> combine
     ([130, 777, 3000], [5, 5, 5], 14, 2, 64),                        # head_dim 64, G = 7
+    ([0, 0, 300], [100, 1, 64], 12, 2, 128),                          # prefill: 32-row blocks across tokens
+    ([500, 1500, 2100], [5, 5, 5], 28, 4, 128),                       # 7B shape: G = 7, two row blocks
+    ([64, 1000, 4095], [5, 5, 5], 40, 8, 128),                        # 32B shape: G = 5
 ]
 
 
@@ -154,3 +170,29 @@ def test_attention_verify_window_equals_single_decode_bit_exact():
             one = dict(case, Q=[case["Q"][0][j:j + 1]])
             single = run_gpu(one, [ctx0 + j], [1], nq, nkv, hd, torch.bfloat16)
             assert torch.equal(single[0], full[j]), (ctx0, j)
+
+
+@pytest.mark.parametrize("split", [4, 6, 5])
+def test_attention_split_sizes(split):
+    """Non-default split sizes: even sizes keep the tcgen05 kernel's 128-key
+    blocks split aligned, odd sizes fall back to the mma.sync kernel."""
+    ctx, q_len, nq, nkv, hd = [300, 900, 1700], [5, 3, 5], 12, 2, 128
+    case = build_case(4, 3, ctx, q_len, nq, nkv, hd, torch.bfloat16)
+    got = run_gpu(case, ctx, q_len, nq, nkv, hd, torch.bfloat16, split=split).double()
+    exp = reference(case, ctx, q_len, nq, nkv, hd, torch.bfloat16)
+    torch.testing.assert_close(got, exp, rtol=1e-2, atol=1e-2)
+
+
+def test_attention_tcgen05_items_chained_per_cta(monkeypatch, attention_kernel):
+    """Three CTAs for ~90 work items: every CTA chains many items through its
+    pipelines (item ring, Q buffers, S/O slots, end-of-work sentinel)."""
+    if attention_kernel != "tcgen05":
+        pytest.skip("grid cap applies to the tcgen05 kernel")
+    monkeypatch.setenv("SR_ATTN_TC_GRID", "3")
+    ctx = [0, 5, 63, 64, 65, 200, 700, 1500, 2047, 2100, 3000, 90, 128, 129, 333]
+    q_len = [1, 2, 5, 5, 3, 4, 5, 5, 1, 5, 2, 5, 5, 1, 4]
+    nq, nkv, hd = 12, 2, 128
+    case = build_case(5, len(ctx), ctx, q_len, nq, nkv, hd, torch.bfloat16)
+    got = run_gpu(case, ctx, q_len, nq, nkv, hd, torch.bfloat16).double()
+    exp = reference(case, ctx, q_len, nq, nkv, hd, torch.bfloat16)
+    torch.testing.assert_close(got, exp, rtol=1e-2, atol=1e-2)
