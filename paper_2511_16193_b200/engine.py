@@ -52,11 +52,11 @@ class SyntheticDrafter:
     name = "synthetic"
 
     def __init__(self, truth: list[list[int]], requests, method: str, seed: int, device="cuda",
-                 vocab: int = 0):
+                 vocab: int = 0, capacity: int = 0):
         from .verify import CHUNK, entropy_words, keyed_fill
 
         B = len(truth)
-        L = max(len(t) for t in truth)
+        L = max(max(len(t) for t in truth), capacity)  # capacity: rows for adopted requests
         chunks = max(1, math.ceil(L / CHUNK))
         self.stride = chunks * CHUNK
         tt = np.zeros((B, self.stride), dtype=np.int32)
@@ -207,7 +207,8 @@ class RolloutEngine:
 
     def __init__(self, target: DeviceModel, prompts: list[np.ndarray], max_new: list[int], *, k: int = 4,
                  drafters: tuple = (NgramDrafter(),), bonus_token: bool = False, history: int = 0,
-                 temperature: float = 0.0, seed: int = 0, acceptance: str = "exact", compact: bool = True):
+                 temperature: float = 0.0, seed: int = 0, acceptance: str = "exact", compact: bool = True,
+                 capacity: int = 0):
         if not prompts:
             raise ConfigError("empty batch")
         if len(prompts) != len(max_new):
@@ -245,7 +246,9 @@ class RolloutEngine:
         if self.B * self.N > target.max_seqs or self.B * self.N * (k + 1) > target.max_tokens:
             raise ConfigError("batch exceeds the model's max_seqs / max_tokens")
         lens = [len(p) for p in prompts]
-        need = max(l + n for l, n in zip(lens, max_new)) + k + 2
+        # capacity: positions per slot beyond this batch's own needs (a rank
+        # that adopts migrated stragglers sizes its slots for the whole job)
+        need = max(max(l + n for l, n in zip(lens, max_new)), capacity) + k + 2
         if need > target.max_len:
             raise ConfigError(f"prompt + generation ({need}) exceeds model max_len {target.max_len}")
         self.stride = int(math.ceil(need / 16) * 16)

@@ -37,17 +37,31 @@ def _check_compatible(src, dst) -> None:
         raise ConfigError("migration needs the same window k")
 
 
+def _synthetic(eng) -> list:
+    from .engine import SyntheticDrafter
+
+    return [d for d in eng.drafters if isinstance(d, SyntheticDrafter)]
+
+
 def pack_request(eng, b: int) -> dict:
-    """Gather request ``b``'s state into contiguous device tensors."""
+    """Gather request ``b``'s state into contiguous device tensors.  A
+    reference-acceptance (synthetic) drafter's per-slot rows -- the request's
+    target continuation, its keyed accept uniforms and latent rate -- travel
+    with it, so the request keeps drafting under the same law."""
     n = _pages(eng, b)
     pages = eng.m.block_table[b, :n].long()
     L = int(eng.seq_len[b])
-    return {
+    st = {
         "lens": torch.stack([eng.seq_len[b], eng.gen_len[b], eng.max_new[b],
                              torch.tensor(n, dtype=torch.int32, device=eng.dev)]).to(torch.int32),
         "tokens": eng.tokens[b, :L].clone(),
         "kv": eng.m.kv_cache[:, pages].contiguous(),   # [layers, n, 2, kv_heads, 64, hd]
     }
+    for i, d in enumerate(_synthetic(eng)):
+        st[f"syn{i}_truth"] = d.truth[b].clone()
+        st[f"syn{i}_u"] = d.uniforms[b].clone()
+        st[f"syn{i}_meta"] = torch.stack([d.p[b], d.truth_len[b].to(torch.float64)])
+    return st
 
 
 def _check_room(eng, seq_len: int, gen_len: int, max_new: int, n: int) -> None:
@@ -72,9 +86,13 @@ def unpack_request(eng, b: int, st: dict) -> None:
 
     seq_len, gen_len, max_new, n = (int(x) for x in st["lens"].tolist())
     _check_room(eng, seq_len, gen_len, max_new, n)
-    if any(isinstance(d, SyntheticDrafter) for d in eng.drafters):
-        raise ConfigError("engines with a synthetic drafter hold per-slot truth rows; migrate into an "
-                          "engine with n-gram or model drafters")
+    syn = _synthetic(eng)
+    for i, d in enumerate(syn):
+        if f"syn{i}_truth" not in st:
+            raise ConfigError("engines with a synthetic drafter hold per-slot truth rows; the migrated "
+                              "request must bring its own (from an engine with the same drafters)")
+        if st[f"syn{i}_truth"].numel() > d.truth.shape[1]:
+            raise ConfigError("destination synthetic drafter rows are shorter than the request's")
     eng.tokens[b, :seq_len].copy_(st["tokens"][:seq_len])
     eng.seq_len[b] = seq_len
     eng.gen_len[b] = gen_len
@@ -87,6 +105,15 @@ def unpack_request(eng, b: int, st: dict) -> None:
     for d in eng.drafters:
         if isinstance(d, ModelDrafter) and d.eng is eng:
             d.reset_slot(b)
+    for i, d in enumerate(syn):
+        t, u = st[f"syn{i}_truth"], st[f"syn{i}_u"]
+        d.truth[b].zero_()
+        d.truth[b, : t.numel()].copy_(t)
+        d.uniforms[b].zero_()
+        d.uniforms[b, : u.numel()].copy_(u)
+        meta = st[f"syn{i}_meta"].to(d.p.device)
+        d.p[b] = meta[0]
+        d.truth_len[b] = meta[1].to(torch.int32)
 
 
 def migrate_local(src, b_src: int, dst, b_dst: int) -> int:
@@ -102,44 +129,67 @@ def migrate_local(src, b_src: int, dst, b_dst: int) -> int:
     return sum(v.numel() * v.element_size() for v in st.values())
 
 
+def _host_staged(dist) -> bool:
+    """gloo (CPU tests, one-GPU multi-process runs) moves host tensors only."""
+    return dist.get_backend() == "gloo"
+
+
+def _p2p(dist, kind: str, tensors: list, peer: int) -> None:
+    """Post one batch of sends or receives to ``peer`` and wait for it."""
+    fn = dist.isend if kind == "send" else dist.irecv
+    ops = [dist.P2POp(fn, t, peer) for t in tensors if t.numel()]
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
 def send_requests(dist, eng, bs: list[int], peer: int) -> int:
-    """NCCL P2P: ship requests ``bs`` to rank ``peer`` (which calls
-    :func:`recv_requests` with the same count) as three messages -- a meta
-    table, all token rows, all KV pages -- and retire them here.  Returns the
-    bytes sent."""
+    """P2P (NCCL over NVLink, or host-staged gloo): ship requests ``bs`` to
+    rank ``peer`` (which calls :func:`recv_requests` with the same count) as
+    a meta table, then all token rows, all KV pages and any synthetic drafter
+    rows in one batch; retire them here.  Returns the bytes sent."""
     sts = [pack_request(eng, b) for b in bs]
     meta = torch.stack([st["lens"] for st in sts])
-    toks = torch.cat([st["tokens"] for st in sts])
-    kv = torch.cat([st["kv"] for st in sts], 1)
+    payload = [torch.cat([st["tokens"] for st in sts]), torch.cat([st["kv"] for st in sts], 1).contiguous()]
+    for i in range(len(_synthetic(eng))):
+        for key in ("truth", "u", "meta"):
+            payload.append(torch.stack([st[f"syn{i}_{key}"] for st in sts]).contiguous())
+    if _host_staged(dist):
+        meta, payload = meta.cpu(), [t.cpu() for t in payload]
     dist.send(meta, peer)
-    ops = [dist.P2POp(dist.isend, toks, peer)]
-    if kv.numel():
-        ops.append(dist.P2POp(dist.isend, kv.contiguous(), peer))
-    for w in dist.batch_isend_irecv(ops):
-        w.wait()
+    _p2p(dist, "send", payload, peer)
     for b in bs:
         eng.retire(b)
-    return meta.numel() * 4 + toks.numel() * 4 + kv.numel() * kv.element_size()
+    return meta.numel() * 4 + sum(t.numel() * t.element_size() for t in payload)
 
 
 def recv_requests(dist, eng, bs: list[int], peer: int) -> None:
-    """NCCL P2P: receive ``len(bs)`` requests from rank ``peer`` into slots ``bs``."""
+    """P2P: receive ``len(bs)`` requests from rank ``peer`` into slots ``bs``."""
     m = eng.m
-    meta = torch.empty((len(bs), 4), dtype=torch.int32, device=eng.dev)
+    dev = "cpu" if _host_staged(dist) else eng.dev
+    meta = torch.empty((len(bs), 4), dtype=torch.int32, device=dev)
     dist.recv(meta, peer)
     lens = meta.tolist()
-    toks = torch.empty(sum(r[0] for r in lens), dtype=torch.int32, device=eng.dev)
+    toks = torch.empty(sum(r[0] for r in lens), dtype=torch.int32, device=dev)
     npages = sum(r[3] for r in lens)
-    kv = torch.empty((m.s.layers, npages) + tuple(m.kv_cache.shape[2:]), dtype=m.kv_cache.dtype,
-                     device=eng.dev)
-    ops = [dist.P2POp(dist.irecv, toks, peer)]
-    if kv.numel():
-        ops.append(dist.P2POp(dist.irecv, kv, peer))
-    for w in dist.batch_isend_irecv(ops):
-        w.wait()
+    kv = torch.empty((m.s.layers, npages) + tuple(m.kv_cache.shape[2:]), dtype=m.kv_cache.dtype, device=dev)
+    payload = [toks, kv]
+    syn = _synthetic(eng)
+    for d in syn:
+        payload += [torch.empty((len(bs), d.truth.shape[1]), dtype=torch.int32, device=dev),
+                    torch.empty((len(bs), d.uniforms.shape[1]), dtype=torch.float64, device=dev),
+                    torch.empty((len(bs), 2), dtype=torch.float64, device=dev)]
+    _p2p(dist, "recv", payload, peer)
+    payload = [t.to(eng.dev) for t in payload]
+    meta = meta.to(eng.dev)
+    toks, kv = payload[0], payload[1]
     t0 = p0 = 0
     for i, b in enumerate(bs):
         seq_len, n = lens[i][0], lens[i][3]
-        unpack_request(eng, b, {"lens": meta[i], "tokens": toks[t0:t0 + seq_len], "kv": kv[:, p0:p0 + n]})
+        st = {"lens": meta[i], "tokens": toks[t0:t0 + seq_len], "kv": kv[:, p0:p0 + n]}
+        for j in range(len(syn)):
+            st[f"syn{j}_truth"], st[f"syn{j}_u"], st[f"syn{j}_meta"] = (payload[2 + 3 * j][i], payload[3 + 3 * j][i],
+                                                                         payload[4 + 3 * j][i])
+        unpack_request(eng, b, st)
         t0 += seq_len
         p0 += n

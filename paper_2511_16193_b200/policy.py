@@ -98,6 +98,12 @@ class OutcomeRings:
         self.a[b, n, slot] = accepted[b, n]
         self.count[b, n] += 1
 
+    def reset(self, b: int) -> None:
+        """Slot b took a new request: back to the priors."""
+        self.p[b] = 0
+        self.a[b] = 0
+        self.count[b] = 0
+
     def estimate(self) -> np.ndarray:
         tp, ta = self.p.sum(-1), self.a.sum(-1)
         return np.where(tp > 0, ta / np.maximum(tp, 1), self.prior)
@@ -125,7 +131,7 @@ class RolloutDriver:
     def __init__(self, eng, requests: list[Request], methods: list[str], *, bon_on_drain: bool = True,
                  b_max: int = 8, bon_policy: str = "greedy", reconfig=None, reconfig_interval: int = 1000,
                  tail_fraction: float = 0.5, estimator_window: int = 64, priors: dict | None = None,
-                 log_events: bool = False):
+                 log_events: bool = False, straggler=None):
         if len(requests) != eng.B or len(methods) != eng.N:
             raise ConfigError("one request per slot and one method name per drafter")
         self.eng, self.reqs, self.methods = eng, list(requests), list(methods)
@@ -138,6 +144,76 @@ class RolloutDriver:
         self.log_events = log_events
         self.state = ClusterState(b_max=b_max)
         self.pairs: dict[tuple[int, str], str] = {}   # live (request id, method) -> worker
+        # cross-rank straggler pulls (straggler.StragglerPull), run at
+        # quiescent points: every `interval` steps, and continuously once
+        # this rank has drained (it is then a pull target)
+        self.straggler = straggler
+        self._gen = self._budget = self._budget_h = None
+        self.released: set[int] = set()          # slots whose request moved to another rank
+        self.stashed: dict[int, list[int]] = {}  # outputs of finished requests whose slot was reused
+
+    # -- slot movement (straggler pulls) --------------------------------------------
+
+    def slot_states(self):
+        """(live [(slot, request id, incumbent estimate)], free slots)."""
+        est = self.rings.estimate()[:, 0]   # the incumbent's ring estimates, vectorised
+        live, free = [], []
+        for b in range(self.eng.B):
+            if self._gen[b] < self._budget[b]:
+                live.append((b, self.reqs[b].id, float(est[b])))
+            else:
+                free.append(b)
+        return live, free
+
+    def release_slot(self, b: int) -> None:
+        """Slot b's request leaves this rank: stop it here for good (the
+        pinned host budget is what every captured step copies to the device)
+        and hand back its Best-of-N drafters."""
+        self._budget[b] = self._gen[b]
+        self._budget_h[b] = int(self._gen[b])
+        self.released.add(b)
+        rid = self.reqs[b].id
+        for method in self.methods[1:]:
+            w = self.pairs.pop((rid, method), None)
+            if w is not None:
+                release_pair(self.state, rid, method, w)
+        if self.eng.N > 1:
+            mask = self.eng.active.cpu().numpy()
+            mask[1:, b] = 0
+            self.eng.set_active(mask)
+
+    def stash_slot(self, b: int) -> None:
+        """Keep the output of slot b's finished request before the slot is
+        reused by an adopted one."""
+        if b not in self.released:
+            self.stashed[self.reqs[b].id] = self.eng.outputs()[b]
+
+    def outputs_by_id(self) -> dict[int, list[int]]:
+        """Every request that finished on this engine: request id -> tokens."""
+        out = dict(self.stashed)
+        for b, toks in enumerate(self.eng.outputs()):
+            if b not in self.released:
+                out[self.reqs[b].id] = toks
+        return out
+
+    def adopt_slot(self, b: int, request: Request) -> None:
+        """Slot b now holds ``request`` (already installed on the device by
+        ``migrate.recv_requests``): host lengths, budget and a fresh
+        estimator follow it."""
+        self.reqs[b] = request
+        self.released.discard(b)
+        self._gen[b] = int(self.eng.gen_len[b])
+        self._budget[b] = int(self.eng.max_new[b])
+        self._budget_h[b] = int(self._budget[b])
+        self.rings.reset(b)
+        if self.eng.N > 1:
+            mask = self.eng.active.cpu().numpy()
+            mask[1:, b] = 0
+            self.eng.set_active(mask)
+
+    def log_event(self, events: list, t_ms: float, kind: str, worker: str, rid: int, detail: dict) -> None:
+        if self.log_events:
+            events.append(Event(t_ms, kind, worker, rid, detail))
 
     # -- policies ------------------------------------------------------------------
 
@@ -196,6 +272,7 @@ class RolloutDriver:
         budget = eng.max_new.cpu().numpy().astype(np.int32)
         gen = eng.gen_len.cpu().numpy().astype(np.int64)
         budget_h = torch.from_numpy(budget.copy()).pin_memory()
+        self._gen, self._budget, self._budget_h = gen, budget, budget_h.numpy()
         cols = 4 * N + k + 2
         res = [torch.zeros((B, cols), dtype=torch.int32).pin_memory() for _ in range(2)]
         graphs = [eng.capture_io(budget_h, r) for r in res]
@@ -214,9 +291,13 @@ class RolloutDriver:
         last_ms = 0.0
         pending = None          # the launched step whose results are not read yet
         all_done = not (gen < budget).any()
+        hook = self.straggler
+        last_hook = 0
         while True:
+            # a straggler exchange needs every step read: launch nothing this round
+            due = hook is not None and (all_done or step >= max_steps or step - last_hook >= hook.interval)
             launched = None
-            if step < max_steps and not all_done:
+            if not due and step < max_steps and not all_done:
                 # launch step s, then read step s-1's results while s runs;
                 # policy decisions made now apply from step s+1
                 eng.step_io(graphs[step % 2])
@@ -275,7 +356,15 @@ class RolloutDriver:
                     since_reconfig = 0
                     reconfigs += self._reconfigure(still, t_ms, events)
             pending = launched
-            if pending is None:
+            if pending is not None:
+                continue
+            if hook is None:
+                break
+            last_hook = step
+            t_ms = start.elapsed_time(done_ev[(step - 1) % 2]) if step else 0.0
+            keep = hook(self, all_done or step >= max_steps, t_ms, events)
+            all_done = not (gen < budget).any()
+            if not keep:
                 break
         torch.cuda.synchronize()
         return RolloutReport(makespan_ms=last_ms, steps=step, committed=committed, windows=windows,
