@@ -109,6 +109,25 @@ class StragglerPull:
         self.bytes_moved = 0
         self.exchanges = 0
 
+    def warmup(self, device) -> None:
+        """Create the P2P communicators every rank pair may use before the
+        timed rollout: NCCL builds a pair's communicator lazily on its first
+        send/recv, which costs far more than a move."""
+        dist = self.dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        dev = "cpu" if dist.get_backend() == "gloo" else device
+        t = torch.zeros(4, dtype=torch.int32, device=dev)
+        for a in range(world):
+            for b in range(a + 1, world):
+                if rank == a:
+                    dist.send(t, b)
+                    dist.batch_isend_irecv([dist.P2POp(dist.isend, t, b)])[0].wait()
+                elif rank == b:
+                    dist.recv(t, a)
+                    dist.batch_isend_irecv([dist.P2POp(dist.irecv, t, a)])[0].wait()
+        recs = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(recs, t)
+
     def __call__(self, driver, local_done: bool, t_ms: float, events: list) -> bool:
         """One exchange at a quiescent point; returns False once every rank
         is done (the driver then stops)."""

@@ -80,6 +80,8 @@ def run(args) -> dict:
     hook = StragglerPull(dist, {r.id: r for r in trace}, interval=args.interval) if args.pull else None
     drv = RolloutDriver(eng, mine, [scenarios.DEFAULT_METHOD], bon_on_drain=False,
                         priors=scenarios.estimator_priors(), straggler=hook)
+    if hook is not None:
+        hook.warmup(eng.dev)
     dist.barrier()
     torch.cuda.synchronize()
     rep = drv.run()
