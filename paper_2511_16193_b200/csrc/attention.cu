@@ -102,6 +102,7 @@ struct AttnArgs {
   int* order;          // work items, longest first (attn_plan_kernel)
   int* counters;       // [0] items in order, [1 + layer] work-claim counter of a layer
   int n_slots;         // S*nkv * qblocks * splits
+  int early;           // the work list is from an earlier launch: claim + stream context pages before the wait
 };
 
 // SR_ATTN_TC=1 runs head_dim 128 on the tcgen05 kernel (attn_tc_kernel).  It
@@ -140,7 +141,6 @@ __device__ __forceinline__ int block_max_key(const SeqInfo& sq, int r0, int rows
 template <int HD>
 __global__ void __launch_bounds__(kAttnThreads, 2)
 attn_bf16_kernel(AttnArgs A) {
-  grid_dep_sync();
   constexpr int CH = HD / 8;       // 16-byte chunks per row
   constexpr int NO = HD / 8;       // n8 tiles of O per m-tile
   constexpr uint32_t kTileBytes = kKT * HD * 2;
@@ -160,11 +160,59 @@ attn_bf16_kernel(AttnArgs A) {
     sm100::fence_barrier_init();
   }
   uint32_t gi = 0;
+  // Programmatic dependent launch: the previous kernel (this layer's qkv
+  // GEMM) writes Q and the window's K/V, nothing else this kernel reads.  When
+  // the work list comes from an earlier launch (layers >= 1 of a forward), a
+  // CTA claims its first item and streams that item's first pages that hold
+  // only context keys (written by earlier steps) before waiting, so their
+  // latency hides behind the GEMM's tail.
+  uint32_t pre_issued = 0;  // first-item tiles (bit p: t_begin + p) already in flight
+  bool pre_claimed = false;
+  if (A.early) {
+    __syncthreads();  // barrier init visible
+    if (tid == 0) {
+      const int i = atomicAdd(&A.counters[1 + A.layer], 1);
+      s_item = i;
+      if (i < A.counters[0]) {
+        const int pk = A.order[i];
+        const int sp0 = pk % A.splits;
+        const int qb0 = (pk / A.splits) % A.qblocks;
+        const int z0 = pk / (A.splits * A.qblocks);
+        const SeqInfo sq0 = A.seqs[z0 / nkv];
+        const int rows0 = min(kRows, sq0.q_len * G - qb0 * kRows);
+        const int tb = sp0 * A.split_tiles;
+        const int te = min(block_max_key(sq0, qb0 * kRows, rows0, G) / kKT + 1, tb + A.split_tiles);
+        const __nv_bfloat16* cache0 = reinterpret_cast<const __nv_bfloat16*>(A.kv.cache) +
+                                      (int64_t)A.layer * A.kv.cache_layer_elems();
+        const int32_t* bt0 = A.kv.block_table + (int64_t)sq0.request * A.kv.max_pages;
+        constexpr uint32_t kTB = kKT * HD * 2;
+        for (int p = 0; p < 2; ++p) {
+          const int t = tb + p;
+          if (t >= te || t * kKT + kKT - 1 >= sq0.ctx_len) break;  // window keys: after the wait
+          const int stage = p;  // gi == 0
+          uint8_t* k_dst = sKV + stage * 2 * kTB;
+          const __nv_bfloat16* kb = cache0 + ((int64_t)bt0[t] * 2 * nkv + z0 % nkv) * A.kv.page * HD;
+          sm100::mbar_arrive_expect_tx(&full[stage], 2 * kTB);
+          sm100::bulk_load_hint(k_dst, kb, kTB, &full[stage], sm100::kEvictFirst);
+          sm100::bulk_load_hint(k_dst + kTB, kb + (int64_t)nkv * A.kv.page * HD, kTB, &full[stage],
+                                sm100::kEvictFirst);
+          pre_issued |= 1u << p;
+        }
+      }
+    }
+    pre_claimed = true;
+  }
+  grid_dep_sync();
   for (;;) {
   __syncthreads();  // previous item fully consumed (smem reusable)
-  if (tid == 0) s_item = atomicAdd(&A.counters[1 + A.layer], 1);
+  if (tid == 0 && !pre_claimed) s_item = atomicAdd(&A.counters[1 + A.layer], 1);
+  pre_claimed = false;
   __syncthreads();
   if (s_item >= A.counters[0]) break;
+  // only thread 0 issues (and skips) bulk copies; a pre-issued tile is a
+  // cache page, which the other threads' load_tile leaves to thread 0 anyway
+  const uint32_t issued = pre_issued;
+  pre_issued = 0;
   const int packed = A.order[s_item];
   const int sp = packed % A.splits;
   const int qb = (packed / A.splits) % A.qblocks;
@@ -272,8 +320,8 @@ attn_bf16_kernel(AttnArgs A) {
     qpos[hi] = r < rows ? sq.ctx_len + (r0 + r) / G : -1;  // -1: padding row, all masked
   }
   const int min_qpos = sq.ctx_len + r0 / G;  // first query row of the block
-  load_tile(t_begin, gi % kStages);
-  load_tile(t_begin + 1, (gi + 1) % kStages);
+  if (!(issued & 1u)) load_tile(t_begin, gi % kStages);
+  if (!(issued & 2u)) load_tile(t_begin + 1, (gi + 1) % kStages);
   cp_async_commit();
   cp_async_wait<0>();  // Q block
   // ldmatrix addresses, hoisted: a fragment row r reads logical chunk
@@ -1319,6 +1367,7 @@ int attention_bf16(const __nv_bfloat16* q, const SeqInfo* seqs, int num_seqs, in
   a.split_tiles = g_split_tiles;
   a.splits = ceil_div(max_key / kKT + 1, a.split_tiles);
   a.n_slots = num_seqs * kv.kv_heads * a.qblocks * a.splits;
+  a.early = (phase == 0 && !plan) ? 1 : 0;
   // partial workspace = [counters (1 + kMaxLayers) + item list (n_slots), 256 B aligned | O | (m, l)]
   const size_t list_floats = ((size_t)a.n_slots + 1 + kMaxLayers + 63) / 64 * 64;
   const size_t need = list_floats + attention_partial_floats(num_seqs, kv.kv_heads, a.qblocks, a.splits, hd);
