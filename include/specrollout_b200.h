@@ -308,10 +308,19 @@ int sr_accept_rejection(int num_requests, int k, const void* seqs, const int32_t
                         int32_t* seq_len, int32_t* gen_len, const int32_t* max_new, int bonus_token,
                         float* stats, int32_t* outcome, int32_t* bon, sr_stream_t stream);
 
+/* Host-facing step prologue (RolloutEngine.capture_io): max_new[b] =
+ * budget_host[b] read zero-copy from PINNED host memory (clamped later to the
+ * slot capacity by sr_build_verify_batch) and seq_before[b] = seq_len[b].
+ * Replaces the H2D copy of the reference-facing step's inputs
+ * (sim.py:983-1042 budgets per request). */
+int sr_io_begin(int num_requests, const int32_t* budget_host, int32_t* max_new, const int32_t* seq_len,
+                int32_t* seq_before, sr_stream_t stream);
+
 /* Host-facing step result (RolloutEngine.capture_io): out [B, 4N + width] =
  * the N drafters' outcome rows of request b (4N ints) then
  * tokens[b, seq_before[b] + j] for j < width (clamped to the row) -- the
- * committed window of the step. */
+ * committed window of the step.  `out` may be device memory or pinned host
+ * memory (written zero-copy: the step's D2H without a copy-engine node). */
 int sr_pack_results(int num_requests, int num_drafters, int width, const int32_t* outcome,
                     const int32_t* tokens, int64_t tok_stride, const int32_t* seq_before, int32_t* out,
                     sr_stream_t stream);

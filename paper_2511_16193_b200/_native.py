@@ -58,6 +58,7 @@ SIGNATURES: dict[str, list] = {
     "sr_decoupled_verify_post": [_i32, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "sr_decoupled_verify_receive": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "sr_pack_results": [_i32, _i32, _i32, _vp, _vp, _i64, _vp, _vp, _vp],
+    "sr_io_begin": [_i32, _vp, _vp, _vp, _vp, _vp],
     "sr_build_verify_batch": [_i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               _vp, _vp, _vp, _vp, _vp],
 }

@@ -382,7 +382,33 @@ __global__ void pack_results_kernel(int B, int N, int w, const int32_t* __restri
   out[e] = v;
 }
 
+// Host-facing step prologue: this step's request budgets straight from the
+// caller's pinned host buffer (zero-copy over the host link; build_verify
+// clamps them to each slot's capacity) and the pre-step lengths the result
+// pack reads.  One kernel instead of two copy-engine nodes in the step graph.
+__global__ void io_begin_kernel(int B, const int32_t* __restrict__ budget_host, int32_t* __restrict__ max_new,
+                                const int32_t* __restrict__ seq_len, int32_t* __restrict__ seq_before) {
+  grid_dep_sync();
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  max_new[b] = budget_host[b];
+  seq_before[b] = seq_len[b];
+}
+
 }  // namespace sr
+
+extern "C" int sr_io_begin(int num_requests, const int32_t* budget_host, int32_t* max_new, const int32_t* seq_len,
+                           int32_t* seq_before, sr_stream_t stream) {
+  SR_REQUIRE(num_requests >= 0, "negative request count");
+  if (num_requests == 0) return SR_OK;
+  SR_REQUIRE(budget_host && max_new && seq_len && seq_before, "null pointer");
+  void* dev = nullptr;
+  SR_REQUIRE(cudaHostGetDevicePointer(&dev, const_cast<int32_t*>(budget_host), 0) == cudaSuccess,
+             "budget_host must be pinned (page-locked) host memory");
+  sr::launch_k(sr::io_begin_kernel, sr::ceil_div(num_requests, 256), 256, 0, (cudaStream_t)stream, num_requests,
+               reinterpret_cast<const int32_t*>(dev), max_new, seq_len, seq_before);
+  return sr::check_launch("io_begin_kernel");
+}
 
 extern "C" int sr_pack_results(int num_requests, int num_drafters, int width, const int32_t* outcome,
                                const int32_t* tokens, int64_t tok_stride, const int32_t* seq_before, int32_t* out,
@@ -390,6 +416,14 @@ extern "C" int sr_pack_results(int num_requests, int num_drafters, int width, co
   SR_REQUIRE(num_requests >= 0 && num_drafters >= 1 && width >= 0 && tok_stride > 0, "bad result shape");
   if (num_requests == 0) return SR_OK;
   SR_REQUIRE(outcome && tokens && seq_before && out, "null pointer");
+  // `out` may be pinned host memory: the kernel then writes it zero-copy
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, out) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
+    void* dev = nullptr;
+    SR_REQUIRE(cudaHostGetDevicePointer(&dev, out, 0) == cudaSuccess, "result buffer: host memory must be pinned");
+    out = reinterpret_cast<int32_t*>(dev);
+  }
+  cudaGetLastError();  // a pageable pointer leaves a sticky query error behind
   const int n = num_requests * (4 * num_drafters + width);
   sr::launch_k(sr::pack_results_kernel, sr::ceil_div(n, 256), 256, 0, (cudaStream_t)stream, num_requests,
                num_drafters, width, outcome, tokens, tok_stride, seq_before, out);

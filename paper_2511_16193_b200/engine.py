@@ -428,24 +428,29 @@ class RolloutEngine:
         cols = 4 * self.N + w
         if tuple(result_host.shape) != (self.B, cols) or budget_host.numel() != self.B:
             raise ConfigError("result_host must be [B, 4 * N + k + 2] and budget_host [B]")
+        if not (budget_host.is_pinned() and result_host.is_pinned()):
+            raise ConfigError("capture_io needs pinned host buffers (tensor.pin_memory())")
+        if budget_host.dtype != torch.int32 or result_host.dtype != torch.int32 or not result_host.is_contiguous():
+            raise ConfigError("capture_io buffers are contiguous int32")
         seq_before = torch.empty_like(self.seq_len)
-        res = torch.empty((self.B, cols), dtype=torch.int32, device=self.dev)
         if not hasattr(self, "_io_keep"):
             self._io_keep = []
-        self._io_keep.append((seq_before, res))   # buffers the graph reads/writes stay alive
+        self._io_keep.append((seq_before, budget_host, result_host))   # buffers the graph reads/writes stay alive
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             g.capture_begin()
-            self.max_new.copy_(budget_host, non_blocking=True)
-            seq_before.copy_(self.seq_len)
+            # H2D of the budgets and D2H of the results are zero-copy kernel
+            # accesses to the pinned buffers: no copy-engine nodes in the graph
+            _native.check(self.lib.sr_io_begin(
+                self.B, budget_host.data_ptr(), self.max_new.data_ptr(), self.seq_len.data_ptr(),
+                seq_before.data_ptr(), _native.stream_handle()), "sr_io_begin")
             self._enqueue_step(0)
             _native.check(self.lib.sr_pack_results(
                 self.B, self.N, w, self.history[0].data_ptr(), self.tokens.data_ptr(), self.stride,
-                seq_before.data_ptr(), res.data_ptr(), _native.stream_handle()), "sr_pack_results")
-            result_host.copy_(res, non_blocking=True)
+                seq_before.data_ptr(), result_host.data_ptr(), _native.stream_handle()), "sr_pack_results")
             g.capture_end()
         torch.cuda.current_stream().wait_stream(s)
         self.graph_io = g
