@@ -567,9 +567,14 @@ __device__ unsigned long long g_tc_trace[8][64];
 #define TC_TRACE(ev, blk) do { } while (0)
 #endif
 
-// mbarrier wait that names itself if it stalls (a protocol bug reports the
-// role, barrier and phase before the watchdog trap)
+// mbarrier wait that, in probe builds (SR_ATTN_PROBE), names itself if it
+// stalls (a protocol bug reports role, barrier and phase before the trap)
 __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t phase, int tag) {
+#if SR_ATTN_PROBE == 0
+  (void)tag;  // release builds: the plain watchdog wait (no printf path in the kernel)
+  sm100::mbar_wait(bar, phase);
+  return;
+#endif
   if (sm100::mbar_try_wait(bar, phase)) return;
   const uint64_t t0 = sm100::global_timer_ns();
   bool said = false;
