@@ -644,6 +644,58 @@ def variant_ngram_kernel(lib, _native, B=1024, L=20480, reps=20):
             "achieved_gbs": nbytes / (ms * 1e-3) / 1e9, "frac_of_hbm": nbytes / (ms * 1e-3) / 1e9 / hbm}
 
 
+def variant_rejection_kernel(lib, _native, B=256, k=K, V=151936, reps=20):
+    """K3 in rejection-sampling mode (sr_accept_rejection: rs_stats, rs_sample, rs_commit)
+    at the bench's verify shape: B requests x k draft slots over fp32 logit
+    rows of the 1.5B vocabulary.  HBM-bound: rs_stats reads every draft slot's
+    target row p_j and drafter row q_j once; rs_commit reads p_a and q_a (the
+    residual at a rejection) or p_n (the bonus after a full accept) per
+    request.  Algorithmic bytes are counted from the outcome rows."""
+    import numpy as np
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(0)
+    R = B * (k + 1)
+    p = torch.randn((R, V), generator=g, device="cuda") * 2.0
+    q = (p.view(B, k + 1, V)[:, :k].transpose(0, 1) + 0.7 * torch.randn((k, B, V), generator=g, device="cuda")).contiguous()
+    seqs = torch.zeros((B, 8), dtype=torch.int32, device="cuda")
+    seqs[:, 0] = torch.arange(B, device="cuda", dtype=torch.int32) * (k + 1)
+    seqs[:, 1] = k + 1
+    seqs[:, 2] = torch.arange(B, device="cuda", dtype=torch.int32)
+    seqs[:, 3] = 1000
+    seqs[:, 4] = -1
+    # drafts: the drafter's argmax (a plausible sample), so acceptance is mixed
+    tok = torch.zeros(R, dtype=torch.int32, device="cuda")
+    tok.view(B, k + 1)[:, 1:] = q.argmax(-1).t().to(torch.int32)
+    stride = 1000 + (reps + 8) * (k + 1) + 8
+    tokens = torch.zeros((B, stride), dtype=torch.int32, device="cuda")
+    seq_len = torch.full((B,), 1001, dtype=torch.int32, device="cuda")
+    gen_len = torch.zeros(B, dtype=torch.int32, device="cuda")
+    max_new = torch.full((B,), 1 << 20, dtype=torch.int32, device="cuda")
+    stats = torch.zeros(int(lib.sr_accept_rejection_workspace_floats(B, k)), dtype=torch.float32, device="cuda")
+    outcome = torch.zeros((B, 4), dtype=torch.int32, device="cuda")
+    bon = torch.zeros(B, dtype=torch.int32, device="cuda")
+    st = _native.stream_handle()
+
+    def go():
+        _native.check(lib.sr_accept_rejection(
+            B, k, seqs.data_ptr(), tok.data_ptr(), p.data_ptr(), V, q.data_ptr(), V, V, 1.0, 7,
+            tokens.data_ptr(), stride, seq_len.data_ptr(), gen_len.data_ptr(), max_new.data_ptr(), 1,
+            stats.data_ptr(), outcome.data_ptr(), bon.data_ptr(), st), "sr_accept_rejection")
+    for _ in range(3):
+        go()
+    ms = timed(go, reps)
+    o = outcome.cpu().numpy()
+    residual = int((o[:, 1] < o[:, 0]).sum())          # rejection: p_a and q_a rows
+    extra_rows = 2 * residual + (B - residual)         # else the bonus from p_n
+    nbytes = (k * B * 2 + extra_rows) * V * 4
+    _, _, hbm, _ = peaks()
+    return {"shape": f"{B} requests x {k} draft slots, fp32 logits over V={V} (rs_stats + rs_sample + rs_commit)",
+            "us_per_launch": ms * 1e3, "algorithmic_bytes": int(nbytes),
+            "mean_accepted": float(o[:, 1].mean()),
+            "achieved_gbs": nbytes / (ms * 1e-3) / 1e9, "frac_of_hbm": nbytes / (ms * 1e-3) / 1e9 / hbm}
+
+
 def variant_configs2(steps=10, warmup=2, batch=64, graph=True):
     """configs[2] on one GPU: Qwen2.5-7B-shaped target, the per-GPU share of
     batch 512 over 8 GPUs (64 prompts), Best-of-N with N = 3 drafters
@@ -922,7 +974,8 @@ def main():
         if world == 1 and not args.no_variants and args.layers is None and args.model == MODEL:
             lib = _native.lib()
             result["variants"] = {"ngram": variant_ngram(args, s, model, prompts, truth),
-                                  "ngram_kernel": variant_ngram_kernel(lib, _native)}
+                                  "ngram_kernel": variant_ngram_kernel(lib, _native),
+                                  "accept_rejection_kernel": variant_rejection_kernel(lib, _native)}
         cpu_ok = world == 1 and not args.no_cpu_baseline and shape(args.model).linear_params() <= 10e9
         result["cpu_baseline"] = cpu_baseline(s, model, prompts, trace, truth) if cpu_ok else None
         result["cpu_baseline_simulator"] = cpu_baseline_simulator() if cpu_ok else None

@@ -308,6 +308,11 @@ int sr_accept_rejection(int num_requests, int k, const void* seqs, const int32_t
                         int32_t* seq_len, int32_t* gen_len, const int32_t* max_new, int bonus_token,
                         float* stats, int32_t* outcome, int32_t* bon, sr_stream_t stream);
 
+/* Floats of the `stats` workspace sr_accept_rejection needs: per verify row
+ * (lse_p, lse_q, log p(d), log q(d)), then 16 per-request vocabulary-chunk
+ * (value, index) partials of the extra-token sample. */
+uint64_t sr_accept_rejection_workspace_floats(int num_requests, int k);
+
 /* Host-facing step prologue (RolloutEngine.capture_io): max_new[b] =
  * budget_host[b] read zero-copy from PINNED host memory (clamped later to the
  * slot capacity by sr_build_verify_batch) and seq_before[b] = seq_len[b].

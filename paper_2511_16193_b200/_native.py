@@ -52,6 +52,7 @@ SIGNATURES: dict[str, list] = {
                              _vp, _vp, _vp, _vp],
     "sr_accept_rejection": [_i32, _i32, _vp, _vp, _vp, _i64, _vp, _i64, _i32, ctypes.c_float, ctypes.c_uint32,
                             _vp, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp],
+    "sr_accept_rejection_workspace_floats": [_i32, _i32],
     "sr_decoupled_draft_prep": [_i32, _vp, _vp, _vp, _vp, _vp, _vp],
     "sr_decoupled_draft_post": [_i32, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "sr_decoupled_draft_apply": [_i32, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
@@ -63,6 +64,7 @@ SIGNATURES: dict[str, list] = {
                               _vp, _vp, _vp, _vp, _vp],
 }
 _RESTYPES = {"sr_last_error": ctypes.c_char_p, "sr_model_workspace_bytes": ctypes.c_uint64,
+             "sr_accept_rejection_workspace_floats": ctypes.c_uint64,
              "sr_launch_count": ctypes.c_longlong}
 
 

@@ -290,7 +290,9 @@ class RolloutEngine:
         self.live_rows = torch.zeros(1, dtype=torch.int32, device=dev)
         if acceptance == "rejection":
             self.p_logits = torch.empty((R, target.s.vocab), dtype=torch.float32, device=dev)
-            self.rs_stats = torch.zeros((R, 4), dtype=torch.float32, device=dev)
+            # per verify row (lse_p, lse_q, log p(d), log q(d)) + per-request chunk partials
+            self.rs_stats = torch.zeros(int(_native.lib().sr_accept_rejection_workspace_floats(self.B, k)),
+                                        dtype=torch.float32, device=dev)
         self.steps = 0
         self.max_key = need - 1
         self.graph = None

@@ -52,7 +52,7 @@ def test_rejection_kernel_preserves_target_distribution():
         seqs=seqs, token_ids=token_ids, p=p_logits, q=q_logits,
         tokens=np.zeros((B, stride), np.int32), seq_len=np.full(B, ctx + 1, np.int32),
         gen_len=np.zeros(B, np.int32), max_new=np.full(B, 8, np.int32)).items()}
-    stats_ws = torch.zeros((2 * B, 4), dtype=torch.float32, device="cuda")
+    stats_ws = torch.zeros(int(lib.sr_accept_rejection_workspace_floats(B, 1)), dtype=torch.float32, device="cuda")
     outcome = torch.zeros((B, 4), dtype=torch.int32, device="cuda")
     bon = torch.zeros(B, dtype=torch.int32, device="cuda")
     _native.check(lib.sr_accept_rejection(
