@@ -362,7 +362,7 @@ class RolloutDriver:
                 break
             last_hook = step
             t_ms = start.elapsed_time(done_ev[(step - 1) % 2]) if step else 0.0
-            keep = hook(self, all_done or step >= max_steps, t_ms, events)
+            keep = hook(self, all_done or step >= max_steps, t_ms, events, can_run=step < max_steps)
             all_done = not (gen < budget).any()
             if not keep:
                 break

@@ -128,12 +128,15 @@ class StragglerPull:
         recs = [torch.empty_like(t) for _ in range(world)]
         dist.all_gather(recs, t)
 
-    def __call__(self, driver, local_done: bool, t_ms: float, events: list) -> bool:
+    def __call__(self, driver, local_done: bool, t_ms: float, events: list, can_run: bool = True) -> bool:
         """One exchange at a quiescent point; returns False once every rank
-        is done (the driver then stops)."""
+        is done (the driver then stops).  A rank out of steps (``can_run``
+        False) offers no free slots: it could not run adopted requests."""
         dist = self.dist
         rank = dist.get_rank()
         live, free = driver.slot_states()
+        if not can_run:
+            free = []
         # one fixed-size record per rank, one all_gather (device tensors
         # over NCCL, host over gloo): ~tens of us, unlike all_gather_object
         mine = encode_state([] if local_done else live, free)
