@@ -18,6 +18,8 @@
 // then the final norm and the lm_head GEMM with a fused vocabulary argmax
 // epilogue (logits never reach HBM) or an fp32 logits epilogue.
 #include "common.cuh"
+
+#include <cstdlib>
 #include "gemm.cuh"
 #include "layers.cuh"
 
@@ -276,8 +278,13 @@ int sr_model_create(const sr_model_desc* desc, void** handle) {
     m->p_down.resize(d.layers);
     for (int l = 0; l < d.layers; ++l) {
       const void* const* w = m->layer_ptrs.data() + (size_t)l * sr::kLayerPtrs;
+      // SR_QKV_BN (measurement knob): explicit pair tile width of the qkv plan
+      static const int qkv_bn = [] {
+        const char* v = getenv("SR_QKV_BN");
+        return v ? -atoi(v) : 0;
+      }();
       rc = sr::gemm_bf16_plan(&m->p_qkv[l], T, m->qkv_width, H, (const bf*)m->h, H, (const bf*)w[1], H,
-                              m->qkv, m->qkv_width, sr::kEpiQkvRope, (const float*)w[2], 0);
+                              m->qkv, m->qkv_width, sr::kEpiQkvRope, (const float*)w[2], qkv_bn);
       if (!rc) {
         sr::RopeArgs& ra = m->p_qkv[l].rope;
         ra.kv_dst = m->kv_dst;
