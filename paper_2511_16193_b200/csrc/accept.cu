@@ -418,12 +418,15 @@ extern "C" int sr_pack_results(int num_requests, int num_drafters, int width, co
   SR_REQUIRE(outcome && tokens && seq_before && out, "null pointer");
   // `out` may be pinned host memory: the kernel then writes it zero-copy
   cudaPointerAttributes pa{};
-  if (cudaPointerGetAttributes(&pa, out) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
+  const bool known = cudaPointerGetAttributes(&pa, out) == cudaSuccess;
+  cudaGetLastError();  // clear a failed query
+  SR_REQUIRE(known && pa.type != cudaMemoryTypeUnregistered,
+             "result buffer must be device memory or pinned (page-locked) host memory");
+  if (pa.type == cudaMemoryTypeHost) {
     void* dev = nullptr;
     SR_REQUIRE(cudaHostGetDevicePointer(&dev, out, 0) == cudaSuccess, "result buffer: host memory must be pinned");
     out = reinterpret_cast<int32_t*>(dev);
   }
-  cudaGetLastError();  // a pageable pointer leaves a sticky query error behind
   const int n = num_requests * (4 * num_drafters + width);
   sr::launch_k(sr::pack_results_kernel, sr::ceil_div(n, 256), 256, 0, (cudaStream_t)stream, num_requests,
                num_drafters, width, outcome, tokens, tok_stride, seq_before, out);

@@ -774,3 +774,26 @@ def test_compacted_batch_equals_fixed_layout(N):
     for got, total in res[1][2]:
         assert got == total                    # packed rows == sum of window lengths
     assert res[1][2][-1][0] < B * N * (k + 1)  # the tail ran on fewer rows
+
+
+def test_pack_results_rejects_pageable_host_buffer():
+    """sr_pack_results writes device or pinned host memory (zero-copy D2H); a
+    pageable host buffer is a config error, not a device fault."""
+    from paper_2511_16193_b200 import _native
+
+    lib = _native.lib()
+    B, N, w = 4, 1, 6
+    outcome = torch.zeros((B, 4), dtype=torch.int32, device="cuda")
+    tokens = torch.zeros((B, 32), dtype=torch.int32, device="cuda")
+    seq_before = torch.ones(B, dtype=torch.int32, device="cuda")
+    pageable = torch.zeros((B, 4 * N + w), dtype=torch.int32)
+    rc = lib.sr_pack_results(B, N, w, outcome.data_ptr(), tokens.data_ptr(), 32, seq_before.data_ptr(),
+                             pageable.data_ptr(), _native.stream_handle())
+    assert rc == 2
+    pinned = pageable.pin_memory()
+    tokens[:, 1:7] = torch.arange(6, dtype=torch.int32, device="cuda")
+    outcome[:, 0] = 3
+    _native.check(lib.sr_pack_results(B, N, w, outcome.data_ptr(), tokens.data_ptr(), 32, seq_before.data_ptr(),
+                                      pinned.data_ptr(), _native.stream_handle()), "pack")
+    torch.cuda.synchronize()
+    assert pinned[:, 0].tolist() == [3] * B and pinned[0, 4:].tolist() == list(range(6))
