@@ -133,6 +133,7 @@ CASES = [
     ([0, 0, 300], [100, 1, 64], 12, 2, 128),                          # prefill: 32-row blocks across tokens
     ([500, 1500, 2100], [5, 5, 5], 28, 4, 128),                       # 7B shape: G = 7, two row blocks
     ([64, 1000, 4095], [5, 5, 5], 40, 8, 128),                        # 32B shape: G = 5
+    ([20000, 16385], [5, 1], 12, 2, 128),                             # 20K-key long tail: 10 splits
 ]
 
 
