@@ -117,6 +117,32 @@ class OutcomeRings:
         return est
 
 
+@dataclass(frozen=True)
+class Placement:
+    """The plan search's answer for a batch (reference ``planner.py:113-211``,
+    reported side by side by the CLI's ``plan`` command ``cli.py:406-460``):
+    the mode with the higher modeled throughput, its window, and both plans."""
+
+    mode: str            # "coupled" | "decoupled"
+    window: int
+    tgs_estimate: float
+    decoupled: object    # planner.ExecutionPlan
+    coupled: object      # planner.CoupledPlan
+
+
+def choose_placement(batch: int, model, p: float, method: str | None = None) -> Placement:
+    """Run both plan searches on a (measured) cost model and pick the mode
+    with the higher tokens/GPU/s estimate; ties go to coupled (no drafter
+    GPUs to dedicate)."""
+    from .planner import search_plan, search_plan_coupled
+
+    dec = search_plan(batch, model, p, method)
+    cpl = search_plan_coupled(batch, model, p, method)
+    if dec.tgs_estimate > cpl.tgs_estimate:
+        return Placement("decoupled", dec.window, dec.tgs_estimate, dec, cpl)
+    return Placement("coupled", cpl.window, cpl.tgs_estimate, dec, cpl)
+
+
 class RolloutDriver:
     """Runs a :class:`~paper_2511_16193_b200.engine.RolloutEngine` to
     completion through its host-facing step with SpecActor's tail policies.
@@ -131,7 +157,7 @@ class RolloutDriver:
     def __init__(self, eng, requests: list[Request], methods: list[str], *, bon_on_drain: bool = True,
                  b_max: int = 8, bon_policy: str = "greedy", reconfig=None, reconfig_interval: int = 1000,
                  tail_fraction: float = 0.5, estimator_window: int = 64, priors: dict | None = None,
-                 log_events: bool = False, straggler=None):
+                 log_events: bool = False, straggler=None, placement: Placement | None = None):
         if len(requests) != eng.B or len(methods) != eng.N:
             raise ConfigError("one request per slot and one method name per drafter")
         self.eng, self.reqs, self.methods = eng, list(requests), list(methods)
@@ -148,6 +174,14 @@ class RolloutDriver:
         # quiescent points: every `interval` steps, and continuously once
         # this rank has drained (it is then a pull target)
         self.straggler = straggler
+        # the plan search's window reaches the engine (a decoupled placement
+        # runs through decoupled.run_ranks, not a single-engine driver)
+        self.placement = placement
+        if placement is not None:
+            if placement.mode != "coupled":
+                raise ConfigError("decoupled placement: run it with decoupled.run_ranks "
+                                  f"(g_d = {placement.decoupled.g_d} drafter GPUs per group)")
+            eng.set_windows(np.full(eng.B, max(1, min(eng.k, placement.window)), np.int32))
         self._gen = self._budget = self._budget_h = None
         self.released: set[int] = set()          # slots whose request moved to another rank
         self.stashed: dict[int, list[int]] = {}  # outputs of finished requests whose slot was reused

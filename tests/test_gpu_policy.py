@@ -87,3 +87,26 @@ def test_policy_loop_reconfigure_windows():
     assert rep.reconfigs > 0
     w = eng.window.cpu().numpy()
     assert (w >= 1).all() and (w <= K).all()
+
+
+def test_placement_from_b200_cost_model_reaches_engine():
+    """The plan search on the B200-measured cost model picks the placement
+    (coupled on B200) and its window; the driver applies it to every request
+    and the rollout stays exact."""
+    from pathlib import Path
+
+    from paper_2511_16193_b200 import scenarios
+    from paper_2511_16193_b200.costmodel import CostModel
+    from paper_2511_16193_b200.engine import RolloutEngine, SyntheticDrafter
+    from paper_2511_16193_b200.policy import RolloutDriver, choose_placement
+
+    s, trace, prompts, lens, m, truth = _setup(B=16)
+    cm = CostModel.load(Path(__file__).resolve().parent.parent / "profiles" / "r01" / "costmodel_b200.json")
+    pl = choose_placement(16, cm, 0.7, "ngram")
+    assert pl.mode == "coupled" and 1 <= pl.window <= K
+    d = SyntheticDrafter(truth, trace, scenarios.DEFAULT_METHOD, seed=0, vocab=s.vocab)
+    eng = RolloutEngine(m, prompts, lens, k=K, drafters=(d,), history=1)
+    eng.prefill()
+    rep = RolloutDriver(eng, trace, [scenarios.DEFAULT_METHOD], bon_on_drain=False, placement=pl).run()
+    assert eng.outputs() == truth and rep.committed == sum(lens)
+    assert (eng.window.cpu().numpy() == min(K, pl.window)).all()

@@ -27,3 +27,21 @@ def test_outcome_rings_match_reference_estimator():
                 assert est[b, n] == ref[b][n].estimate()
                 assert rings.estimator(b, n).estimate() == ref[b][n].estimate()
                 assert rings.estimator(b, n).count() == ref[b][n].count()
+
+
+def test_choose_placement_picks_higher_modeled_throughput():
+    """Both reference plan searches run; the placement is the mode with the
+    higher estimate (coupled on the B200 calibration)."""
+    from pathlib import Path
+
+    from paper_2511_16193_b200 import scenarios
+    from paper_2511_16193_b200.costmodel import CostModel
+    from paper_2511_16193_b200.policy import choose_placement
+
+    cm = CostModel.load(Path(__file__).resolve().parent.parent / "profiles" / "r01" / "costmodel_b200.json")
+    pl = choose_placement(256, cm, 0.7, "ngram")
+    assert pl.mode == "coupled"
+    assert pl.tgs_estimate == pl.coupled.tgs_estimate >= pl.decoupled.tgs_estimate
+    ref = scenarios.default_cost_model()
+    pr = choose_placement(256, ref, 0.7)
+    assert pr.tgs_estimate == max(pr.coupled.tgs_estimate, pr.decoupled.tgs_estimate)
