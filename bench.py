@@ -753,13 +753,13 @@ def variant_configs2(steps=10, warmup=2, batch=64, graph=True):
 def variant_configs4(steps=6, warmup=2, batch=64, graph=True):
     """configs[4] on one GPU: Qwen2.5-32B-shaped target (weights built layer
     by layer), 64 prompts (the paper's per-GPU share), T = 1.0 keyed sampling,
-    Best-of-N with N = 4 drafters (n-gram at four (min_n, max_n) settings: the
-    paper has three methods, SURVEY §8(d) C5 leaves the fourth to the
-    builder), k = 4.  Exact-match verification against the target's keyed
+    Best-of-N with N = 4 drafters (n-gram at three (min_n, max_n) settings
+    and the pooled prompt lookup over the batch: the paper has three methods,
+    SURVEY §8(d) C5 leaves the fourth to the builder), k = 4.  Exact-match verification against the target's keyed
     sample keeps the committed tokens equal to plain sampled decoding."""
     import torch
 
-    from paper_2511_16193_b200.engine import NgramDrafter, RolloutEngine
+    from paper_2511_16193_b200.engine import NgramDrafter, PooledNgramDrafter, RolloutEngine
     from paper_2511_16193_b200.model import DeviceModel, init_weights, shape
 
     s = shape("qwen2.5-32b")
@@ -771,7 +771,7 @@ def variant_configs4(steps=6, warmup=2, batch=64, graph=True):
                     max_seqs=batch * N, branches=batch * (N - 1))
     del w
     torch.cuda.empty_cache()
-    drafters = (NgramDrafter(1, 3), NgramDrafter(2, 2), NgramDrafter(1, 1), NgramDrafter(3, 4))
+    drafters = (NgramDrafter(1, 3), NgramDrafter(2, 2), PooledNgramDrafter(2, 4), NgramDrafter(3, 4))
     eng = RolloutEngine(m, prompts, budget, k=K, drafters=drafters, bonus_token=True, history=1,
                         temperature=1.0, seed=7)
     eng.prefill()
@@ -787,7 +787,7 @@ def variant_configs4(steps=6, warmup=2, batch=64, graph=True):
     out = {"value": committed / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
            "verify_rows_last_step": int(rows),
            "config": f"configs[4] per-GPU share: qwen2.5-32b-shaped target, {batch} prompts, k={K}, T=1.0 keyed "
-                     f"sampling, Best-of-N N=4 (n-gram (1,3) (2,2) (1,1) (3,4))",
+                     f"sampling, Best-of-N N=4 (n-gram (1,3), (2,2), (3,4) and pooled prompt lookup (2,4) over the batch)",
            "note": "random-init target + random prompts: n-gram drafts rarely exist, so compacted verify "
                    "batches are ~1 row per request and the step is the 32B weight stream (64 GB bf16)"}
     if tl:

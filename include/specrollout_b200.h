@@ -107,6 +107,18 @@ int sr_ngram_propose(int batch, const int32_t* tokens, int64_t stride, const int
                      int min_n, int max_n, int k, int32_t* out_draft, int32_t* out_ndraft,
                      int64_t* scratch, sr_stream_t stream);
 
+/* Pooled prompt lookup (a fourth Best-of-N drafting method, configs[4]): the
+ * suffix of request b is matched against its own context (sr_ngram_propose
+ * semantics) and every other request's committed tokens; the longest match
+ * in [min_n, max_n] wins, ties to the own context, then other requests in
+ * index order, then the earliest end position; up to k following tokens of
+ * that row are proposed (none past the row's length or b's capacity).  With
+ * batch 1 it equals sr_ngram_propose.  scratch: batch int64 (zero on entry,
+ * left zero). */
+int sr_pooled_ngram_propose(int batch, const int32_t* tokens, int64_t stride, const int32_t* lens, int min_n,
+                            int max_n, int k, int32_t* out_draft, int32_t* out_ndraft, int64_t* scratch,
+                            sr_stream_t stream);
+
 /* ---------------------------------------------------------------------------
  * K1 building block: C = A[M,K] . W[N,K]^T with a fused epilogue (the
  * projections of the target model's verification forward; no reference

@@ -41,3 +41,42 @@ def propose(ctx, min_n: int, max_n: int, k: int, max_model_len: int | None = Non
     start = best_s + best_n
     k = min(k, total - start)
     return [int(x) for x in ctx[start:start + k]]
+
+
+def propose_pooled(rows, b: int, min_n: int, max_n: int, k: int, max_model_len: int | None = None) -> list[int]:
+    """Pooled prompt lookup (``sr_pooled_ngram_propose``): request ``b``'s
+    suffix against its own context (exactly :func:`propose`'s rule) and every
+    other request's tokens ``rows[r]``.  Longest match length n in [min_n,
+    max_n] wins; ties: own context, then other rows in index order, then the
+    earliest match.  Up to k tokens following the match in its row.  Test
+    infrastructure only."""
+    own = np.asarray(rows[b])
+    total = len(own)
+    if max_model_len is None:
+        max_model_len = 1 << 40
+    if total < min_n:
+        return []
+    k = min(k, max_model_len - total)
+    if k <= 0:
+        return []
+    order = [b] + [r for r in range(len(rows)) if r != b]
+    best = (0, None, -1)   # (n, row, start)
+    for r in order:
+        ctx = np.asarray(rows[r])
+        end_lim = (total if r == b else len(ctx)) - 2   # a continuation token must follow
+        for s in range(len(ctx)):
+            n = 0
+            for cand in range(1, max_n + 1):
+                if s + cand - 1 > end_lim or cand > total:
+                    break
+                if np.array_equal(ctx[s:s + cand], own[total - cand:]):
+                    n = cand
+            if n > best[0]:
+                best = (n, r, s)
+    n, r, s = best
+    if n < min_n or r is None:
+        return []
+    ctx = np.asarray(rows[r])
+    start = s + n
+    k = min(k, len(ctx) - start)
+    return [int(x) for x in ctx[start:start + k]]

@@ -31,6 +31,7 @@ SIGNATURES: dict[str, list] = {
     "sr_verify_windows": [_i32, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _i32,
                           _vp, _vp, _vp, _vp],
     "sr_ngram_propose": [_i32, _vp, _i64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
+    "sr_pooled_ngram_propose": [_i32, _vp, _i64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
     "sr_gemm": [_i32, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _i32, _vp, _i32,
                 _vp, _vp],
     "sr_gemm_splits": [_i32, _i32, _i32],

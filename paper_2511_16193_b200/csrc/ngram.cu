@@ -201,3 +201,108 @@ extern "C" int sr_ngram_propose(int batch, const int32_t* tokens, int64_t stride
                  min_n, max_n, k, out_draft, out_ndraft, keys, arrivals);
   return sr::check_launch("ngram_kernel");
 }
+
+// ---------------------------------------------------------------------------
+// Pooled prompt lookup (a fourth drafting method for Best-of-N, configs[4]):
+// the request's suffix is matched against its own context (vLLM n-gram
+// semantics above) AND every other request's committed tokens -- RL rollouts
+// sample each prompt several times, so a group's samples share text.  The
+// longest match length n in [min_n, max_n] wins; ties go to the own context,
+// then to other requests in index order, then to the earliest end position;
+// up to k tokens that follow the match in that row are proposed.  With one
+// request it is exactly the n-gram drafter.
+//
+// One CTA per (row r, request b): stream row r, keep the best (n, rank, e)
+// key, atomicMax it into the request's scratch; a second kernel emits the
+// proposal and re-zeroes the scratch.  Rows stay hot in L2 across the B
+// requests that scan them.
+namespace sr {
+
+__global__ void __launch_bounds__(kNgramThreads)
+pooled_match_kernel(int B, const int32_t* __restrict__ tokens, int64_t stride, const int32_t* __restrict__ lens,
+                    int min_n, int max_n, unsigned long long* __restrict__ keys) {
+  grid_dep_sync();
+  const int r = blockIdx.x, b = blockIdx.y;
+  const int L = lens[b], Lr = lens[r];
+  __shared__ int suf[kMaxNgram];
+  __shared__ unsigned long long warp_best[kNgramThreads / 32];
+  if (L < min_n) return;
+  const int32_t* own = tokens + (int64_t)b * stride;
+  const int32_t* row = tokens + (int64_t)r * stride;
+  if ((int)threadIdx.x < max_n) suf[threadIdx.x] = threadIdx.x < L ? own[L - 1 - threadIdx.x] : -1;  // suf[j] = tokens[L-1-j]
+  __syncthreads();
+  const int rank = r == b ? 0 : (r < b ? r + 1 : r);  // own context first, then others in index order
+  const int lim = (r == b ? L : Lr) - 2;               // a continuation token must follow the match
+  const int last = suf[0];
+  const int cap_own = L;                                // a match cannot use more suffix tokens than exist
+  unsigned long long best = 0ull;
+  for (int e = threadIdx.x; e <= lim; e += kNgramThreads) {
+    if (row[e] != last) continue;
+    int n = 1;
+    const int mx = min(min(max_n, e + 1), cap_own);
+    while (n < mx && row[e - n] == suf[n]) ++n;
+    if (n < min_n) continue;
+    const unsigned long long key = ((unsigned long long)n << 56) | ((unsigned long long)(0xFFFFu - rank) << 32) |
+                                   (unsigned long long)(0xFFFFFFFFu - (unsigned)e);
+    best = key > best ? key : best;
+  }
+  best = warp_max_u64(best);
+  if ((threadIdx.x & 31) == 0) warp_best[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long blk = 0ull;
+    for (int i = 0; i < kNgramThreads / 32; ++i) blk = warp_best[i] > blk ? warp_best[i] : blk;
+    if (blk) atomicMax(&keys[b], blk);
+  }
+}
+
+__global__ void pooled_emit_kernel(int B, const int32_t* __restrict__ tokens, int64_t stride,
+                                   const int32_t* __restrict__ lens, int min_n, int k, int32_t* __restrict__ out_draft,
+                                   int32_t* __restrict__ out_nd, unsigned long long* __restrict__ keys) {
+  grid_dep_sync();
+  const int b = blockIdx.x;
+  const unsigned long long key = keys[b];
+  const int L = lens[b];
+  int nd = 0;
+  const int n = (int)(key >> 56);
+  if (key != 0ull && L >= min_n && n >= min_n) {
+    const int rank = 0xFFFF - (int)((key >> 32) & 0xFFFFu);
+    const int e = (int)(0xFFFFFFFFu - (unsigned)(key & 0xFFFFFFFFull));
+    const int r = rank == 0 ? b : (rank <= b ? rank - 1 : rank);
+    const int Lr = lens[r];
+    const int start = e + 1;
+    const int64_t room = stride - (int64_t)L, after = (int64_t)Lr - start;
+    nd = (int)(room < after ? room : after);
+    nd = max(min(k, nd), 0);
+    if ((int)threadIdx.x < nd) out_draft[(int64_t)b * k + threadIdx.x] = tokens[(int64_t)r * stride + start + threadIdx.x];
+  }
+  __syncthreads();
+  if ((int)threadIdx.x >= nd && (int)threadIdx.x < k) out_draft[(int64_t)b * k + threadIdx.x] = -1;
+  if (threadIdx.x == 0) {
+    out_nd[b] = nd;
+    keys[b] = 0ull;  // ready for the next step
+  }
+}
+
+}  // namespace sr
+
+extern "C" int sr_pooled_ngram_propose(int batch, const int32_t* tokens, int64_t stride, const int32_t* lens,
+                                       int min_n, int max_n, int k, int32_t* out_draft, int32_t* out_ndraft,
+                                       int64_t* scratch, sr_stream_t stream) {
+  SR_REQUIRE(batch >= 0, "negative batch");
+  if (batch == 0) return SR_OK;
+  SR_REQUIRE(min_n >= 1 && max_n >= min_n && max_n <= sr::kMaxNgram, "need 1 <= min_n <= max_n <= 16");
+  SR_REQUIRE(k >= 1 && k <= sr::kNgramThreads, "k out of [1, 256]");
+  SR_REQUIRE(stride >= 1 && stride < (int64_t)1 << 31, "stride out of range");
+  SR_REQUIRE(tokens && lens && out_draft && out_ndraft && scratch, "null pointer");
+  SR_REQUIRE(batch <= 65535, "batch exceeds the 16-bit row rank of the match key");
+  auto* keys = reinterpret_cast<unsigned long long*>(scratch);
+  cudaStream_t st = (cudaStream_t)stream;
+  sr::launch_k(sr::pooled_match_kernel, dim3(batch, batch), sr::kNgramThreads, 0, st, batch, tokens, stride, lens,
+               min_n, max_n, keys);
+  int rc = sr::check_launch("pooled_match_kernel");
+  if (rc) return rc;
+  sr::launch_k(sr::pooled_emit_kernel, batch, k < 32 ? 32 : k, 0, st, batch, tokens, stride, lens, min_n, k,
+               out_draft, out_ndraft, keys);
+  return sr::check_launch("pooled_emit_kernel");
+}

@@ -38,6 +38,18 @@ class NgramDrafter:
     name: str = "ngram"
 
 
+@dataclass(frozen=True)
+class PooledNgramDrafter:
+    """Prompt lookup over the whole batch (``sr_pooled_ngram_propose``): the
+    request's own context first, then the other requests' committed tokens
+    (RL groups sample one prompt several times).  Equals :class:`NgramDrafter`
+    for a single request."""
+
+    min_n: int = 1
+    max_n: int = 3
+    name: str = "pooled-ngram"
+
+
 class SyntheticDrafter:
     """Drafter whose acceptance follows the reference's keyed Bernoulli law.
 
@@ -347,10 +359,11 @@ class RolloutEngine:
                         d.vocab or self.m.s.vocab, self.drafts[n].data_ptr(), self.ndraft[n].data_ptr(), st),
                         "sr_synthetic_draft")
                     continue
-                _native.check(lib.sr_ngram_propose(
+                propose = lib.sr_pooled_ngram_propose if isinstance(d, PooledNgramDrafter) else lib.sr_ngram_propose
+                _native.check(propose(
                     self.B, self.tokens.data_ptr(), self.stride, self.seq_len.data_ptr(), d.min_n, d.max_n,
                     self.k, self.drafts[n].data_ptr(), self.ndraft[n].data_ptr(),
-                    self.ngram_scratch.data_ptr(), st), "sr_ngram_propose")
+                    self.ngram_scratch.data_ptr(), st), "ngram propose")
             for side in forks:
                 cur.wait_stream(side)
             drafts_ptr, nd_ptr = self.drafts.data_ptr(), self.ndraft.data_ptr()
